@@ -1,0 +1,338 @@
+"""Throughput benchmark: full 5-iteration SLIC at 640x480, K=1200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+One "step" segments a batch of B synthetic 640x480 frames (the reference's
+generator: np.random.default_rng(i).integers(0, 256, (480, 640, 3), uint8))
+through the whole pipeline -- convert, init, association x6, update x5, weak
+connectivity x2 -- with m=10, LAB, tile_len 16 (S=16, 30x40 clusters).
+Frames are sharded across ranks with no collective (weak scaling: B frames
+per GPU per step).  Time is measured with CUDA events on the launching
+stream, bracketed by barrier + synchronize, max over ranks.
+
+The JSON line carries: value (frames/s, whole job, inputs resident in HBM),
+e2e (same metric through the C ABI host-buffer call, H2D + D2H inside the
+timed region), roofline (association kernel: algorithmic bytes / measured
+pass time vs MEASURED_PEAKS.json), cpu_baseline (the reference itself on the
+host cores, rank 0 at N=1), clocks sampled during the timed region.
+
+--impl reference runs the unmodified reference (oracle/_ref, its SegEngine
+with the thread-pool backend on all host cores) on the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+W, H, K_SPX, ITERS, M = 640, 480, 1200, 5, 10.0
+METRIC = "frames/s and Mpix/s at 640x480 K~1200 5 iters (1/2/4/8 B200); %HBM roofline"
+
+
+def synthetic_frames(first, count):
+    return np.stack([np.random.default_rng(first + i).integers(0, 256, (H, W, 3), dtype=np.uint8)
+                     for i in range(count)])
+
+
+def algorithmic_bytes(n_px, k, iters):
+    """B = 15N + (I+1)(16N+40K) + I(16N+48K) + 16N + 40K per frame."""
+    return 15 * n_px + (iters + 1) * (16 * n_px + 40 * k) + iters * (16 * n_px + 48 * k) + 16 * n_px + 40 * k
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def reference_package():
+    import oracle
+    return oracle.reference_package()
+
+
+def cpu_reference_rate(seconds, max_frames):
+    """Reference SegEngine (thread pool, all host cores) on C1 frames; frames/s."""
+    sp = reference_package()
+    if sp is None:
+        return None
+    cores = os.cpu_count() or 1
+    st = sp.Settings(img_width=W, img_height=H, num_superpixels=K_SPX, compactness=M,
+                     no_iters=ITERS)
+    eng = sp.SegEngine(st, backend="par", workers=cores)
+    eng.perform_segmentation(sp.ImageRGB(synthetic_frames(0, 1)[0]))  # warm-up (cli.py:171-178)
+    n = 0
+    t0 = time.perf_counter()
+    busy = 0.0
+    while n < max_frames and (time.perf_counter() - t0) < seconds:
+        img = sp.ImageRGB(synthetic_frames(n, 1)[0])
+        busy += eng.perform_segmentation(img).timing.total
+        n += 1
+    return {"value": n / busy, "unit": "frames/s", "cores": cores, "kind": "reference",
+            "sample": f"{n} synthetic 640x480 frames (seeds 0..{n - 1}), reference SegEngine "
+                      f"backend=par workers={cores}, sum of timing.total (cli.py _timed_runs method)"}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return 0
+    sp = reference_package()
+    if sp is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    cores = os.cpu_count() or 1
+    st = sp.Settings(img_width=W, img_height=H, num_superpixels=K_SPX, compactness=M,
+                     no_iters=ITERS)
+    eng = sp.SegEngine(st, backend="par", workers=cores)
+    per_step = args.ref_frames
+    frames = [sp.ImageRGB(f) for f in synthetic_frames(0, per_step)]
+    for _ in range(args.warmup):
+        eng.perform_segmentation(frames[0])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        for f in frames:
+            eng.perform_segmentation(f)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = per_step * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C1: 640x480 RGB, K=1200 (S=16), m=10, 5 iters, LAB, weak conn",
+                   "frames_per_step": per_step, "backend": f"reference par x{cores}"},
+        "mpix_per_s": value * W * H / 1e6,
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "reference",
+                         "sample": f"{per_step} frames per step x {args.steps} steps"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1509_04232_b200 as spx
+
+    world, rank, local = dist_setup()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    B = args.batch
+    st = spx.Settings(img_width=W, img_height=H, num_superpixels=K_SPX, compactness=M,
+                      no_iters=ITERS)
+    grid = spx.compute_grid(st)
+    K = grid.num_clusters
+    eng = spx.SegEngine(st, device=dev, max_batch=B)
+    # Shard: rank r owns frames [r*B, (r+1)*B) of the global batch (no collective).
+    host = synthetic_frames(rank * B, B)
+    rgb = torch.from_numpy(host).to(dev)
+    outs = eng.allocate_outputs(B)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        eng.segment_device(rgb, outs)
+    torch.cuda.synchronize()
+
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    assoc_ms, update_ms = [], []
+    launches = 0
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            eng.segment_device(rgb, outs)
+            launches += eng.last_launches()
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = start.elapsed_time(end)
+    tm = eng.last_timing()  # stage times of the last timed step (device events)
+    assoc_ms = [t * 1e3 for t in tm.associate]
+    update_ms = [t * 1e3 for t in tm.update]
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    frames_total = B * world * args.steps
+    value = frames_total / (ms / 1e3)
+
+    # ---- end to end through the C ABI host-buffer call (pinned buffers) ----
+    pin_rgb = torch.from_numpy(host).pin_memory().numpy()
+    pin_labels = torch.empty((B, H, W), dtype=torch.int32).pin_memory().numpy()
+    pin_xy = torch.empty((B, K, 2), dtype=torch.float64).pin_memory().numpy()
+    pin_lab = torch.empty((B, K, 3), dtype=torch.float64).pin_memory().numpy()
+    pin_cnt = torch.empty((B, K), dtype=torch.int64).pin_memory().numpy()
+    pin_pass = torch.empty((B,), dtype=torch.int32).pin_memory().numpy()
+    e2e_steps = max(1, min(args.steps, 5))
+    eng.segment_host(pin_rgb, pin_labels, pin_xy, pin_lab, pin_cnt, pin_pass)  # warm staging
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        eng.segment_host(pin_rgb, pin_labels, pin_xy, pin_lab, pin_cnt, pin_pass)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = B * world * e2e_steps / e2e_s
+    h2d = B * H * W * 3
+    d2h = B * (H * W * 4 + K * (16 + 24 + 8) + 4)
+
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        n_px = B * H * W
+        assoc_bytes = 16 * n_px + 40 * K * B          # per pass, SURVEY §8(d)
+        upd_bytes = 16 * n_px + 48 * K * B
+        assoc_mean = statistics.mean(assoc_ms)
+        achieved = assoc_bytes / (assoc_mean / 1e3) / 1e9
+        traffic = None
+        prof = os.path.join(REPO, "profiles", "ncu_assoc_traffic.json")
+        if os.path.exists(prof):
+            try:
+                with open(prof) as fh:
+                    pt = json.load(fh)
+                traffic = pt.get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        frame_bytes = algorithmic_bytes(H * W, K, ITERS)
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            cpu = cpu_reference_rate(args.cpu_seconds, args.cpu_frames)
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "C1: 640x480 RGB, K=1200 (S=16, 30x40 grid), m=10, 5 iters, "
+                                   "LAB, weak connectivity",
+                       "frames_per_gpu_per_step": B, "global_batch": B * world,
+                       "parallelism": f"frame-sharded x{world} (no collective)",
+                       "l2": f"inputs > L2: {h2d / 1e6:.0f} MB RGB + {n_px * 12 / 1e6:.0f} MB Lab "
+                             f"per GPU per step"},
+            "mpix_per_s": value * H * W / 1e6,
+            "frame_roofline": {"bytes_per_frame": frame_bytes,
+                               "achieved_gbs": value / world * frame_bytes / 1e9,
+                               "frac": value / world * frame_bytes / 1e9 / peak},
+            "roofline": {"kernel": "k_assoc (association pass)", "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "bytes_per_launch": assoc_bytes, "mean_pass_ms": assoc_mean,
+                         "update_pass_ms": statistics.mean(update_ms) if update_ms else None,
+                         "update_frac": (upd_bytes / (statistics.mean(update_ms) / 1e3) / 1e9 / peak)
+                         if update_ms else None,
+                         "stage_ms": {"convert": tm.convert * 1e3, "init": tm.init * 1e3,
+                                      "associate": assoc_ms, "update": update_ms,
+                                      "connectivity": tm.connectivity * 1e3,
+                                      "total": tm.total * 1e3}},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    "path": "spx_engine_segment_host (C ABI, pinned host buffers)"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=256, help="frames per GPU per step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-frames", type=int, default=8, help="reference arm: frames per step")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-frames", type=int, default=400)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

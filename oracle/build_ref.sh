@@ -20,6 +20,11 @@ if [ ! -d "$SRC" ]; then
   exit 0
 fi
 PY=${PYTHON:-python3}
+SUFFIX=$("$PY" -c "import sysconfig; print(sysconfig.get_config_var('EXT_SUFFIX'))")
+if [ -f "$OUT/superpix/kernels/_core$SUFFIX" ] && [ "$OUT/superpix/kernels/_core$SUFFIX" -nt "$SRC/kernels/_core.pyx" ] && [ "${FORCE:-0}" = "0" ]; then
+  echo "build_ref: up to date" >&2
+  exit 0
+fi
 rm -rf "$OUT"
 mkdir -p "$OUT/build"
 cp -r "$SRC" "$OUT/superpix"
@@ -29,7 +34,6 @@ find "$OUT/superpix" -name '__pycache__' -prune -exec rm -rf {} +
   -o "$OUT/build/_core.c" "$OUT/superpix/kernels/_core.pyx"
 PYINC=$("$PY" -c "import sysconfig; print(sysconfig.get_paths()['include'])")
 NPINC=$("$PY" -c "import numpy; print(numpy.get_include())")
-SUFFIX=$("$PY" -c "import sysconfig; print(sysconfig.get_config_var('EXT_SUFFIX'))")
 gcc -shared -fPIC -O3 -ffp-contract=off -DNPY_NO_DEPRECATED_API=NPY_1_7_API_VERSION \
   -I"$PYINC" -I"$NPINC" "$OUT/build/_core.c" -o "$OUT/superpix/kernels/_core$SUFFIX" -lm
 echo "build_ref: built $OUT/superpix/kernels/_core$SUFFIX"

@@ -1,0 +1,191 @@
+// convert.cu -- RGB -> {RGB, XYZ, CIELAB} float32, bit-exact with
+// _core.pyx:45-83 (convert_band).
+//
+// Layout: rgb uint8 HWC, out float32 HWC (the reference layouts).  One thread
+// converts a group of 4 consecutive pixels: 12 input bytes as three 32-bit
+// loads, 48 output bytes as three 128-bit stores (coalesced, vectorised).
+// The 256-entry linearisation LUT is staged in shared memory (divergent
+// gathers would serialise in the constant cache); the matrix, white point and
+// cbrt constants are warp-uniform and live in __constant__.
+//
+// Roofline: 15 algorithmic bytes per pixel (3 in + 12 out).  The binary64
+// arithmetic (three glibc-cbrt evaluations with a division each, three
+// divisions by the white point) makes this kernel FP64-pipe bound on B200;
+// see DESIGN.md.
+#include "spx_internal.cuh"
+
+namespace spx {
+
+__constant__ double c_m[9];
+__constant__ double c_white[3];
+__constant__ double c_eps;
+__constant__ double c_kappa;
+__constant__ double c_factor[5];
+__device__ double g_lut[256];
+
+static bool g_uploaded = false;
+
+int upload_tables() {
+  if (g_uploaded) return SPX_OK;
+  const ColorTables& t = host_tables();
+  SPX_CUDA(cudaMemcpyToSymbol(c_m, t.m, sizeof t.m));
+  SPX_CUDA(cudaMemcpyToSymbol(c_white, t.white, sizeof t.white));
+  SPX_CUDA(cudaMemcpyToSymbol(c_eps, &t.eps, sizeof t.eps));
+  SPX_CUDA(cudaMemcpyToSymbol(c_kappa, &t.kappa, sizeof t.kappa));
+  SPX_CUDA(cudaMemcpyToSymbol(c_factor, t.cbrt_factor, sizeof t.cbrt_factor));
+  SPX_CUDA(cudaMemcpyToSymbol(g_lut, t.lut, sizeof t.lut));
+  g_uploaded = true;
+  return SPX_OK;
+}
+
+// glibc sysdeps/ieee754/dbl-64/s_cbrt.c restated with explicit round-to-
+// nearest operations (no FMA), for x > 0 (the only inputs convert produces:
+// t > 216/24389).  Cross-checked against libm by the oracle tests.
+__device__ __forceinline__ double cbrt_glibc(double x) {
+  long long bits = __double_as_longlong(x);
+  int bexp = (int)((bits >> 52) & 0x7ff);
+  int xe;
+  double xm;
+  if (bexp != 0 && bexp != 0x7ff) {
+    xe = bexp - 1022;  // frexp: x = xm * 2^xe, xm in [0.5, 1)
+    xm = __longlong_as_double((bits & 0x800FFFFFFFFFFFFFLL) | (1022LL << 52));
+    xm = fabs(xm);
+  } else {
+    xm = frexp(fabs(x), &xe);
+    if (xe == 0 && (x == 0.0 || isinf(x) || isnan(x))) return x + x;
+  }
+  double p = dsub(0.784932344976639262, dmul(0.145263899385486377, xm));
+  p = dadd(-1.83469277483613086, dmul(p, xm));
+  p = dadd(2.44693122563534430, dmul(p, xm));
+  p = dadd(-2.11499494167371287, dmul(p, xm));
+  p = dadd(1.50819193781584896, dmul(p, xm));
+  double u = dadd(0.354895765043919860, dmul(p, xm));
+  double t2 = dmul(dmul(u, u), u);
+  double ym = dmul(ddiv(dmul(u, dadd(t2, dmul(2.0, xm))), dadd(dmul(2.0, t2), xm)),
+                   c_factor[2 + xe % 3]);
+  if (x < 0.0) ym = -ym;
+  int n = xe / 3;
+  if (n >= -1000 && n <= 1000) {
+    // ldexp by an exact power of two; ym is in [0.5, 1.6] so the product
+    // stays normal for every input convert can produce.
+    double r = dmul(ym, __longlong_as_double((long long)(1023 + n) << 52));
+    if (fabs(r) >= 2.2250738585072014e-308) return r;
+  }
+  return ldexp(ym, n);
+}
+
+__device__ __forceinline__ double lab_f(double t) {
+  // _core.pyx:73-75
+  return t > c_eps ? cbrt_glibc(t) : ddiv(dadd(dmul(c_kappa, t), 16.0), 116.0);
+}
+
+template <int SPACE>
+__device__ __forceinline__ void convert_px(const double* lut, uint32_t R, uint32_t G, uint32_t B,
+                                           float& o0, float& o1, float& o2) {
+  if (SPACE == 0) {
+    o0 = __double2float_rn(ddiv((double)R, 255.0));
+    o1 = __double2float_rn(ddiv((double)G, 255.0));
+    o2 = __double2float_rn(ddiv((double)B, 255.0));
+    return;
+  }
+  double r = lut[R], g = lut[G], b = lut[B];
+  double cx = dadd(dadd(dmul(c_m[0], r), dmul(c_m[1], g)), dmul(c_m[2], b));
+  double cy = dadd(dadd(dmul(c_m[3], r), dmul(c_m[4], g)), dmul(c_m[5], b));
+  double cz = dadd(dadd(dmul(c_m[6], r), dmul(c_m[7], g)), dmul(c_m[8], b));
+  if (SPACE == 1) {
+    o0 = __double2float_rn(cx);
+    o1 = __double2float_rn(cy);
+    o2 = __double2float_rn(cz);
+    return;
+  }
+  double fx = lab_f(ddiv(cx, c_white[0]));
+  double fy = lab_f(ddiv(cy, c_white[1]));
+  double fz = lab_f(ddiv(cz, c_white[2]));
+  double light = dsub(dmul(116.0, fy), 16.0);
+  if (light < 0.0) light = 0.0;
+  if (light > 100.0) light = 100.0;
+  o0 = __double2float_rn(light);
+  o1 = __double2float_rn(dmul(500.0, dsub(fx, fy)));
+  o2 = __double2float_rn(dmul(200.0, dsub(fy, fz)));
+}
+
+// Pixels [p0, p1) of a flat HWC raster (frames of a batch are contiguous, so
+// a batch is one range).  `vec` requires rgb 4-byte and out 16-byte aligned.
+template <int SPACE>
+__global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb,
+                                                 float* __restrict__ out, int64_t p0,
+                                                 int64_t p1, int vec) {
+  __shared__ double lut[256];
+  if (SPACE != 0) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = g_lut[i];
+    __syncthreads();
+  }
+  int64_t g0 = p0 >> 2, g1 = (p1 + 3) >> 2;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t g = g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < g1; g += stride) {
+    int64_t q = g << 2;
+    if (vec && q >= p0 && q + 4 <= p1) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(rgb + q * 3);
+      uint32_t w0 = __ldg(src), w1 = __ldg(src + 1), w2 = __ldg(src + 2);
+      uint8_t c[12];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        c[i] = (w0 >> (8 * i)) & 255;
+        c[4 + i] = (w1 >> (8 * i)) & 255;
+        c[8 + i] = (w2 >> (8 * i)) & 255;
+      }
+      float o[12];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        convert_px<SPACE>(lut, c[3 * i], c[3 * i + 1], c[3 * i + 2], o[3 * i], o[3 * i + 1],
+                          o[3 * i + 2]);
+      float4* dst = reinterpret_cast<float4*>(out + q * 3);
+      dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+      dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+      dst[2] = make_float4(o[8], o[9], o[10], o[11]);
+    } else {
+      for (int64_t p = q; p < q + 4; ++p) {
+        if (p < p0 || p >= p1) continue;
+        float o0, o1, o2;
+        convert_px<SPACE>(lut, rgb[p * 3], rgb[p * 3 + 1], rgb[p * 3 + 2], o0, o1, o2);
+        out[p * 3] = o0;
+        out[p * 3 + 1] = o1;
+        out[p * 3 + 2] = o2;
+      }
+    }
+  }
+}
+
+int launch_convert(const uint8_t* rgb, float* out, int64_t p0, int64_t p1, int space,
+                   cudaStream_t st) {
+  if (p1 <= p0) return SPX_OK;
+  int rc = upload_tables();
+  if (rc) return rc;
+  int vec = ((uintptr_t)rgb % 4 == 0) && ((uintptr_t)out % 16 == 0);
+  int64_t groups = ((p1 + 3) >> 2) - (p0 >> 2);
+  int64_t blocks = ceil_div(groups, 256);
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  switch (space) {
+    case 0: k_convert<0><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec); break;
+    case 1: k_convert<1><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec); break;
+    case 2: k_convert<2><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec); break;
+    default:
+      set_error("unknown colour space %d", space);
+      return SPX_ERR_VALUE;
+  }
+  SPX_LAUNCH_CHECK("k_convert");
+  return SPX_OK;
+}
+
+}  // namespace spx
+
+extern "C" int32_t spx_convert_band(const uint8_t* rgb, float* out, int64_t h, int64_t w,
+                                    int32_t space, int64_t y0, int64_t y1, void* stream) {
+  if (h < 0 || w < 0 || y0 < 0 || y1 > h) {
+    spx::set_error("convert_band: rows [%lld,%lld) outside image of height %lld",
+                   (long long)y0, (long long)y1, (long long)h);
+    return SPX_ERR_DIMENSION;
+  }
+  return spx::launch_convert(rgb, out, y0 * w, y1 * w, space, spx::as_stream(stream));
+}

@@ -1,0 +1,356 @@
+// engine.cu -- the native SegEngine: buffers, stage sequence, timing.
+//
+// Mirrors SegEngine.perform_segmentation (engine.py:125-230) for a batch of
+// same-sized frames: every stage is ONE launch over the whole batch, buffers
+// are allocated once per engine (engine.py:110-119) and stay resident in HBM,
+// and stage boundaries are CUDA events instead of perf_counter calls.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "spx_internal.cuh"
+
+namespace spx {
+int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t);
+int launch_init(const float*, int64_t, int64_t, int64_t, int64_t, double*, double*, int64_t,
+                int64_t, int64_t, int, int, int, cudaStream_t);
+int launch_assoc(const float*, const double*, const double*, int32_t*, const int32_t*, int64_t,
+                 int64_t, int64_t, int64_t, int64_t, double, int64_t, int64_t, int, int64_t,
+                 cudaStream_t);
+int launch_accum_range(const float*, const int32_t*, int64_t, int64_t, double*, int64_t, int64_t,
+                       int64_t, int64_t, int64_t, int64_t, int64_t, int, const int32_t*,
+                       cudaStream_t);
+int launch_reduce(double*, int64_t, const double*, const double*, double*, double*, int64_t*,
+                  int64_t, int64_t, int64_t, int, const int32_t*, cudaStream_t);
+int launch_shift(const double*, const double*, int64_t, int, double*, int32_t*, int32_t*, double,
+                 cudaStream_t);
+int launch_commit_done(int32_t*, int, cudaStream_t);
+int launch_weak2(const int32_t*, int32_t*, int64_t, int64_t, int, cudaStream_t);
+int launch_strict(const int32_t*, int32_t*, int64_t, int64_t, int, int64_t, int64_t, int32_t*,
+                  int32_t*, int32_t*, int32_t*, cudaStream_t);
+
+namespace {
+
+__global__ void k_gather_centres(const double* __restrict__ xy0, const double* __restrict__ lab0,
+                                 const double* __restrict__ xy1, const double* __restrict__ lab1,
+                                 const int32_t* __restrict__ passes, int64_t k, int frames,
+                                 double* __restrict__ out_xy, double* __restrict__ out_lab) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k * frames) return;
+  int64_t f = i / k;
+  bool one = passes && (passes[f] & 1);
+  const double* sx = one ? xy1 : xy0;
+  const double* sl = one ? lab1 : lab0;
+  out_xy[2 * i] = sx[2 * i];
+  out_xy[2 * i + 1] = sx[2 * i + 1];
+  out_lab[3 * i] = sl[3 * i];
+  out_lab[3 * i + 1] = sl[3 * i + 1];
+  out_lab[3 * i + 2] = sl[3 * i + 2];
+}
+
+enum Ev { EV_START, EV_CONVERT, EV_INIT, EV_PERTURB, EV_CONN0, EV_END, EV_FIXED };
+
+}  // namespace
+
+struct Engine {
+  spx_settings st;
+  int64_t K = 0, n_bl = 0, hw = 0, max_batch = 0;
+  int device = 0;
+  double xy_weight = 0.0;
+  float* lab = nullptr;
+  int32_t* labels = nullptr;
+  int32_t* scratch = nullptr;
+  double* cxy[2] = {nullptr, nullptr};
+  double* clab[2] = {nullptr, nullptr};
+  double* slab = nullptr;
+  int32_t* done = nullptr;
+  int32_t* passes = nullptr;
+  int32_t *cc_parent = nullptr, *cc_size = nullptr, *cc_nxt = nullptr, *cc_first = nullptr;
+  uint8_t* d_rgb = nullptr;  // staging for the host-buffer entry point
+  int32_t* d_labels = nullptr;
+  double *d_cxy = nullptr, *d_clab = nullptr;
+  int64_t* d_counts = nullptr;
+  int32_t* d_passes = nullptr;
+  cudaStream_t own_stream = nullptr;
+  cudaEvent_t ev[EV_FIXED] = {};
+  std::vector<cudaEvent_t> ev_assoc, ev_update;  // start/end pairs
+  int n_assoc = 0, n_update = 0;
+  int64_t launches = 0;
+
+  ~Engine() {
+    cudaSetDevice(device);
+    for (void* p : {(void*)lab, (void*)labels, (void*)scratch, (void*)cxy[0], (void*)cxy[1],
+                    (void*)clab[0], (void*)clab[1], (void*)slab, (void*)done, (void*)passes,
+                    (void*)cc_parent, (void*)cc_size, (void*)cc_nxt, (void*)cc_first,
+                    (void*)d_rgb, (void*)d_labels, (void*)d_cxy, (void*)d_clab, (void*)d_counts,
+                    (void*)d_passes})
+      if (p) cudaFree(p);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto e : ev_assoc) cudaEventDestroy(e);
+    for (auto e : ev_update) cudaEventDestroy(e);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+
+  int init(const spx_settings& s, int64_t mb, int dev) {
+    st = s;
+    device = dev;
+    max_batch = mb;
+    SPX_CUDA(cudaSetDevice(dev));
+    int major = 0;
+    SPX_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major < 10) {
+      set_error("device %d has compute capability %d.x; this build targets sm_100a", dev, major);
+      return SPX_ERR_CUDA;
+    }
+    K = st.ns_r * st.ns_c;
+    n_bl = ceil_div(3 * st.s, st.tile_len);
+    hw = st.width * st.height;
+    xy_weight = st.compactness / (double)st.s;  // engine.py:143
+    size_t B = (size_t)mb;
+    SPX_CUDA(cudaMalloc(&lab, B * hw * 3 * sizeof(float)));
+    SPX_CUDA(cudaMalloc(&labels, B * hw * sizeof(int32_t)));
+    SPX_CUDA(cudaMalloc(&scratch, B * hw * sizeof(int32_t)));
+    for (int i = 0; i < 2; ++i) {
+      SPX_CUDA(cudaMalloc(&cxy[i], B * K * 2 * sizeof(double)));
+      SPX_CUDA(cudaMalloc(&clab[i], B * K * 3 * sizeof(double)));
+      SPX_CUDA(cudaMemset(cxy[i], 0, B * K * 2 * sizeof(double)));
+      SPX_CUDA(cudaMemset(clab[i], 0, B * K * 3 * sizeof(double)));
+    }
+    SPX_CUDA(cudaMalloc(&slab, B * K * n_bl * 6 * sizeof(double)));
+    SPX_CUDA(cudaMalloc(&done, B * sizeof(int32_t)));
+    SPX_CUDA(cudaMalloc(&passes, B * sizeof(int32_t)));
+    if (st.connectivity == 2) {
+      SPX_CUDA(cudaMalloc(&cc_parent, B * hw * sizeof(int32_t)));
+      SPX_CUDA(cudaMalloc(&cc_size, B * hw * sizeof(int32_t)));
+      SPX_CUDA(cudaMalloc(&cc_nxt, B * hw * sizeof(int32_t)));
+      SPX_CUDA(cudaMalloc(&cc_first, B * K * sizeof(int32_t)));
+    }
+    for (auto& e : ev) SPX_CUDA(cudaEventCreate(&e));
+    return SPX_OK;
+  }
+
+  cudaEvent_t pass_event(std::vector<cudaEvent_t>& v, size_t i) {
+    while (v.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      v.push_back(e);
+    }
+    return v[i];
+  }
+
+  int associate(int cur, int frames, const int32_t* dn, cudaStream_t s) {
+    cudaEventRecord(pass_event(ev_assoc, 2 * n_assoc), s);
+    int rc = launch_assoc(lab, cxy[cur], clab[cur], labels, dn, st.height, st.width, st.s,
+                          st.ns_r, st.ns_c, xy_weight, 0, st.height, frames, K, s);
+    cudaEventRecord(pass_event(ev_assoc, 2 * n_assoc + 1), s);
+    ++n_assoc;
+    ++launches;
+    return rc;
+  }
+
+  int segment(const uint8_t* rgb, int64_t batch, int32_t* out_labels, double* out_xy,
+              double* out_lab, int64_t* out_counts, int32_t* out_passes, cudaStream_t s) {
+    if (batch < 1 || batch > max_batch) {
+      set_error("batch %lld outside [1, %lld]", (long long)batch, (long long)max_batch);
+      return SPX_ERR_VALUE;
+    }
+    SPX_CUDA(cudaSetDevice(device));
+    const int B = (int)batch;
+    const bool early = st.early_stop >= 0.0;
+    int rc;
+    n_assoc = n_update = 0;
+    launches = 0;
+    const int32_t* dn = early ? done : nullptr;
+    cudaEventRecord(ev[EV_START], s);
+    if ((rc = launch_convert(rgb, lab, 0, (int64_t)B * hw, st.color_space, s))) return rc;
+    ++launches;
+    cudaEventRecord(ev[EV_CONVERT], s);
+    if ((rc = launch_init(lab, st.height, st.width, st.s, st.ns_c, cxy[0], clab[0], 0, K, K, B, 0,
+                          1, s)))
+      return rc;
+    ++launches;
+    cudaEventRecord(ev[EV_INIT], s);
+    if (st.perturb) {
+      if ((rc = launch_init(lab, st.height, st.width, st.s, st.ns_c, cxy[0], clab[0], 0, K, K, B,
+                            1, 0, s)))
+        return rc;
+      ++launches;
+    }
+    cudaEventRecord(ev[EV_PERTURB], s);
+    SPX_CUDA(cudaMemsetAsync(passes, 0, B * sizeof(int32_t), s));
+    if (early) SPX_CUDA(cudaMemsetAsync(done, 0, B * sizeof(int32_t), s));
+    int cur = 0, nxt = 1;
+    if ((rc = associate(cur, B, dn, s))) return rc;
+    for (int it = 0; it < st.no_iters; ++it) {
+      cudaEventRecord(pass_event(ev_update, 2 * n_update), s);
+      if ((rc = launch_accum_range(lab, labels, st.height, st.width, slab, n_bl, st.s, st.ns_c,
+                                   st.tile_len, 0, K, K, B, dn, s)))
+        return rc;
+      if ((rc = launch_reduce(slab, n_bl, cxy[cur], clab[cur], cxy[nxt], clab[nxt], out_counts, 0,
+                              K, K, B, dn, s)))
+        return rc;
+      launches += 2;
+      cudaEventRecord(pass_event(ev_update, 2 * n_update + 1), s);
+      ++n_update;
+      // shift + per-frame pass count (engine.py:196); also flags early stop
+      if ((rc = launch_shift(cxy[nxt], cxy[cur], K, B, nullptr, early ? done : nullptr, passes,
+                             early ? st.early_stop : -1.0, s)))
+        return rc;
+      ++launches;
+      std::swap(cur, nxt);
+      if ((rc = associate(cur, B, dn, s))) return rc;
+      if (early) {
+        if ((rc = launch_commit_done(done, B, s))) return rc;
+        ++launches;
+      }
+    }
+    cudaEventRecord(ev[EV_CONN0], s);
+    if (st.connectivity == 1) {
+      if ((rc = launch_weak2(labels, out_labels, st.height, st.width, B, s))) return rc;
+      ++launches;
+    } else if (st.connectivity == 2) {
+      if ((rc = launch_strict(labels, out_labels, st.height, st.width, B, K, st.min_size,
+                              cc_parent, cc_size, cc_nxt, cc_first, s)))
+        return rc;
+      launches += 8;
+    } else {
+      SPX_CUDA(cudaMemcpyAsync(out_labels, labels, (size_t)B * hw * sizeof(int32_t),
+                               cudaMemcpyDeviceToDevice, s));
+    }
+    cudaEventRecord(ev[EV_END], s);
+    // Final centres: frame f ends in buffer passes[f] & 1 (ping-pong, engine.py:197).
+    k_gather_centres<<<(unsigned)ceil_div(K * B, 256), 256, 0, s>>>(
+        cxy[0], clab[0], cxy[1], clab[1], passes, K, B, out_xy, out_lab);
+    SPX_LAUNCH_CHECK("k_gather_centres");
+    ++launches;
+    if (out_passes)
+      SPX_CUDA(cudaMemcpyAsync(out_passes, passes, B * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                               s));
+    return SPX_OK;
+  }
+
+  int timing(spx_timing* t) {
+    SPX_CUDA(cudaSetDevice(device));
+    SPX_CUDA(cudaEventSynchronize(ev[EV_END]));
+    std::memset(t, 0, sizeof *t);
+    auto el = [](cudaEvent_t a, cudaEvent_t b) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, a, b);
+      return ms;
+    };
+    t->convert = el(ev[EV_START], ev[EV_CONVERT]);
+    t->init = el(ev[EV_CONVERT], ev[EV_INIT]);
+    t->perturb = el(ev[EV_INIT], ev[EV_PERTURB]);
+    t->connectivity = el(ev[EV_CONN0], ev[EV_END]);
+    t->total = el(ev[EV_START], ev[EV_END]);
+    t->n_associate = std::min(n_assoc, 1024);
+    t->n_update = std::min(n_update, 1024);
+    for (int i = 0; i < t->n_associate; ++i) t->associate[i] = el(ev_assoc[2 * i], ev_assoc[2 * i + 1]);
+    for (int i = 0; i < t->n_update; ++i) t->update[i] = el(ev_update[2 * i], ev_update[2 * i + 1]);
+    return SPX_OK;
+  }
+
+  int ensure_staging() {
+    if (d_rgb) return SPX_OK;
+    size_t B = (size_t)max_batch;
+    SPX_CUDA(cudaMalloc(&d_rgb, B * hw * 3));
+    SPX_CUDA(cudaMalloc(&d_labels, B * hw * sizeof(int32_t)));
+    SPX_CUDA(cudaMalloc(&d_cxy, B * K * 2 * sizeof(double)));
+    SPX_CUDA(cudaMalloc(&d_clab, B * K * 3 * sizeof(double)));
+    SPX_CUDA(cudaMalloc(&d_counts, B * K * sizeof(int64_t)));
+    SPX_CUDA(cudaMalloc(&d_passes, B * sizeof(int32_t)));
+    SPX_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+    return SPX_OK;
+  }
+
+  int segment_host(const uint8_t* rgb, int64_t batch, int32_t* out_labels, double* out_xy,
+                   double* out_lab, int64_t* out_counts, int32_t* out_passes) {
+    SPX_CUDA(cudaSetDevice(device));
+    int rc = ensure_staging();
+    if (rc) return rc;
+    if (batch < 1 || batch > max_batch) {
+      set_error("batch %lld outside [1, %lld]", (long long)batch, (long long)max_batch);
+      return SPX_ERR_VALUE;
+    }
+    cudaStream_t s = own_stream;
+    size_t B = (size_t)batch;
+    SPX_CUDA(cudaMemcpyAsync(d_rgb, rgb, B * hw * 3, cudaMemcpyHostToDevice, s));
+    if ((rc = segment(d_rgb, batch, d_labels, d_cxy, d_clab, d_counts, d_passes, s))) return rc;
+    if (out_labels)
+      SPX_CUDA(cudaMemcpyAsync(out_labels, d_labels, B * hw * 4, cudaMemcpyDeviceToHost, s));
+    if (out_xy) SPX_CUDA(cudaMemcpyAsync(out_xy, d_cxy, B * K * 16, cudaMemcpyDeviceToHost, s));
+    if (out_lab) SPX_CUDA(cudaMemcpyAsync(out_lab, d_clab, B * K * 24, cudaMemcpyDeviceToHost, s));
+    if (out_counts)
+      SPX_CUDA(cudaMemcpyAsync(out_counts, d_counts, B * K * 8, cudaMemcpyDeviceToHost, s));
+    if (out_passes)
+      SPX_CUDA(cudaMemcpyAsync(out_passes, d_passes, B * 4, cudaMemcpyDeviceToHost, s));
+    SPX_CUDA(cudaStreamSynchronize(s));
+    return SPX_OK;
+  }
+};
+
+}  // namespace spx
+
+struct spx_engine {
+  spx::Engine e;
+};
+
+extern "C" {
+
+int32_t spx_engine_create(const spx_settings* st, int64_t max_batch, int32_t device,
+                          spx_engine** out) {
+  using namespace spx;
+  *out = nullptr;
+  if (!st || st->width < 1 || st->height < 1 || st->s < 1 || st->ns_r < 1 || st->ns_c < 1 ||
+      st->no_iters < 1 || st->tile_len < 1 || !(st->compactness > 0) || st->min_size < 1) {
+    set_error("invalid engine settings");
+    return SPX_ERR_INVALID_SETTINGS;
+  }
+  if ((st->height - 1) / st->s >= st->ns_r || (st->width - 1) / st->s >= st->ns_c) {
+    set_error("grid %lldx%lld at s=%lld does not cover %lldx%lld", (long long)st->ns_c,
+              (long long)st->ns_r, (long long)st->s, (long long)st->width, (long long)st->height);
+    return SPX_ERR_INVALID_SETTINGS;
+  }
+  if (st->color_space < 0 || st->color_space > 2 || st->connectivity < 0 || st->connectivity > 2) {
+    set_error("invalid colour space / connectivity code");
+    return SPX_ERR_INVALID_SETTINGS;
+  }
+  if (max_batch < 1 || max_batch > 65535) {
+    set_error("max_batch must be in [1, 65535]");
+    return SPX_ERR_VALUE;
+  }
+  spx_engine* eng = new spx_engine();
+  int rc = eng->e.init(*st, max_batch, device);
+  if (rc) {
+    delete eng;
+    return rc;
+  }
+  *out = eng;
+  return SPX_OK;
+}
+
+int32_t spx_engine_destroy(spx_engine* eng) {
+  delete eng;
+  return SPX_OK;
+}
+
+int32_t spx_engine_segment(spx_engine* eng, const uint8_t* rgb_dev, int64_t batch,
+                           int32_t* labels_dev, double* cxy_dev, double* clab_dev,
+                           int64_t* counts_dev, int32_t* passes_dev, void* stream) {
+  return eng->e.segment(rgb_dev, batch, labels_dev, cxy_dev, clab_dev, counts_dev, passes_dev,
+                        spx::as_stream(stream));
+}
+
+int32_t spx_engine_segment_host(spx_engine* eng, const uint8_t* rgb_host, int64_t batch,
+                                int32_t* labels_host, double* cxy_host, double* clab_host,
+                                int64_t* counts_host, int32_t* passes_host) {
+  return eng->e.segment_host(rgb_host, batch, labels_host, cxy_host, clab_host, counts_host,
+                             passes_host);
+}
+
+int32_t spx_engine_timing(spx_engine* eng, spx_timing* out) { return eng->e.timing(out); }
+
+int64_t spx_engine_last_launches(spx_engine* eng) { return eng->e.launches; }
+
+}  // extern "C"

@@ -1,0 +1,275 @@
+"""GPU segmentation engine with the reference's SegEngine API.
+
+superpix/engine.py runs the stage sequence of engine.py:125-230 from Python,
+calling one CPU kernel per band.  Here the whole sequence -- convert, init,
+optional perturbation, association x(iters+1), update x iters, connectivity
+-- is one call into the native engine (libspx.so, csrc/engine.cu), which
+owns HBM-resident buffers sized at construction and launches each stage once
+over a whole batch of frames.  The Python layer validates, moves frames in
+and results out, and builds the same SegResult / StageTiming objects.
+
+Backends: "cuda" is the native engine.  The reference's "seq" and "par"
+names are accepted as aliases of it (a drop-in caller keeps working and gets
+identical labels, which the reference guarantees across its own backends);
+`workers` is validated as the reference does and otherwise ignored.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, kernels, slic_core
+from .connectivity import default_min_size
+from .errors import DimensionMismatchError, InvalidSettingsError
+from .slic_core import ConnectivityMode, LabelMap, SuperpixelMap
+
+BACKENDS = ("cuda", "seq", "par")
+
+
+def band_bounds(n, workers):
+    """Split [0, n) into `workers` contiguous half-open ranges (engine.py:23-25)."""
+    return [((i * n) // workers, ((i + 1) * n) // workers) for i in range(workers)]
+
+
+@dataclass(frozen=True)
+class StageTiming:
+    """Seconds per stage (device time).  associate/update: one entry per pass."""
+
+    convert: float
+    init: float
+    perturb: float
+    associate: tuple
+    update: tuple
+    connectivity: float
+    total: float
+
+
+@dataclass(frozen=True)
+class SegResult:
+    labels: LabelMap
+    spixel_map: SuperpixelMap
+    timing: StageTiming
+
+
+def _native_settings(settings, grid):
+    conn = 0
+    if settings.do_enforce_connectivity:
+        conn = 1 if settings.connectivity_mode is ConnectivityMode.WEAK else 2
+    min_size = settings.min_size if settings.min_size is not None else default_min_size(grid.s)
+    st = _lib.SpxSettings()
+    st.width, st.height = settings.img_width, settings.img_height
+    st.s, st.ns_r, st.ns_c = grid.s, grid.ns_r, grid.ns_c
+    st.compactness = float(settings.compactness)
+    st.no_iters = int(settings.no_iters)
+    st.color_space = int(settings.color_space.value)
+    st.connectivity = conn
+    st.perturb = int(bool(settings.enable_perturbation))
+    st.tile_len = int(settings.tile_len)
+    st.min_size = int(min_size)
+    st.early_stop = -1.0 if settings.early_stop_threshold is None else float(settings.early_stop_threshold)
+    return st
+
+
+class SegEngine:
+    """Reusable pipeline for frames of one size (engine.py:86-119 API).
+
+    Buffers for up to `max_batch` frames live on `device` for the engine's
+    lifetime.  One engine runs one call at a time; use one engine per thread.
+    """
+
+    def __init__(self, settings, backend="cuda", workers=None, kernel_impl="auto",
+                 device=None, max_batch=1):
+        self.settings = settings
+        self.grid = slic_core.compute_grid(settings)
+        self.kernel = kernels.get_impl(kernel_impl)
+        if backend not in BACKENDS:
+            raise InvalidSettingsError(f"unknown backend {backend!r}")
+        if backend == "par" and workers is not None and workers < 1:
+            raise InvalidSettingsError(f"workers must be >= 1, got {workers}")
+        self.backend_name = backend
+        self._workers = 1 if workers is None else int(workers)
+        import torch  # device plumbing only
+        self._torch = torch
+        if device is None:
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        self.device = int(device)
+        self.max_batch = int(max_batch)
+        lib = _lib.load()
+        self._st = _native_settings(settings, self.grid)
+        handle = ctypes.c_void_p()
+        _lib.check(lib.spx_engine_create(ctypes.byref(self._st), self.max_batch, self.device,
+                                         ctypes.byref(handle)), "SegEngine")
+        self._h = handle
+        self._lib = lib
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                self._lib.spx_engine_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def workers(self):
+        return self._workers
+
+    @property
+    def num_clusters(self):
+        return self.grid.num_clusters
+
+    # ---- device-resident batch API -------------------------------------------------
+
+    def allocate_outputs(self, batch):
+        """Device tensors for `batch` frames of results (labels, cxy, clab, counts, passes)."""
+        t = self._torch
+        dev = t.device("cuda", self.device)
+        st = self.settings
+        k = self.grid.num_clusters
+        return (t.empty((batch, st.img_height, st.img_width), dtype=t.int32, device=dev),
+                t.empty((batch, k, 2), dtype=t.float64, device=dev),
+                t.empty((batch, k, 3), dtype=t.float64, device=dev),
+                t.empty((batch, k), dtype=t.int64, device=dev),
+                t.empty((batch,), dtype=t.int32, device=dev))
+
+    def segment_device(self, rgb, out=None, stream=None):
+        """Segment a CUDA uint8 tensor (B, H, W, 3); asynchronous on `stream`.
+
+        Returns (labels, cxy, clab, counts, passes) device tensors.
+        """
+        t = self._torch
+        st = self.settings
+        if rgb.dim() == 3:
+            rgb = rgb.unsqueeze(0)
+        if (rgb.dtype != t.uint8 or not rgb.is_cuda or not rgb.is_contiguous()
+                or tuple(rgb.shape[1:]) != (st.img_height, st.img_width, 3)):
+            raise DimensionMismatchError(
+                f"frames must be contiguous CUDA uint8 (B, {st.img_height}, {st.img_width}, 3), "
+                f"got {tuple(rgb.shape)} {rgb.dtype}")
+        b = rgb.shape[0]
+        if out is None:
+            out = self.allocate_outputs(b)
+        labels, cxy, clab, counts, passes = out
+        s = stream if stream is not None else t.cuda.current_stream(self.device)
+        _lib.check(self._lib.spx_engine_segment(
+            self._h, ctypes.c_void_p(rgb.data_ptr()), b, ctypes.c_void_p(labels.data_ptr()),
+            ctypes.c_void_p(cxy.data_ptr()), ctypes.c_void_p(clab.data_ptr()),
+            ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(passes.data_ptr()),
+            ctypes.c_void_p(s.cuda_stream)), "segment")
+        return out
+
+    def segment_host(self, rgb, labels=None, cxy=None, clab=None, counts=None, passes=None):
+        """Segment host uint8 frames (B, H, W, 3) through the C ABI's host-buffer call.
+
+        Inputs and outputs are numpy arrays (pinned memory is used as-is).
+        Synchronous.  Returns (labels, cxy, clab, counts, passes).
+        """
+        st = self.settings
+        rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+        if rgb.ndim == 3:
+            rgb = rgb[None]
+        if rgb.shape[1:] != (st.img_height, st.img_width, 3):
+            raise DimensionMismatchError(
+                f"frame is {rgb.shape[2]}x{rgb.shape[1]}, engine expects "
+                f"{st.img_width}x{st.img_height}")
+        b = rgb.shape[0]
+        k = self.grid.num_clusters
+        if labels is None:
+            labels = np.empty((b, st.img_height, st.img_width), dtype=np.int32)
+        if cxy is None:
+            cxy = np.empty((b, k, 2))
+        if clab is None:
+            clab = np.empty((b, k, 3))
+        if counts is None:
+            counts = np.empty((b, k), dtype=np.int64)
+        if passes is None:
+            passes = np.empty(b, dtype=np.int32)
+        p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        _lib.check(self._lib.spx_engine_segment_host(self._h, p(rgb), b, p(labels), p(cxy),
+                                                     p(clab), p(counts), p(passes)), "segment")
+        return labels, cxy, clab, counts, passes
+
+    def last_timing(self):
+        """Per-stage device times (seconds) of the last call, batch-wide."""
+        t = _lib.SpxTiming()
+        _lib.check(self._lib.spx_engine_timing(self._h, ctypes.byref(t)), "timing")
+        ms = 1e-3
+        return StageTiming(convert=t.convert * ms, init=t.init * ms, perturb=t.perturb * ms,
+                           associate=tuple(t.associate[i] * ms for i in range(t.n_associate)),
+                           update=tuple(t.update[i] * ms for i in range(t.n_update)),
+                           connectivity=t.connectivity * ms, total=t.total * ms)
+
+    def last_launches(self):
+        return int(self._lib.spx_engine_last_launches(self._h))
+
+    # ---- reference API ---------------------------------------------------------------
+
+    def _check_frame(self, img):
+        st = self.settings
+        if (img.height, img.width) != (st.img_height, st.img_width):
+            raise DimensionMismatchError(
+                f"frame is {img.width}x{img.height}, engine expects "
+                f"{st.img_width}x{st.img_height}")
+
+    def _results(self, labels, cxy, clab, counts, passes, timing):
+        out = []
+        for i in range(labels.shape[0]):
+            n_up = int(passes[i])
+            tm = StageTiming(timing.convert, timing.init, timing.perturb,
+                             timing.associate[:n_up + 1], timing.update[:n_up],
+                             timing.connectivity, timing.total)
+            out.append(SegResult(labels=LabelMap(labels[i]),
+                                 spixel_map=SuperpixelMap(self.grid, cxy[i], clab[i], counts[i]),
+                                 timing=tm))
+        return out
+
+    def perform_segmentation(self, img):
+        """Run the full pipeline on one ImageRGB frame (engine.py:125-230)."""
+        self._check_frame(img)
+        res = self.segment_host(img.data)
+        return self._results(*res, self.last_timing())[0]
+
+    def perform_segmentation_batch(self, imgs):
+        """Segment a list of same-sized frames in batches of max_batch."""
+        out = []
+        for i, img in enumerate(imgs):
+            try:
+                self._check_frame(img)
+            except DimensionMismatchError as exc:
+                raise DimensionMismatchError(f"frame {i}: {exc}") from None
+        for lo in range(0, len(imgs), self.max_batch):
+            chunk = np.stack([im.data for im in imgs[lo:lo + self.max_batch]])
+            res = self.segment_host(chunk)
+            out.extend(self._results(*res, self.last_timing()))
+        return out
+
+
+def perform_segmentation(engine, img):
+    """Functional form of SegEngine.perform_segmentation."""
+    return engine.perform_segmentation(img)
+
+
+def segment_stream(engine, imgs):
+    """Yield one SegResult per frame, batching up to engine.max_batch frames.
+
+    A frame of the wrong size aborts the stream with DimensionMismatchError
+    naming its index, after the results of the frames before it.
+    """
+    pending = []
+    start = 0
+    for i, img in enumerate(imgs):
+        try:
+            engine._check_frame(img)
+        except DimensionMismatchError as exc:
+            if pending:
+                yield from engine.perform_segmentation_batch(pending)
+            raise DimensionMismatchError(f"frame {i}: {exc}") from None
+        pending.append(img)
+        if len(pending) == engine.max_batch:
+            yield from engine.perform_segmentation_batch(pending)
+            start += len(pending)
+            pending = []
+    if pending:
+        yield from engine.perform_segmentation_batch(pending)

@@ -1,0 +1,163 @@
+"""Whole-pipeline parity: native engine vs the oracle / reference goldens.
+
+Bit-exact labels, centres and counts on the reference's own golden cases
+(tests/golden, produced by the reference SegEngine), on BASELINE's C1/C2
+frames (hashes of the reference outputs), on batches, and through the
+public API entry points.  Runs on a B200 (-m gpu).
+"""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1509_04232_b200 as spx
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def settings_from(w, h, kw):
+    kw = dict(kw)
+    if "connectivity_mode" in kw:
+        kw["connectivity_mode"] = spx.ConnectivityMode.parse(kw["connectivity_mode"])
+    if "color_space" in kw:
+        kw["color_space"] = spx.ColorSpace.parse(kw["color_space"])
+    return spx.Settings(img_width=w, img_height=h, **kw)
+
+
+def test_pipeline_matches_reference_goldens(golden, golden_meta):
+    for name, w, h, kw, _seed in golden_meta["pipeline_cases"]:
+        st = settings_from(w, h, kw)
+        res = spx.SegEngine(st).perform_segmentation(spx.ImageRGB(golden[f"pipe_{name}_rgb"]))
+        assert np.array_equal(res.labels.data, golden[f"pipe_{name}_labels"]), name
+        assert res.spixel_map.centers_xy.tobytes() == golden[f"pipe_{name}_cxy"].tobytes(), name
+        assert res.spixel_map.centers_lab.tobytes() == golden[f"pipe_{name}_clab"].tobytes(), name
+        assert np.array_equal(res.spixel_map.num_pixels, golden[f"pipe_{name}_counts"]), name
+        n_assoc, n_update = (int(v) for v in golden[f"pipe_{name}_passes"])
+        assert (len(res.timing.associate), len(res.timing.update)) == (n_assoc, n_update), name
+
+
+@pytest.mark.parametrize("case", ["frame_C1_640x480", "frame_C1_640x480_seed1",
+                                  "frame_C2_1280x960"])
+def test_baseline_frames_match_reference_hashes(golden_meta, case):
+    m = golden_meta["hashes"][case]
+    rgb = np.random.default_rng(m["seed"]).integers(0, 256, (m["h"], m["w"], 3), dtype=np.uint8)
+    st = settings_from(m["w"], m["h"], m["settings"])
+    res = spx.SegEngine(st).perform_segmentation(spx.ImageRGB(rgb))
+    assert sha(res.labels.data) == m["labels"]
+    assert sha(res.spixel_map.centers_xy) == m["cxy"]
+    assert sha(res.spixel_map.centers_lab) == m["clab"]
+    assert sha(res.spixel_map.num_pixels) == m["counts"]
+
+
+def test_batch_equals_single_frames():
+    w, h = 160, 120
+    st = spx.Settings(img_width=w, img_height=h, num_superpixels=75)
+    frames = [np.random.default_rng(i).integers(0, 256, (h, w, 3), dtype=np.uint8)
+              for i in range(7)]
+    eng = spx.SegEngine(st, max_batch=4)
+    batch = eng.perform_segmentation_batch([spx.ImageRGB(f) for f in frames])
+    g = spx.compute_grid(st)
+    for f, r in zip(frames, batch):
+        labels, cxy, clab, counts, _ = oracle.segment(f, g.s, g.ns_r, g.ns_c, st.compactness)
+        assert np.array_equal(r.labels.data, labels)
+        assert r.spixel_map.centers_lab.tobytes() == clab.tobytes()
+        assert np.array_equal(r.spixel_map.num_pixels, counts)
+
+
+def test_device_batch_api_and_early_stop_per_frame():
+    import torch
+    w, h = 96, 64
+    st = spx.Settings(img_width=w, img_height=h, num_superpixels=24, no_iters=8,
+                      early_stop_threshold=15.0)
+    frames = [np.random.default_rng(50 + i).integers(0, 256, (h, w, 3), dtype=np.uint8)
+              for i in range(5)]
+    frames[2][:] = 77  # flat frame converges after one update
+    eng = spx.SegEngine(st, max_batch=5)
+    d = torch.from_numpy(np.stack(frames)).cuda()
+    labels, cxy, clab, counts, passes = eng.segment_device(d)
+    torch.cuda.synchronize()
+    g = spx.compute_grid(st)
+    for i, f in enumerate(frames):
+        lw, xw, lb, cw, pw = oracle.segment(f, g.s, g.ns_r, g.ns_c, st.compactness, no_iters=8,
+                                            early_stop=15.0)
+        assert int(passes[i]) == pw
+        assert np.array_equal(labels[i].cpu().numpy(), lw)
+        assert cxy[i].cpu().numpy().tobytes() == xw.tobytes()
+        assert np.array_equal(counts[i].cpu().numpy(), cw)
+
+
+def test_strict_and_perturb_larger():
+    w, h = 200, 150
+    rgb = np.random.default_rng(77).integers(0, 256, (h, w, 3), dtype=np.uint8)
+    for kw in (dict(connectivity_mode=spx.ConnectivityMode.STRICT),
+               dict(enable_perturbation=True), dict(do_enforce_connectivity=False, tile_len=5)):
+        st = spx.Settings(img_width=w, img_height=h, num_superpixels=120, **kw)
+        res = spx.SegEngine(st).perform_segmentation(spx.ImageRGB(rgb))
+        g = spx.compute_grid(st)
+        conn = 0 if not st.do_enforce_connectivity else (
+            2 if st.connectivity_mode is spx.ConnectivityMode.STRICT else 1)
+        labels, cxy, clab, counts, _ = oracle.segment(
+            rgb, g.s, g.ns_r, g.ns_c, st.compactness, perturb=st.enable_perturbation,
+            connectivity=conn, tile_len=st.tile_len)
+        assert np.array_equal(res.labels.data, labels), kw
+        assert res.spixel_map.centers_xy.tobytes() == cxy.tobytes(), kw
+        assert np.array_equal(res.spixel_map.num_pixels, counts), kw
+
+
+def test_flat_image_block_tiling():
+    st = spx.Settings(img_width=64, img_height=64, spixel_size=8)
+    res = spx.SegEngine(st).perform_segmentation(spx.ImageRGB(np.full((64, 64, 3), 137, np.uint8)))
+    want = (np.arange(64)[:, None] // 8) * 8 + np.arange(64)[None, :] // 8
+    assert np.array_equal(res.labels.data, want)
+
+
+def test_single_shot_api_chain_matches_oracle():
+    rng = np.random.default_rng(303)
+    w, h = 47, 31
+    img = spx.ImageRGB(rng.integers(0, 256, (h, w, 3), dtype=np.uint8))
+    st = spx.Settings(img_width=w, img_height=h, num_superpixels=12)
+    grid = spx.compute_grid(st)
+    lab = spx.convert_color_space(img, spx.ColorSpace.LAB)
+    sp = spx.init_cluster_centers(lab, grid)
+    ref_lab = np.empty((h, w, 3), np.float32)
+    oracle.convert_band(img.data, ref_lab, 2, 0, h)
+    assert lab.data.tobytes() == ref_lab.tobytes()
+    for _ in range(3):
+        labels = spx.find_center_association(lab, sp, st)
+        want = np.empty((h, w), np.int32)
+        oracle.associate_band(ref_lab, sp.centers_xy, sp.centers_lab, want, grid.s, grid.ns_r,
+                              grid.ns_c, st.compactness / grid.s, 0, h)
+        assert np.array_equal(labels.data, want)
+        buf = spx.accumulate_cluster_stats(lab, labels, grid, st.tile_len)
+        sp = spx.reduce_cluster_stats(buf, sp)
+        assert int(sp.num_pixels.sum()) == w * h
+    # centroids vs brute force 5-D means (test_acceptance.py:144-180)
+    ys, xs = np.mgrid[0:h, 0:w]
+    for k in range(grid.num_clusters):
+        if sp.num_pixels[k]:
+            assert math.isclose(sp.centers_xy[k, 0], xs[labels.data == k].mean(), rel_tol=1e-9) or \
+                sp.num_pixels[k] == 0
+
+
+def test_center_shift_device_matches_numpy():
+    import ctypes
+    import torch
+    from paper_1509_04232_b200 import _lib
+    rng = np.random.default_rng(4)
+    for k in (1, 5, 64, 1200, 8160, 129600):
+        a = rng.random((k, 2)) * 1000
+        b = a + rng.normal(0, 1, (k, 2))
+        da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        _lib.check(_lib.load().spx_center_shift(ctypes.c_void_p(db.data_ptr()),
+                                                ctypes.c_void_p(da.data_ptr()), k,
+                                                ctypes.c_void_p(out.data_ptr()), None))
+        torch.cuda.synchronize()
+        assert float(out.item()) == float(np.abs(b - a).sum()), k
