@@ -67,7 +67,8 @@ class _Arg:
         if writable and not a.flags.writeable:
             raise ValueError(f"{name}: buffer source array is read-only")
         self.host = a
-        self.dev = torch.from_numpy(a).to("cuda", non_blocking=False) if a.size else \
+        src = a if a.flags.writeable else a.copy()
+        self.dev = torch.from_numpy(src).to("cuda", non_blocking=False) if a.size else \
             torch.empty(a.shape, dtype=_np_to_torch_dtype(dtype), device="cuda")
 
     @property
