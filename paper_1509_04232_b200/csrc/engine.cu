@@ -28,6 +28,16 @@ int launch_commit_done(int32_t*, int, cudaStream_t);
 int launch_weak2(const int32_t*, int32_t*, int64_t, int64_t, int, cudaStream_t);
 int launch_strict(const int32_t*, int32_t*, int64_t, int64_t, int, int64_t, int64_t, int32_t*,
                   int32_t*, int32_t*, int32_t*, cudaStream_t);
+bool cell_path_ok(int64_t, int64_t, int64_t, int64_t);
+int launch_cell(const float*, const double*, const double*, const CRec*, int32_t*, Part*,
+                const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, double, int, bool,
+                cudaStream_t);
+int launch_records(const double*, const double*, CRec*, int64_t, int64_t, int64_t, int,
+                   cudaStream_t);
+int launch_reduce_cells(const Part*, const float*, const int32_t*, const double*, const double*,
+                        double*, double*, int64_t*, CRec*, const int32_t*, int64_t, int64_t,
+                        int64_t, int64_t, int64_t, int64_t, int, cudaStream_t);
+int launch_fill_i32(int32_t*, int, int, cudaStream_t);
 
 namespace {
 
@@ -66,6 +76,9 @@ struct Engine {
   int32_t* done = nullptr;
   int32_t* passes = nullptr;
   int32_t *cc_parent = nullptr, *cc_size = nullptr, *cc_nxt = nullptr, *cc_first = nullptr;
+  CRec* rec = nullptr;   // fp32 filter records of the current centres (cell path)
+  Part* part = nullptr;  // per (cell, slot) partial sums (cell path)
+  bool use_cell = false;
   uint8_t* d_rgb = nullptr;  // staging for the host-buffer entry point
   int32_t* d_labels = nullptr;
   double *d_cxy = nullptr, *d_clab = nullptr;
@@ -82,7 +95,7 @@ struct Engine {
     for (void* p : {(void*)lab, (void*)labels, (void*)scratch, (void*)cxy[0], (void*)cxy[1],
                     (void*)clab[0], (void*)clab[1], (void*)slab, (void*)done, (void*)passes,
                     (void*)cc_parent, (void*)cc_size, (void*)cc_nxt, (void*)cc_first,
-                    (void*)d_rgb, (void*)d_labels, (void*)d_cxy, (void*)d_clab, (void*)d_counts,
+                    (void*)rec, (void*)part, (void*)d_rgb, (void*)d_labels, (void*)d_cxy, (void*)d_clab, (void*)d_counts,
                     (void*)d_passes})
       if (p) cudaFree(p);
     for (auto& e : ev)
@@ -117,7 +130,13 @@ struct Engine {
       SPX_CUDA(cudaMemset(cxy[i], 0, B * K * 2 * sizeof(double)));
       SPX_CUDA(cudaMemset(clab[i], 0, B * K * 3 * sizeof(double)));
     }
-    SPX_CUDA(cudaMalloc(&slab, B * K * n_bl * 6 * sizeof(double)));
+    use_cell = cell_path_ok(st.height, st.width, st.s, st.tile_len) && K < (1ll << 31);
+    if (use_cell) {
+      SPX_CUDA(cudaMalloc(&rec, B * K * sizeof(CRec)));
+      SPX_CUDA(cudaMalloc(&part, B * K * 9 * sizeof(Part)));
+    } else {
+      SPX_CUDA(cudaMalloc(&slab, B * K * n_bl * 6 * sizeof(double)));
+    }
     SPX_CUDA(cudaMalloc(&done, B * sizeof(int32_t)));
     SPX_CUDA(cudaMalloc(&passes, B * sizeof(int32_t)));
     if (st.connectivity == 2) {
@@ -139,10 +158,12 @@ struct Engine {
     return v[i];
   }
 
-  int associate(int cur, int frames, const int32_t* dn, cudaStream_t s) {
+  int associate(int cur, int frames, const int32_t* dn, bool acc, cudaStream_t s) {
     cudaEventRecord(pass_event(ev_assoc, 2 * n_assoc), s);
-    int rc = launch_assoc(lab, cxy[cur], clab[cur], labels, dn, st.height, st.width, st.s,
-                          st.ns_r, st.ns_c, xy_weight, 0, st.height, frames, K, s);
+    int rc = use_cell ? launch_cell(lab, cxy[cur], clab[cur], rec, labels, part, dn, st.height,
+                                    st.width, st.s, st.ns_r, st.ns_c, xy_weight, frames, acc, s)
+                      : launch_assoc(lab, cxy[cur], clab[cur], labels, dn, st.height, st.width,
+                                     st.s, st.ns_r, st.ns_c, xy_weight, 0, st.height, frames, K, s);
     cudaEventRecord(pass_event(ev_assoc, 2 * n_assoc + 1), s);
     ++n_assoc;
     ++launches;
@@ -177,29 +198,45 @@ struct Engine {
         return rc;
       ++launches;
     }
+    if (use_cell) {
+      if ((rc = launch_records(cxy[0], clab[0], rec, st.ns_r, st.ns_c, st.s, B, s))) return rc;
+      ++launches;
+    }
     cudaEventRecord(ev[EV_PERTURB], s);
-    SPX_CUDA(cudaMemsetAsync(passes, 0, B * sizeof(int32_t), s));
-    if (early) SPX_CUDA(cudaMemsetAsync(done, 0, B * sizeof(int32_t), s));
+    if (early) {
+      SPX_CUDA(cudaMemsetAsync(passes, 0, B * sizeof(int32_t), s));
+      SPX_CUDA(cudaMemsetAsync(done, 0, B * sizeof(int32_t), s));
+    }
     int cur = 0, nxt = 1;
-    if ((rc = associate(cur, B, dn, s))) return rc;
+    if ((rc = associate(cur, B, dn, true, s))) return rc;
     for (int it = 0; it < st.no_iters; ++it) {
       cudaEventRecord(pass_event(ev_update, 2 * n_update), s);
-      if ((rc = launch_accum_range(lab, labels, st.height, st.width, slab, n_bl, st.s, st.ns_c,
-                                   st.tile_len, 0, K, K, B, dn, s)))
-        return rc;
-      if ((rc = launch_reduce(slab, n_bl, cxy[cur], clab[cur], cxy[nxt], clab[nxt], out_counts, 0,
-                              K, K, B, dn, s)))
-        return rc;
-      launches += 2;
+      if (use_cell) {
+        if ((rc = launch_reduce_cells(part, lab, labels, cxy[cur], clab[cur], cxy[nxt], clab[nxt],
+                                      out_counts, rec, dn, st.height, st.width, st.s, st.ns_r,
+                                      st.ns_c, st.tile_len, B, s)))
+          return rc;
+        launches += 1;
+      } else {
+        if ((rc = launch_accum_range(lab, labels, st.height, st.width, slab, n_bl, st.s, st.ns_c,
+                                     st.tile_len, 0, K, K, B, dn, s)))
+          return rc;
+        if ((rc = launch_reduce(slab, n_bl, cxy[cur], clab[cur], cxy[nxt], clab[nxt], out_counts,
+                                0, K, K, B, dn, s)))
+          return rc;
+        launches += 2;
+      }
       cudaEventRecord(pass_event(ev_update, 2 * n_update + 1), s);
       ++n_update;
-      // shift + per-frame pass count (engine.py:196); also flags early stop
-      if ((rc = launch_shift(cxy[nxt], cxy[cur], K, B, nullptr, early ? done : nullptr, passes,
-                             early ? st.early_stop : -1.0, s)))
-        return rc;
-      ++launches;
+      if (early) {
+        // shift + per-frame pass count (engine.py:196); flags early stop
+        if ((rc = launch_shift(cxy[nxt], cxy[cur], K, B, nullptr, done, passes, st.early_stop, s)))
+          return rc;
+        ++launches;
+      }
       std::swap(cur, nxt);
-      if ((rc = associate(cur, B, dn, s))) return rc;
+      const bool more = it + 1 < st.no_iters;
+      if ((rc = associate(cur, B, dn, more, s))) return rc;
       if (early) {
         if ((rc = launch_commit_done(done, B, s))) return rc;
         ++launches;
@@ -219,6 +256,10 @@ struct Engine {
                                cudaMemcpyDeviceToDevice, s));
     }
     cudaEventRecord(ev[EV_END], s);
+    if (!early) {
+      if ((rc = launch_fill_i32(passes, B, st.no_iters, s))) return rc;
+      ++launches;
+    }
     // Final centres: frame f ends in buffer passes[f] & 1 (ping-pong, engine.py:197).
     k_gather_centres<<<(unsigned)ceil_div(K * B, 256), 256, 0, s>>>(
         cxy[0], clab[0], cxy[1], clab[1], passes, K, B, out_xy, out_lab);

@@ -161,3 +161,59 @@ def test_center_shift_device_matches_numpy():
                                                 ctypes.c_void_p(out.data_ptr()), None))
         torch.cuda.synchronize()
         assert float(out.item()) == float(np.abs(b - a).sum()), k
+
+
+def _oracle_pipeline(rgb, st):
+    g = spx.compute_grid(st)
+    conn = 0 if not st.do_enforce_connectivity else (
+        2 if st.connectivity_mode is spx.ConnectivityMode.STRICT else 1)
+    return oracle.segment(rgb, g.s, g.ns_r, g.ns_c, st.compactness, no_iters=st.no_iters,
+                          space=st.color_space.value, perturb=st.enable_perturbation,
+                          connectivity=conn, tile_len=st.tile_len,
+                          early_stop=st.early_stop_threshold)
+
+
+def _images(h, w, seed):
+    rng = np.random.default_rng(seed)
+    noise = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+    # gray-heavy image: exercises the certified-sum fallback (tiny a/b values)
+    gray = np.repeat(rng.integers(0, 256, (h, w, 1), dtype=np.uint8), 3, axis=2)
+    gray[::7] = noise[::7]
+    # smooth gradient + mild noise: natural-image-like, coherent clusters
+    yy, xx = np.mgrid[0:h, 0:w]
+    smooth = np.stack([(xx * 255 // max(w - 1, 1)), (yy * 255 // max(h - 1, 1)),
+                       ((xx + yy) * 127 // max(w + h - 2, 1))], -1)
+    smooth = np.clip(smooth + rng.integers(-6, 7, (h, w, 3)), 0, 255).astype(np.uint8)
+    dark = (noise // 40).astype(np.uint8)  # near-black: small L, tiny a/b
+    return {"noise": noise, "gray": gray, "smooth": smooth, "dark": dark}
+
+
+@pytest.mark.parametrize("s", [8, 12, 16, 20, 24, 32])
+def test_cell_path_grid_sizes_bitexact(s):
+    # W % 4 == 0 and 8 <= S <= 32, S % 4 == 0 select the fused cell kernels;
+    # ragged last row/column of cells included.
+    h, w = 3 * s + 5, 4 * s + 4 * ((s // 4) % 3) + 8
+    w -= w % 4
+    for name, rgb in _images(h, w, s).items():
+        for tile in (16, 5):
+            st = spx.Settings(img_width=w, img_height=h, spixel_size=s, tile_len=tile, no_iters=3)
+            res = spx.SegEngine(st).perform_segmentation(spx.ImageRGB(rgb))
+            labels, cxy, clab, counts, _ = _oracle_pipeline(rgb, st)
+            assert np.array_equal(res.labels.data, labels), (s, name, tile)
+            assert res.spixel_map.centers_xy.tobytes() == cxy.tobytes(), (s, name, tile)
+            assert res.spixel_map.centers_lab.tobytes() == clab.tobytes(), (s, name, tile)
+            assert np.array_equal(res.spixel_map.num_pixels, counts), (s, name, tile)
+
+
+def test_cell_path_batch_gray_heavy_frames():
+    h, w = 480, 640
+    st = spx.Settings(img_width=w, img_height=h, num_superpixels=1200)
+    frames = [_images(h, w, 900 + i)[name] for i, name in enumerate(("gray", "dark", "smooth", "noise"))]
+    eng = spx.SegEngine(st, max_batch=4)
+    res = eng.perform_segmentation_batch([spx.ImageRGB(f) for f in frames])
+    for f, r in zip(frames, res):
+        labels, cxy, clab, counts, _ = _oracle_pipeline(f, st)
+        assert np.array_equal(r.labels.data, labels)
+        assert r.spixel_map.centers_lab.tobytes() == clab.tobytes()
+        assert r.spixel_map.centers_xy.tobytes() == cxy.tobytes()
+        assert np.array_equal(r.spixel_map.num_pixels, counts)
