@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(128) k_cell(CellParams p) {
         sx += (wi - row * p.runs_per_row) * 4 + i;
         sy += row;
         cnt += 1;
-        flag |= (wv >> (bit + 4)) & 1u;
+        flag |= (wv >> (i * 8 + 4)) & 1u;
       }
     }
   }
