@@ -43,6 +43,11 @@ __device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigne
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
   unsigned long long r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -115,67 +120,107 @@ __device__ __noinline__ int exact_argmin(const double* __restrict__ cxy, const d
   return best_k;
 }
 
+// Shared-memory layout per warp.
+//   cand[cpw][9]: duplicated fp32 pairs (l,l) (a,a) (b,b) (x,x) for FFMA2
+//   cy[cpw][9]:   candidate y (cell relative)
+//   acc (ACC):    lane-private per-slot accumulators, lane-interleaved so
+//                 any per-lane slot choice is bank-conflict free:
+//                 accd[9][3][32] double, acci[9][32] uint32 (packed
+//                 count | flags<<6 | sum_x<<12 | sum_y<<22).
+struct alignas(16) CandPairs {
+  unsigned long long l, a, b, x, y, pad;
+};
+constexpr int kWarps = 4;
+constexpr size_t kCandBytes = 944;  // 18 CandPairs + 18 floats (cpw <= 2), 16-aligned
+static_assert(sizeof(CandPairs) * 18 + sizeof(float) * 18 <= kCandBytes, "cand smem");
+constexpr size_t kAccBytes = 9 * 3 * 32 * sizeof(double) + 9 * 32 * sizeof(uint32_t);
+constexpr size_t kWarpSmemAcc = kCandBytes + kAccBytes;
+constexpr size_t kWarpSmemNoAcc = kCandBytes;
+
 template <bool ACC>
-__global__ void __launch_bounds__(128) k_cell(CellParams p) {
+__global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lpc = p.lanes_per_cell;
-  const int cpw = 32 / lpc;                       // cells per warp
-  const int ci = lane / lpc, ll = lane % lpc;     // cell within warp, lane within cell
+  const int cpw = 32 / lpc;                    // cells per warp (1 or 2)
+  const int ci = lane / lpc, ll = lane % lpc;  // cell within warp, lane within cell
   const int S = p.s;
-  const int cells_per_frame = p.ns_r * p.ns_c;
-  const long long gcell = ((long long)blockIdx.x * (blockDim.x >> 5) + warp) * cpw + ci;
-  const long long total_cells = (long long)cells_per_frame * p.frames;
-  // per-cell smem: slot bytes [runs] words + Lab [4][runs] float4
-  const int cell_bytes = p.runs * 4 + p.runs * 4 * 16;
-  unsigned char* cbuf = smem + (size_t)((threadIdx.x >> 5) * cpw + ci) * cell_bytes;
-  uint32_t* slot_words = reinterpret_cast<uint32_t*>(cbuf);
-  float4* labv = reinterpret_cast<float4*>(cbuf + p.runs * 4);
+  const int K = p.ns_r * p.ns_c;
+  const long long gcell = ((long long)blockIdx.x * kWarps + warp) * cpw + ci;
+  const long long total_cells = (long long)K * p.frames;
+  unsigned char* wbase = smem + (size_t)warp * (ACC ? kWarpSmemAcc : kWarpSmemNoAcc);
+  CandPairs* cand = reinterpret_cast<CandPairs*>(wbase) + ci * 9;
+  float* cyv = reinterpret_cast<float*>(wbase + sizeof(CandPairs) * 18) + ci * 9;
+  double* accd = reinterpret_cast<double*>(wbase + kCandBytes);
+  uint32_t* acci = reinterpret_cast<uint32_t*>(wbase + kCandBytes + 9 * 3 * 32 * sizeof(double));
 
   bool active = gcell < total_cells;
   int f = 0, cr = 0, cc = 0;
   if (active) {
-    f = (int)(gcell / cells_per_frame);
-    int cell = (int)(gcell % cells_per_frame);
+    f = (int)(gcell / K);
+    const int cell = (int)(gcell % K);
     cr = cell / p.ns_c;
     cc = cell % p.ns_c;
     if (p.done && p.done[f] == 1) active = false;
   }
 
-  // ---- candidates: 9 records, relative to this cell's origin ----------------
-  float cl[9], ca[9], cb[9], cx[9], cy[9];
-  unsigned valid = 0;
-  float mc = 0.f, mxy = 0.f;
-  bool all_ok = true;
-  if (active) {
-    const CRec* rf = p.rec + (long long)f * cells_per_frame;
+  // ---- stage the 9 candidates (lanes ll < 9 of each cell) ------------------
+  float mc = 0.f, mxy = 0.f, okf = 1.f;
+  if (active && ll < 9) {
+    const int t = ll;
+    const int kr = cr + off_r(t), kc = cc + off_c(t);
+    CandPairs cp;
+    float cyt;
+    if (kr >= 0 && kr < p.ns_r && kc >= 0 && kc < p.ns_c) {
+      const float4* q = reinterpret_cast<const float4*>(p.rec + (long long)f * K + kr * p.ns_c + kc);
+      const float4 v0 = __ldg(q), v1 = __ldg(q + 1);
+      const float cxt = __fadd_rn(v0.w, (float)(off_c(t) * S));
+      cyt = __fadd_rn(v1.x, (float)(off_r(t) * S));
+      cp.l = f2_pack(v0.x, v0.x);
+      cp.a = f2_pack(v0.y, v0.y);
+      cp.b = f2_pack(v0.z, v0.z);
+      cp.x = f2_pack(cxt, cxt);
+      cp.y = f2_pack(cyt, cyt);
+      mc = v1.y;
+      mxy = fmaxf(fabsf(cxt), fabsf(cyt));
+      okf = v1.w;
+    } else {
+      // Out of the grid: colour 1e18 away makes D ~1e18, never the argmin.
+      cp.l = f2_pack(1e18f, 1e18f);
+      cp.a = cp.b = f2_pack(0.f, 0.f);
+      cp.x = f2_pack(0.f, 0.f);
+      cp.y = f2_pack(0.f, 0.f);
+      cyt = 0.f;
+    }
+    cand[t] = cp;
+    cyv[t] = cyt;
+  }
+  // cell-wide maxima over the 9 staging lanes
+#pragma unroll
+  for (int o = 8; o; o >>= 1) {
+    mc = fmaxf(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, o));
+    mxy = fmaxf(mxy, __shfl_xor_sync(0xFFFFFFFFu, mxy, o));
+    okf = fminf(okf, __shfl_xor_sync(0xFFFFFFFFu, okf, o));
+  }
+  // lanes 0..15 of each cell hold the reduction; broadcast from the cell's lane 0
+  mc = __shfl_sync(0xFFFFFFFFu, mc, ci * lpc);
+  mxy = __shfl_sync(0xFFFFFFFFu, mxy, ci * lpc);
+  okf = __shfl_sync(0xFFFFFFFFu, okf, ci * lpc);
+  if (ACC) {
+    // zero this lane's private accumulators
 #pragma unroll
     for (int t = 0; t < 9; ++t) {
-      int kr = cr + off_r(t), kc = cc + off_c(t);
-      bool in = kr >= 0 && kr < p.ns_r && kc >= 0 && kc < p.ns_c;
-      CRec r = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 1.f};
-      if (in) {
-        const float4* q = reinterpret_cast<const float4*>(rf + kr * p.ns_c + kc);
-        float4 v0 = __ldg(q), v1 = __ldg(q + 1);
-        r = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-        valid |= 1u << t;
-      }
-      cl[t] = r.l;
-      ca[t] = r.a;
-      cb[t] = r.b;
-      cx[t] = __fadd_rn(r.xr, (float)(off_c(t) * S));
-      cy[t] = __fadd_rn(r.yr, (float)(off_r(t) * S));
-      if (in) {
-        mc = fmaxf(mc, r.mag_lab);
-        mxy = fmaxf(mxy, fmaxf(fabsf(cx[t]), fabsf(cy[t])));
-        all_ok = all_ok && (r.ok != 0.f);
-      }
+      accd[(t * 3 + 0) * 32 + lane] = 0.0;
+      accd[(t * 3 + 1) * 32 + lane] = 0.0;
+      accd[(t * 3 + 2) * 32 + lane] = 0.0;
+      acci[t * 32 + lane] = 0u;
     }
   }
-  // Cell constant part of 2A: k_mc*Mc + k_xy*(3*Mxy + 2S) + k_const
+  __syncwarp();
+
+  // Cell constant of 2A: k_mc*Mc + k_xy*(3*Mxy + 2S) + k_const
   float two_a_cell = __fmaf_rn(mc, p.k_mc, __fmaf_rn(__fmaf_rn(3.f, mxy, 2.f * S), p.k_xy, p.k_const));
-  if (!all_ok) two_a_cell = INFINITY;
-  const unsigned long long W2 = f2_pack(p.w32, p.w32);
+  if (okf == 0.f) two_a_cell = INFINITY;
   const unsigned long long TINY2 = f2_pack(1e-30f, 1e-30f);
   const int x_cell = cc * S, y_cell = cr * S;
   const long long img_base = (long long)f * p.h * p.w;
@@ -185,160 +230,115 @@ __global__ void __launch_bounds__(128) k_cell(CellParams p) {
       const int row = j / p.runs_per_row;
       const int c4 = (j - row * p.runs_per_row) * 4;
       const int y = y_cell + row, x = x_cell + c4;
-      uint32_t word = 0xFFFFFFFFu;  // slot bytes; 0xFF = no pixel
-      if (y < p.h && x < p.w) {
-        const long long pix = img_base + (long long)y * p.w + x;
-        const float4* src = reinterpret_cast<const float4*>(p.img + pix * 3);
-        float4 v0 = __ldg(src), v1 = __ldg(src + 1), v2 = __ldg(src + 2);
-        float L[4] = {v0.x, v0.w, v1.z, v2.y};
-        float A[4] = {v0.y, v1.x, v1.w, v2.z};
-        float B[4] = {v0.z, v1.y, v2.x, v2.w};
-        const unsigned long long NL01 = f2_pack(-L[0], -L[1]), NL23 = f2_pack(-L[2], -L[3]);
-        const unsigned long long NA01 = f2_pack(-A[0], -A[1]), NA23 = f2_pack(-A[2], -A[3]);
-        const unsigned long long NB01 = f2_pack(-B[0], -B[1]), NB23 = f2_pack(-B[2], -B[3]);
-        const float xr0 = (float)c4;
-        const unsigned long long NX01 = f2_pack(-xr0, -(xr0 + 1.f));
-        const unsigned long long NX23 = f2_pack(-(xr0 + 2.f), -(xr0 + 3.f));
-        const float yr = (float)row;
-        unsigned k1[4] = {0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu};
-        unsigned k2[4] = {0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu};
+      if (y >= p.h || x >= p.w) continue;
+      const long long pix = img_base + (long long)y * p.w + x;   // label index
+      const long long pl = (long long)f * 3 * p.h * p.w + (long long)y * p.w + x;  // planar Lab
+      const long long hw = (long long)p.h * p.w;
+      const float4 Lv = __ldg(reinterpret_cast<const float4*>(p.img + pl));
+      const float4 Av = __ldg(reinterpret_cast<const float4*>(p.img + pl + hw));
+      const float4 Bv = __ldg(reinterpret_cast<const float4*>(p.img + pl + 2 * hw));
+      const float L[4] = {Lv.x, Lv.y, Lv.z, Lv.w};
+      const float A[4] = {Av.x, Av.y, Av.z, Av.w};
+      const float B[4] = {Bv.x, Bv.y, Bv.z, Bv.w};
+      const unsigned long long L01 = f2_pack(Lv.x, Lv.y), L23 = f2_pack(Lv.z, Lv.w);
+      const unsigned long long A01 = f2_pack(Av.x, Av.y), A23 = f2_pack(Av.z, Av.w);
+      const unsigned long long B01 = f2_pack(Bv.x, Bv.y), B23 = f2_pack(Bv.z, Bv.w);
+      const float xr0 = (float)c4;
+      const unsigned long long X01 = f2_pack(xr0, xr0 + 1.f);
+      const unsigned long long X23 = f2_pack(xr0 + 2.f, xr0 + 3.f);
+      const float yr = (float)row;
+      const unsigned long long Y2 = f2_pack(yr, yr);
+      unsigned k1[4] = {0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu};
+      unsigned k2[4] = {0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu};
+      const float w32 = p.w32;
 #pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          const unsigned long long CL = f2_pack(cl[t], cl[t]);
-          const unsigned long long CA = f2_pack(ca[t], ca[t]);
-          const unsigned long long CB = f2_pack(cb[t], cb[t]);
-          const unsigned long long CX = f2_pack(cx[t], cx[t]);
-          const float dy = __fsub_rn(cy[t], yr);
-          const float dyy = __fmaf_rn(dy, dy, 1e-30f);
-          const unsigned long long DYY = f2_pack(dyy, dyy);
-          unsigned long long d01, d23;
-          {
-            unsigned long long dl = add2(CL, NL01), da = add2(CA, NA01), db = add2(CB, NB01);
-            unsigned long long q = fma2(db, db, fma2(da, da, fma2(dl, dl, TINY2)));
-            unsigned long long dx = add2(CX, NX01);
-            unsigned long long r = fma2(dx, dx, DYY);
-            d01 = fma2(W2, sqrt2(r), sqrt2(q));
-          }
-          {
-            unsigned long long dl = add2(CL, NL23), da = add2(CA, NA23), db = add2(CB, NB23);
-            unsigned long long q = fma2(db, db, fma2(da, da, fma2(dl, dl, TINY2)));
-            unsigned long long dx = add2(CX, NX23);
-            unsigned long long r = fma2(dx, dx, DYY);
-            d23 = fma2(W2, sqrt2(r), sqrt2(q));
-          }
-          float D[4];
-          f2_unpack(d01, D[0], D[1]);
-          f2_unpack(d23, D[2], D[3]);
-          const bool vt = (valid >> t) & 1u;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            unsigned key = vt ? ((__float_as_uint(D[i]) & ~15u) | (unsigned)t) : 0x7F7FFFFFu;
-            k2[i] = min(k2[i], max(k1[i], key));
-            k1[i] = min(k1[i], key);
-          }
+      for (int t = 0; t < 9; ++t) {
+        const CandPairs c = cand[t];
+        const unsigned long long dy = sub2(c.y, Y2);
+        const unsigned long long dyy = fma2(dy, dy, TINY2);
+        float Q[4], R[4];
+        {
+          unsigned long long dl = sub2(c.l, L01), da = sub2(c.a, A01), db = sub2(c.b, B01);
+          unsigned long long q = fma2(db, db, fma2(da, da, fma2(dl, dl, TINY2)));
+          unsigned long long dx = sub2(c.x, X01);
+          unsigned long long r = fma2(dx, dx, dyy);
+          f2_unpack(q, Q[0], Q[1]);
+          f2_unpack(r, R[0], R[1]);
         }
-        int lab4[4];
-        word = 0;
+        {
+          unsigned long long dl = sub2(c.l, L23), da = sub2(c.a, A23), db = sub2(c.b, B23);
+          unsigned long long q = fma2(db, db, fma2(da, da, fma2(dl, dl, TINY2)));
+          unsigned long long dx = sub2(c.x, X23);
+          unsigned long long r = fma2(dx, dx, dyy);
+          f2_unpack(q, Q[2], Q[3]);
+          f2_unpack(r, R[2], R[3]);
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const float mp = fabsf(L[i]) + fabsf(A[i]) + fabsf(B[i]);
-          const float f2v = __uint_as_float(k2[i]);
-          const float thr = __fmaf_rn(f2v, p.k_rel, __fmaf_rn(mp, p.k_mp, two_a_cell));
-          const float gap = __fsub_rn(f2v, __uint_as_float(k1[i]));
-          int t = (int)(k1[i] & 15u);
-          int k = (cr + off_r(t)) * p.ns_c + (cc + off_c(t));
-          if (!(gap > thr) || !(mp < 1e15f)) {
-            k = exact_argmin(p.cxy + (long long)f * cells_per_frame * 2,
-                             p.clab + (long long)f * cells_per_frame * 3, L[i], A[i], B[i],
-                             x + i, y, cr, cc, p.ns_r, p.ns_c, p.xy_weight);
-            const int idx = (k / p.ns_c - cr + 1) * 3 + (k % p.ns_c - cc + 1);
-            t = idx < 4 ? idx + 1 : (idx == 4 ? 0 : idx);  // (dr,dc) -> scan slot
-          }
-          lab4[i] = k;
-          if (ACC) {
-            unsigned fl = sum_flag(L[i], p.tau) | sum_flag(A[i], p.tau) | sum_flag(B[i], p.tau);
-            word |= ((unsigned)t | (fl << 4)) << (8 * i);
-          }
-        }
-        int4* dst = reinterpret_cast<int4*>(p.labels + pix);
-        *dst = make_int4(lab4[0], lab4[1], lab4[2], lab4[3]);
-        if (ACC) {
-          labv[0 * p.runs + j] = make_float4(L[0], A[0], B[0], 0.f);
-          labv[1 * p.runs + j] = make_float4(L[1], A[1], B[1], 0.f);
-          labv[2 * p.runs + j] = make_float4(L[2], A[2], B[2], 0.f);
-          labv[3 * p.runs + j] = make_float4(L[3], A[3], B[3], 0.f);
+          // D = sqrt(q) + w * sqrt(r), both square roots as v * rsqrt(v)
+          const float s1 = __fmul_rn(Q[i], rsq(Q[i]));
+          const float d = __fmaf_rn(w32, __fmul_rn(R[i], rsq(R[i])), s1);
+          const unsigned key = (__float_as_uint(d) & ~15u) | (unsigned)t;
+          k2[i] = min(k2[i], max(k1[i], key));
+          k1[i] = min(k1[i], key);
         }
       }
-      if (ACC) slot_words[j] = word;
+      int lab4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float mp = fabsf(L[i]) + fabsf(A[i]) + fabsf(B[i]);
+        const float f2v = __uint_as_float(k2[i]);
+        const float thr = __fmaf_rn(f2v, p.k_rel, __fmaf_rn(mp, p.k_mp, two_a_cell));
+        const float gap = __fsub_rn(f2v, __uint_as_float(k1[i]));
+        int t = (int)(k1[i] & 15u);
+        int k = (cr + off_r(t)) * p.ns_c + (cc + off_c(t));
+        if (!(gap > thr) || !(mp < 1e15f)) {
+          k = exact_argmin(p.cxy + (long long)f * K * 2, p.clab + (long long)f * K * 3, L[i], A[i],
+                           B[i], x + i, y, cr, cc, p.ns_r, p.ns_c, p.xy_weight);
+          const int idx = (k / p.ns_c - cr + 1) * 3 + (k % p.ns_c - cc + 1);
+          t = idx < 4 ? idx + 1 : (idx == 4 ? 0 : idx);  // (dr,dc) -> scan slot
+        }
+        lab4[i] = k;
+        if (ACC) {
+          const unsigned fl = sum_flag(L[i], p.tau) | sum_flag(A[i], p.tau) | sum_flag(B[i], p.tau);
+          double* d = accd + t * 96 + lane;
+          d[0] = dadd(d[0], (double)L[i]);
+          d[32] = dadd(d[32], (double)A[i]);
+          d[64] = dadd(d[64], (double)B[i]);
+          acci[t * 32 + lane] += 1u | (fl << 6) | ((unsigned)(c4 + i) << 12) | ((unsigned)row << 22);
+        }
+      }
+      *reinterpret_cast<int4*>(p.labels + pix) = make_int4(lab4[0], lab4[1], lab4[2], lab4[3]);
     }
   }
   if (!ACC) return;
   __syncwarp();
-
-  // ---- owner lanes: fold each slot's members -------------------------------
-  const int segs = lpc / 9;  // 3 (32 lanes) or 1 (16 lanes)
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  int sx = 0, sy = 0, cnt = 0;
-  unsigned flag = 0;
-  const int slot = ll % 9, seg = ll / 9;
-  if (active && seg < segs) {
-    const int w0 = (p.runs * seg) / segs, w1 = (p.runs * (seg + 1)) / segs;
-    const uint32_t rep = 0x01010101u * (uint32_t)slot;
-    for (int wi = w0; wi < w1; ++wi) {
-      uint32_t wv = slot_words[wi];
-      uint32_t z = (wv & 0x0F0F0F0Fu) ^ rep;  // zero byte <=> slot match
-      // exact zero-byte detection (no false positives across bytes)
-      uint32_t m = ~(((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z | 0x7F7F7F7Fu);
-      m &= ~((wv & 0x80808080u));  // 0xFF marks "no pixel"
-      while (m) {
-        const int bit = __ffs(m) - 1;
-        const int i = bit >> 3;
-        m &= m - 1;
-        const float4 v = labv[i * p.runs + wi];
-        s0 = dadd(s0, (double)v.x);
-        s1 = dadd(s1, (double)v.y);
-        s2 = dadd(s2, (double)v.z);
-        const int row = wi / p.runs_per_row;
-        sx += (wi - row * p.runs_per_row) * 4 + i;
-        sy += row;
-        cnt += 1;
-        flag |= (wv >> (i * 8 + 4)) & 1u;
+  // ---- per-cell column reduction: 9 slots x (3 colour + 1 packed int) -------
+  // column c < 27: colour (slot c/3, channel c%3); 27 <= c < 36: ints of slot c-27
+  const int lane0 = ci * lpc;
+  for (int col = ll; col < 36; col += lpc) {
+    if (!active) break;
+    if (col < 27) {
+      const double* src = accd + col * 32 + lane0;
+      double sacc = 0.0;
+      for (int q = 0; q < lpc; ++q) sacc = dadd(sacc, src[q]);
+      p.part[gcell * 9 + col / 3].s[col % 3] = sacc;
+    } else {
+      const uint32_t* src = acci + (col - 27) * 32 + lane0;
+      int cnt = 0, fl = 0, sx = 0, sy = 0;
+      for (int q = 0; q < lpc; ++q) {
+        const uint32_t v = src[q];
+        cnt += v & 63u;
+        fl += (v >> 6) & 63u;
+        sx += (v >> 12) & 1023u;
+        sy += v >> 22;
       }
+      Part* o = p.part + gcell * 9 + (col - 27);
+      o->sx = sx;
+      o->sy = sy;
+      o->cnt = cnt;
+      o->flag = fl;
     }
-  }
-  // combine the segments (fixed order: seg 0 + seg 1 + seg 2)
-  const unsigned full = 0xFFFFFFFFu;
-  if (segs > 1) {
-#pragma unroll
-    for (int g = 1; g < 3; ++g) {
-      const int srcl = (lane & ~(lpc - 1)) + slot + 9 * g;
-      double t0 = __shfl_sync(full, s0, srcl), t1 = __shfl_sync(full, s1, srcl),
-             t2 = __shfl_sync(full, s2, srcl);
-      int ux = __shfl_sync(full, sx, srcl), uy = __shfl_sync(full, sy, srcl),
-          uc = __shfl_sync(full, cnt, srcl);
-      unsigned uf = __shfl_sync(full, flag, srcl);
-      if (seg == 0) {
-        s0 = dadd(s0, t0);
-        s1 = dadd(s1, t1);
-        s2 = dadd(s2, t2);
-        sx += ux;
-        sy += uy;
-        cnt += uc;
-        flag |= uf;
-      }
-    }
-  }
-  if (active && seg == 0) {
-    Part* o = p.part + (gcell * 9 + slot);
-    Part r;
-    r.s[0] = s0;
-    r.s[1] = s1;
-    r.s[2] = s2;
-    r.sx = sx;
-    r.sy = sy;
-    r.cnt = cnt;
-    r.flag = (int)flag;
-    *o = r;
   }
 }
 
@@ -368,7 +368,7 @@ __global__ void k_records(const double* __restrict__ cxy, const double* __restri
 
 // Reference strip fold for one (cluster, strip): _core.pyx:221-255 verbatim
 // order (row-major, binary64 colour, integer x/y/count).
-__device__ void strip_fold(const float* __restrict__ img, const int32_t* __restrict__ lab, int h,
+__device__ void strip_fold(const LabView im, const int32_t* __restrict__ lab, int h,
                            int w, int k, int j, int s, int ns_c, int tile_len, double out[6]) {
   int r = k / ns_c, c = k % ns_c;
   int wx0 = max((c - 1) * s, 0), wx1 = min((c + 2) * s, w);
@@ -379,10 +379,9 @@ __device__ void strip_fold(const float* __restrict__ img, const int32_t* __restr
   for (int y = sy0; y < sy1; ++y)
     for (int x = wx0; x < wx1; ++x)
       if (__ldg(lab + (long long)y * w + x) == k) {
-        const float* px = img + ((long long)y * w + x) * 3;
-        sl = dadd(sl, (double)__ldg(px));
-        sa = dadd(sa, (double)__ldg(px + 1));
-        sb = dadd(sb, (double)__ldg(px + 2));
+        sl = dadd(sl, (double)im.get(y, x, 0));
+        sa = dadd(sa, (double)im.get(y, x, 1));
+        sb = dadd(sb, (double)im.get(y, x, 2));
         sx += x;
         sy += y;
         cnt += 1;
@@ -494,7 +493,7 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
     need &= need - 1;
     const int fk = __shfl_sync(0xFFFFFFFFu, k, src);
     const int ff = __shfl_sync(0xFFFFFFFFu, f, src);
-    const float* im = p.img + (long long)ff * p.h * p.w * 3;
+    const LabView im{p.img + (long long)ff * p.h * p.w * 3, p.w, (long long)p.h * p.w, true};
     const int32_t* lb = p.labels + (long long)ff * p.h * p.w;
     if (lane < p.n_bl) strip_fold(im, lb, p.h, p.w, fk, lane, p.s, p.ns_c, p.tile_len, strips[warp][lane]);
     __syncwarp();
@@ -532,11 +531,8 @@ bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
 }
 
 size_t cell_smem_bytes(int64_t s, bool acc) {
-  if (!acc) return 0;
-  int runs = (int)(s * s / 4);
-  int lpc = runs >= 32 ? 32 : 16;
-  int cpw = 32 / lpc;
-  return (size_t)4 * cpw * (runs * 4 + runs * 4 * 16);
+  (void)s;
+  return (size_t)kWarps * (acc ? kWarpSmemAcc : kWarpSmemNoAcc);
 }
 
 void assoc_bound_coefficients(double xy_weight, float& w32, float& k_mp, float& k_mc, float& k_xy,
@@ -572,7 +568,7 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   const int cpw = 32 / p.lanes_per_cell;
   const long long cells = ns_r * ns_c * (long long)frames;
   const long long warps = ceil_div(cells, cpw);
-  const unsigned blocks = (unsigned)ceil_div(warps, 4);
+  const unsigned blocks = (unsigned)ceil_div(warps, kWarps);
   const size_t smem = cell_smem_bytes(s, acc);
   if (acc) {
     static size_t configured = 0;
@@ -583,7 +579,7 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
     }
     k_cell<true><<<blocks, 128, smem, st>>>(p);
   } else {
-    k_cell<false><<<blocks, 128, 0, st>>>(p);
+    k_cell<false><<<blocks, 128, smem, st>>>(p);
   }
   SPX_LAUNCH_CHECK("k_cell");
   return SPX_OK;

@@ -7,36 +7,31 @@
 namespace spx {
 
 // _core.pyx:110-120 _gradient, exact binary64.
-__device__ __forceinline__ double gradient_at(const float* __restrict__ img, int64_t w, int64_t x,
-                                              int64_t y) {
-  const float* l = img + (y * w + x - 1) * 3;
-  const float* r = img + (y * w + x + 1) * 3;
-  const float* u = img + ((y - 1) * w + x) * 3;
-  const float* d = img + ((y + 1) * w + x) * 3;
-  double dl = dsub((double)r[0], (double)l[0]);
-  double da = dsub((double)r[1], (double)l[1]);
-  double db = dsub((double)r[2], (double)l[2]);
+__device__ __forceinline__ double gradient_at(const LabView& im, int64_t x, int64_t y) {
+  double dl = dsub((double)im.get(y, x + 1, 0), (double)im.get(y, x - 1, 0));
+  double da = dsub((double)im.get(y, x + 1, 1), (double)im.get(y, x - 1, 1));
+  double db = dsub((double)im.get(y, x + 1, 2), (double)im.get(y, x - 1, 2));
   double gx = dadd(dadd(dmul(dl, dl), dmul(da, da)), dmul(db, db));
-  dl = dsub((double)d[0], (double)u[0]);
-  da = dsub((double)d[1], (double)u[1]);
-  db = dsub((double)d[2], (double)u[2]);
+  dl = dsub((double)im.get(y + 1, x, 0), (double)im.get(y - 1, x, 0));
+  da = dsub((double)im.get(y + 1, x, 1), (double)im.get(y - 1, x, 1));
+  db = dsub((double)im.get(y + 1, x, 2), (double)im.get(y - 1, x, 2));
   double gy = dadd(dadd(dmul(dl, dl), dmul(da, da)), dmul(db, db));
   return dadd(gx, gy);
 }
 
 // _core.pyx:123-156 perturb for one centre (in place).
-__device__ __forceinline__ void perturb_one(const float* __restrict__ img, int64_t h, int64_t w,
-                                            double* cxy, double* clab) {
+__device__ __forceinline__ void perturb_one(const LabView& im, int64_t h, int64_t w, double* cxy,
+                                            double* clab) {
   int64_t ix = (int64_t)cxy[0], iy = (int64_t)cxy[1];
   if (ix < 1 || ix > w - 2 || iy < 1 || iy > h - 2) return;
-  double best = gradient_at(img, w, ix, iy);
+  double best = gradient_at(im, ix, iy);
   int64_t bx = ix, by = iy;
   for (int dy = -1; dy < 2; ++dy)
     for (int dx = -1; dx < 2; ++dx) {
       if (dx == 0 && dy == 0) continue;
       int64_t nx = ix + dx, ny = iy + dy;
       if (nx < 1 || nx > w - 2 || ny < 1 || ny > h - 2) continue;
-      double g = gradient_at(img, w, nx, ny);
+      double g = gradient_at(im, nx, ny);
       if (g < best) {
         best = g;
         bx = nx;
@@ -45,24 +40,23 @@ __device__ __forceinline__ void perturb_one(const float* __restrict__ img, int64
     }
   cxy[0] = (double)bx;
   cxy[1] = (double)by;
-  const float* p = img + (by * w + bx) * 3;
-  clab[0] = p[0];
-  clab[1] = p[1];
-  clab[2] = p[2];
+  clab[0] = im.get(by, bx, 0);
+  clab[1] = im.get(by, bx, 1);
+  clab[2] = im.get(by, bx, 2);
 }
 
 // _core.pyx:86-107 (+ optional perturb).  Clusters [k0,k1) of each of
-// `frames` frames; frame f uses img + f*img_stride etc.
+// `frames` frames; `planar` selects the engine's [3][H][W] Lab layout.
 __global__ void k_init(const float* __restrict__ img, int64_t h, int64_t w, int64_t s,
                        int64_t ns_c, double* __restrict__ cxy, double* __restrict__ clab,
                        int64_t k0, int64_t k1, int64_t k_stride, int frames, int perturb,
-                       int do_init) {
+                       int do_init, int planar) {
   int64_t nk = k1 - k0;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nk * frames) return;
   int64_t f = i / nk;
   int64_t k = k0 + i % nk;
-  const float* im = img + f * h * w * 3;
+  const LabView im{img + f * h * w * 3, w, h * w, planar != 0};
   double* xy = cxy + (f * k_stride + k) * 2;
   double* lab = clab + (f * k_stride + k) * 3;
   if (do_init) {
@@ -73,21 +67,20 @@ __global__ void k_init(const float* __restrict__ img, int64_t h, int64_t w, int6
     if (iy > h - 1) iy = h - 1;
     xy[0] = (double)ix;
     xy[1] = (double)iy;
-    const float* p = im + (iy * w + ix) * 3;
-    lab[0] = p[0];
-    lab[1] = p[1];
-    lab[2] = p[2];
+    lab[0] = im.get(iy, ix, 0);
+    lab[1] = im.get(iy, ix, 1);
+    lab[2] = im.get(iy, ix, 2);
   }
   if (perturb) perturb_one(im, h, w, xy, lab);
 }
 
 int launch_init(const float* img, int64_t h, int64_t w, int64_t s, int64_t ns_c, double* cxy,
                 double* clab, int64_t k0, int64_t k1, int64_t k_stride, int frames, int perturb,
-                int do_init, cudaStream_t st) {
+                int do_init, cudaStream_t st, int planar) {
   int64_t n = (k1 - k0) * frames;
   if (n <= 0) return SPX_OK;
   k_init<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(img, h, w, s, ns_c, cxy, clab, k0, k1,
-                                                     k_stride, frames, perturb, do_init);
+                                                     k_stride, frames, perturb, do_init, planar);
   SPX_LAUNCH_CHECK("k_init");
   return SPX_OK;
 }
@@ -243,7 +236,7 @@ extern "C" int32_t spx_init_centers_range(const float* img, int64_t h, int64_t w
     set_error("init_centers_range: bad grid (s=%lld ns_c=%lld)", (long long)s, (long long)ns_c);
     return SPX_ERR_VALUE;
   }
-  return launch_init(img, h, w, s, ns_c, cxy, clab, k0, k1, 0, 1, 0, 1, as_stream(stream));
+  return launch_init(img, h, w, s, ns_c, cxy, clab, k0, k1, 0, 1, 0, 1, as_stream(stream), 0);
 }
 
 extern "C" int32_t spx_perturb_range(const float* img, int64_t h, int64_t w, double* cxy,
@@ -252,7 +245,7 @@ extern "C" int32_t spx_perturb_range(const float* img, int64_t h, int64_t w, dou
     set_error("perturb_range: negative cluster index");
     return SPX_ERR_VALUE;
   }
-  return launch_init(img, h, w, 1, 1, cxy, clab, k0, k1, 0, 1, 1, 0, as_stream(stream));
+  return launch_init(img, h, w, 1, 1, cxy, clab, k0, k1, 0, 1, 1, 0, as_stream(stream), 0);
 }
 
 extern "C" int32_t spx_reduce_range(double* slab, int64_t n_bl, const double* prev_xy,

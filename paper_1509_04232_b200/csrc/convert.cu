@@ -111,10 +111,12 @@ __device__ __forceinline__ void convert_px(const double* lut, uint32_t R, uint32
 
 // Pixels [p0, p1) of a flat HWC raster (frames of a batch are contiguous, so
 // a batch is one range).  `vec` requires rgb 4-byte and out 16-byte aligned.
-template <int SPACE>
+// PLANAR: out is [frames][3][hw] (the engine's internal layout) instead of
+// HWC; requires hw % 4 == 0 so a 4-pixel group never straddles frames.
+template <int SPACE, bool PLANAR>
 __global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb,
                                                  float* __restrict__ out, int64_t p0,
-                                                 int64_t p1, int vec) {
+                                                 int64_t p1, int vec, int64_t hw) {
   __shared__ double lut[256];
   if (SPACE != 0) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = g_lut[i];
@@ -139,37 +141,61 @@ __global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb
       for (int i = 0; i < 4; ++i)
         convert_px<SPACE>(lut, c[3 * i], c[3 * i + 1], c[3 * i + 2], o[3 * i], o[3 * i + 1],
                           o[3 * i + 2]);
-      float4* dst = reinterpret_cast<float4*>(out + q * 3);
-      dst[0] = make_float4(o[0], o[1], o[2], o[3]);
-      dst[1] = make_float4(o[4], o[5], o[6], o[7]);
-      dst[2] = make_float4(o[8], o[9], o[10], o[11]);
+      if (PLANAR) {
+        const int64_t f = q / hw, r = q - f * hw;
+        float* base = out + f * 3 * hw + r;
+        *reinterpret_cast<float4*>(base) = make_float4(o[0], o[3], o[6], o[9]);
+        *reinterpret_cast<float4*>(base + hw) = make_float4(o[1], o[4], o[7], o[10]);
+        *reinterpret_cast<float4*>(base + 2 * hw) = make_float4(o[2], o[5], o[8], o[11]);
+      } else {
+        float4* dst = reinterpret_cast<float4*>(out + q * 3);
+        dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+        dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+        dst[2] = make_float4(o[8], o[9], o[10], o[11]);
+      }
     } else {
       for (int64_t p = q; p < q + 4; ++p) {
         if (p < p0 || p >= p1) continue;
         float o0, o1, o2;
         convert_px<SPACE>(lut, rgb[p * 3], rgb[p * 3 + 1], rgb[p * 3 + 2], o0, o1, o2);
-        out[p * 3] = o0;
-        out[p * 3 + 1] = o1;
-        out[p * 3 + 2] = o2;
+        if (PLANAR) {
+          const int64_t f = p / hw, r = p - f * hw;
+          out[f * 3 * hw + r] = o0;
+          out[f * 3 * hw + hw + r] = o1;
+          out[f * 3 * hw + 2 * hw + r] = o2;
+        } else {
+          out[p * 3] = o0;
+          out[p * 3 + 1] = o1;
+          out[p * 3 + 2] = o2;
+        }
       }
     }
   }
 }
 
 int launch_convert(const uint8_t* rgb, float* out, int64_t p0, int64_t p1, int space,
-                   cudaStream_t st) {
+                   cudaStream_t st, int64_t planar_hw) {
   if (p1 <= p0) return SPX_OK;
   int rc = upload_tables();
   if (rc) return rc;
   int vec = ((uintptr_t)rgb % 4 == 0) && ((uintptr_t)out % 16 == 0);
+  const bool planar = planar_hw > 0;
+  if (planar && (planar_hw % 4 != 0 || !vec)) {
+    set_error("planar convert needs h*w %% 4 == 0 and aligned buffers");
+    return SPX_ERR_VALUE;
+  }
   int64_t groups = ((p1 + 3) >> 2) - (p0 >> 2);
   int64_t blocks = ceil_div(groups, 256);
   int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
+#define SPX_CONVERT(SP)                                                                  \
+  (planar ? k_convert<SP, true><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec,  \
+                                                                  planar_hw)              \
+          : k_convert<SP, false><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec, 1))
   switch (space) {
-    case 0: k_convert<0><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec); break;
-    case 1: k_convert<1><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec); break;
-    case 2: k_convert<2><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec); break;
+    case 0: SPX_CONVERT(0); break;
+    case 1: SPX_CONVERT(1); break;
+    case 2: SPX_CONVERT(2); break;
     default:
       set_error("unknown colour space %d", space);
       return SPX_ERR_VALUE;
@@ -187,5 +213,5 @@ extern "C" int32_t spx_convert_band(const uint8_t* rgb, float* out, int64_t h, i
                    (long long)y0, (long long)y1, (long long)h);
     return SPX_ERR_DIMENSION;
   }
-  return spx::launch_convert(rgb, out, y0 * w, y1 * w, space, spx::as_stream(stream));
+  return spx::launch_convert(rgb, out, y0 * w, y1 * w, space, spx::as_stream(stream), 0);
 }

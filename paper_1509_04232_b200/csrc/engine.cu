@@ -11,9 +11,9 @@
 #include "spx_internal.cuh"
 
 namespace spx {
-int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t);
+int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t);
 int launch_init(const float*, int64_t, int64_t, int64_t, int64_t, double*, double*, int64_t,
-                int64_t, int64_t, int, int, int, cudaStream_t);
+                int64_t, int64_t, int, int, int, cudaStream_t, int);
 int launch_assoc(const float*, const double*, const double*, int32_t*, const int32_t*, int64_t,
                  int64_t, int64_t, int64_t, int64_t, double, int64_t, int64_t, int, int64_t,
                  cudaStream_t);
@@ -184,17 +184,18 @@ struct Engine {
     launches = 0;
     const int32_t* dn = early ? done : nullptr;
     cudaEventRecord(ev[EV_START], s);
-    if ((rc = launch_convert(rgb, lab, 0, (int64_t)B * hw, st.color_space, s))) return rc;
+    if ((rc = launch_convert(rgb, lab, 0, (int64_t)B * hw, st.color_space, s, use_cell ? hw : 0)))
+      return rc;
     ++launches;
     cudaEventRecord(ev[EV_CONVERT], s);
     if ((rc = launch_init(lab, st.height, st.width, st.s, st.ns_c, cxy[0], clab[0], 0, K, K, B, 0,
-                          1, s)))
+                          1, s, use_cell)))
       return rc;
     ++launches;
     cudaEventRecord(ev[EV_INIT], s);
     if (st.perturb) {
       if ((rc = launch_init(lab, st.height, st.width, st.s, st.ns_c, cxy[0], clab[0], 0, K, K, B,
-                            1, 0, s)))
+                            1, 0, s, use_cell)))
         return rc;
       ++launches;
     }
