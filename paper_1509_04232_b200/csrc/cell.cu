@@ -38,11 +38,6 @@ __device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
 __device__ __forceinline__ void f2_unpack(unsigned long long v, float& lo, float& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
-__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
-  unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
 __device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
   unsigned long long r;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -64,13 +59,6 @@ __device__ __forceinline__ float rsq(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-// sqrt of a packed pair as q * rsqrt(q) (q >= 1e-30 by construction).
-__device__ __forceinline__ unsigned long long sqrt2(unsigned long long q) {
-  float q0, q1;
-  f2_unpack(q, q0, q1);
-  return mul2(q, f2_pack(rsq(q0), rsq(q1)));
-}
-
 __device__ __forceinline__ bool fin_small(double v) { return fabs(v) < 1e15; }
 
 // Out-of-range flag for the certified sums: nonzero |v| < tau or |v| >= 128
@@ -125,15 +113,16 @@ __device__ __noinline__ int exact_argmin(const double* __restrict__ cxy, const d
 //   cy[cpw][9]:   candidate y (cell relative)
 //   acc (ACC):    lane-private per-slot accumulators, lane-interleaved so
 //                 any per-lane slot choice is bank-conflict free:
-//                 accd[9][3][32] double, acci[9][32] uint32 (packed
-//                 count | flags<<6 | sum_x<<12 | sum_y<<22).
+//                 accd[9][3][32] double, acci[9][32] uint64 (packed
+//                 count | flags<<11 | sum_x<<22 | sum_y<<43).
+//   cand_k[cpw][9]: cluster id of each candidate slot
 struct alignas(16) CandPairs {
   unsigned long long l, a, b, x, y, pad;
 };
 constexpr int kWarps = 4;
 constexpr size_t kCandBytes = 944;  // 18 CandPairs + 18 floats (cpw <= 2), 16-aligned
 static_assert(sizeof(CandPairs) * 18 + sizeof(float) * 18 <= kCandBytes, "cand smem");
-constexpr size_t kAccBytes = 9 * 3 * 32 * sizeof(double) + 9 * 32 * sizeof(uint32_t);
+constexpr size_t kAccBytes = 9 * 3 * 32 * sizeof(double) + 9 * 32 * sizeof(uint64_t);
 constexpr size_t kWarpSmemAcc = kCandBytes + kAccBytes;
 constexpr size_t kWarpSmemNoAcc = kCandBytes;
 
@@ -150,9 +139,10 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   const long long total_cells = (long long)K * p.frames;
   unsigned char* wbase = smem + (size_t)warp * (ACC ? kWarpSmemAcc : kWarpSmemNoAcc);
   CandPairs* cand = reinterpret_cast<CandPairs*>(wbase) + ci * 9;
-  float* cyv = reinterpret_cast<float*>(wbase + sizeof(CandPairs) * 18) + ci * 9;
+  int* cand_k = reinterpret_cast<int*>(wbase + sizeof(CandPairs) * 18) + ci * 9;
   double* accd = reinterpret_cast<double*>(wbase + kCandBytes);
-  uint32_t* acci = reinterpret_cast<uint32_t*>(wbase + kCandBytes + 9 * 3 * 32 * sizeof(double));
+  unsigned long long* acci =
+      reinterpret_cast<unsigned long long*>(wbase + kCandBytes + 9 * 3 * 32 * sizeof(double));
 
   bool active = gcell < total_cells;
   int f = 0, cr = 0, cc = 0;
@@ -193,7 +183,7 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
       cyt = 0.f;
     }
     cand[t] = cp;
-    cyv[t] = cyt;
+    cand_k[t] = kr * p.ns_c + kc;  // only read for in-grid winners
   }
   // cell-wide maxima over the 9 staging lanes
 #pragma unroll
@@ -213,7 +203,7 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
       accd[(t * 3 + 0) * 32 + lane] = 0.0;
       accd[(t * 3 + 1) * 32 + lane] = 0.0;
       accd[(t * 3 + 2) * 32 + lane] = 0.0;
-      acci[t * 32 + lane] = 0u;
+      acci[t * 32 + lane] = 0ull;
     }
   }
   __syncwarp();
@@ -291,7 +281,7 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
         const float thr = __fmaf_rn(f2v, p.k_rel, __fmaf_rn(mp, p.k_mp, two_a_cell));
         const float gap = __fsub_rn(f2v, __uint_as_float(k1[i]));
         int t = (int)(k1[i] & 15u);
-        int k = (cr + off_r(t)) * p.ns_c + (cc + off_c(t));
+        int k = cand_k[t];
         if (!(gap > thr) || !(mp < 1e15f)) {
           k = exact_argmin(p.cxy + (long long)f * K * 2, p.clab + (long long)f * K * 3, L[i], A[i],
                            B[i], x + i, y, cr, cc, p.ns_r, p.ns_c, p.xy_weight);
@@ -305,7 +295,9 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
           d[0] = dadd(d[0], (double)L[i]);
           d[32] = dadd(d[32], (double)A[i]);
           d[64] = dadd(d[64], (double)B[i]);
-          acci[t * 32 + lane] += 1u | (fl << 6) | ((unsigned)(c4 + i) << 12) | ((unsigned)row << 22);
+          acci[t * 32 + lane] += 1ull | ((unsigned long long)fl << 11) |
+                                 ((unsigned long long)(c4 + i) << 22) |
+                                 ((unsigned long long)row << 43);
         }
       }
       *reinterpret_cast<int4*>(p.labels + pix) = make_int4(lab4[0], lab4[1], lab4[2], lab4[3]);
@@ -314,30 +306,32 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   if (!ACC) return;
   __syncwarp();
   // ---- per-cell column reduction: 9 slots x (3 colour + 1 packed int) -------
-  // column c < 27: colour (slot c/3, channel c%3); 27 <= c < 36: ints of slot c-27
+  // column c < 27: colour (slot c/3, channel c%3); 27 <= c < 36: ints of slot
+  // c-27.  Each column holds lpc lane entries, read as 16-byte vectors.
   const int lane0 = ci * lpc;
-  for (int col = ll; col < 36; col += lpc) {
-    if (!active) break;
-    if (col < 27) {
-      const double* src = accd + col * 32 + lane0;
-      double sacc = 0.0;
-      for (int q = 0; q < lpc; ++q) sacc = dadd(sacc, src[q]);
-      p.part[gcell * 9 + col / 3].s[col % 3] = sacc;
-    } else {
-      const uint32_t* src = acci + (col - 27) * 32 + lane0;
-      int cnt = 0, fl = 0, sx = 0, sy = 0;
-      for (int q = 0; q < lpc; ++q) {
-        const uint32_t v = src[q];
-        cnt += v & 63u;
-        fl += (v >> 6) & 63u;
-        sx += (v >> 12) & 1023u;
-        sy += v >> 22;
+  if (active) {
+    for (int col = ll; col < 36; col += lpc) {
+      if (col < 27) {
+        const double2* src = reinterpret_cast<const double2*>(accd + col * 32 + lane0);
+        double sacc = 0.0;
+        for (int q = 0; q < lpc / 2; ++q) {
+          const double2 v = src[q];
+          sacc = dadd(dadd(sacc, v.x), v.y);
+        }
+        p.part[gcell * 9 + col / 3].s[col % 3] = sacc;
+      } else {
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(acci + (col - 27) * 32 + lane0);
+        unsigned long long tot = 0;
+        for (int q = 0; q < lpc / 2; ++q) {
+          const ulonglong2 v = src[q];
+          tot += v.x + v.y;  // fields cannot overflow (see packing above)
+        }
+        Part* o = p.part + gcell * 9 + (col - 27);
+        o->cnt = (int)(tot & 2047ull);
+        o->flag = (int)((tot >> 11) & 2047ull);
+        o->sx = (int)((tot >> 22) & 0x1FFFFFull);
+        o->sy = (int)(tot >> 43);
       }
-      Part* o = p.part + gcell * 9 + (col - 27);
-      o->sx = sx;
-      o->sy = sy;
-      o->cnt = cnt;
-      o->flag = fl;
     }
   }
 }
@@ -364,34 +358,6 @@ __global__ void k_records(const double* __restrict__ cxy, const double* __restri
   r.mag_xy = fmaxf(fabsf(r.xr), fabsf(r.yr));
   r.ok = ok ? 1.f : 0.f;
   rec[i] = r;
-}
-
-// Reference strip fold for one (cluster, strip): _core.pyx:221-255 verbatim
-// order (row-major, binary64 colour, integer x/y/count).
-__device__ void strip_fold(const LabView im, const int32_t* __restrict__ lab, int h,
-                           int w, int k, int j, int s, int ns_c, int tile_len, double out[6]) {
-  int r = k / ns_c, c = k % ns_c;
-  int wx0 = max((c - 1) * s, 0), wx1 = min((c + 2) * s, w);
-  int ry0 = (r - 1) * s, ry1 = min((r + 2) * s, h);
-  int sy0 = max(ry0 + j * tile_len, 0), sy1 = min(ry0 + (j + 1) * tile_len, ry1);
-  double sl = 0.0, sa = 0.0, sb = 0.0;
-  long long sx = 0, sy = 0, cnt = 0;
-  for (int y = sy0; y < sy1; ++y)
-    for (int x = wx0; x < wx1; ++x)
-      if (__ldg(lab + (long long)y * w + x) == k) {
-        sl = dadd(sl, (double)im.get(y, x, 0));
-        sa = dadd(sa, (double)im.get(y, x, 1));
-        sb = dadd(sb, (double)im.get(y, x, 2));
-        sx += x;
-        sy += y;
-        cnt += 1;
-      }
-  out[0] = sl;
-  out[1] = sa;
-  out[2] = sb;
-  out[3] = (double)sx;
-  out[4] = (double)sy;
-  out[5] = (double)cnt;
 }
 
 struct ReduceParams {
@@ -486,7 +452,9 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
     if (!flagged)
       write_centre(p, gk, kr, kc, (double)cnt, s0, s1, s2, (double)sx, (double)sy);
   }
-  // exact fallback for flagged clusters, one at a time per warp
+  // exact fallback for flagged clusters, one at a time per warp: the warp
+  // scans each strip row 32 labels at a time (coalesced) and lane 0 folds the
+  // matches in the reference's row-major order (_core.pyx:233-243).
   unsigned need = __ballot_sync(0xFFFFFFFFu, flagged);
   while (need) {
     const int src = __ffs(need) - 1;
@@ -495,10 +463,51 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
     const int ff = __shfl_sync(0xFFFFFFFFu, f, src);
     const LabView im{p.img + (long long)ff * p.h * p.w * 3, p.w, (long long)p.h * p.w, true};
     const int32_t* lb = p.labels + (long long)ff * p.h * p.w;
-    if (lane < p.n_bl) strip_fold(im, lb, p.h, p.w, fk, lane, p.s, p.ns_c, p.tile_len, strips[warp][lane]);
+    const int r = fk / p.ns_c, c = fk % p.ns_c;
+    const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
+    const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
+    double (*sk)[6] = strips[warp];
+    for (int j = 0; j < p.n_bl; ++j) {
+      const int sy0 = max(ry0 + j * p.tile_len, 0), sy1 = min(ry0 + (j + 1) * p.tile_len, ry1);
+      double sl = 0.0, sa = 0.0, sb = 0.0;
+      long long sx = 0, sy = 0, cnt = 0;
+      for (int y = sy0; y < sy1; ++y) {
+        for (int x0 = wx0; x0 < wx1; x0 += 32) {
+          const int x = x0 + lane;
+          const bool match = x < wx1 && __ldg(lb + (long long)y * p.w + x) == fk;
+          unsigned m = __ballot_sync(0xFFFFFFFFu, match);
+          float vl = 0.f, va = 0.f, vb = 0.f;
+          if (match) {
+            vl = im.get(y, x, 0);
+            va = im.get(y, x, 1);
+            vb = im.get(y, x, 2);
+          }
+          while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            const float ql = __shfl_sync(0xFFFFFFFFu, vl, b);
+            const float qa = __shfl_sync(0xFFFFFFFFu, va, b);
+            const float qb = __shfl_sync(0xFFFFFFFFu, vb, b);
+            sl = dadd(sl, (double)ql);
+            sa = dadd(sa, (double)qa);
+            sb = dadd(sb, (double)qb);
+            sx += x0 + b;
+            sy += y;
+            cnt += 1;
+          }
+        }
+      }
+      if (lane == 0) {
+        sk[j][0] = sl;
+        sk[j][1] = sa;
+        sk[j][2] = sb;
+        sk[j][3] = (double)sx;
+        sk[j][4] = (double)sy;
+        sk[j][5] = (double)cnt;
+      }
+    }
     __syncwarp();
     if (lane == 0) {
-      double (*sk)[6] = strips[warp];
       int m = p.n_bl;
       while (m > 1) {  // pairwise tree, _core.pyx:301-311
         int half = m >> 1;
@@ -508,8 +517,8 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
           for (int comp = 0; comp < 6; ++comp) sk[half][comp] = sk[m - 1][comp];
         m = half + (m & 1);
       }
-      write_centre(p, (long long)ff * K + fk, fk / p.ns_c, fk % p.ns_c, sk[0][5], sk[0][0], sk[0][1],
-                   sk[0][2], sk[0][3], sk[0][4]);
+      write_centre(p, (long long)ff * K + fk, r, c, sk[0][5], sk[0][0], sk[0][1], sk[0][2],
+                   sk[0][3], sk[0][4]);
     }
     __syncwarp();
   }
