@@ -43,11 +43,6 @@ __device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigne
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
-__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
-  unsigned long long r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
 __device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b,
                                                    unsigned long long c) {
   unsigned long long r;
@@ -82,6 +77,7 @@ struct CellParams {
   int lanes_per_cell;      // 32 or 16
   int runs_per_row;        // S / 4
   int runs;                // S * S / 4
+  unsigned row_magic;      // ceil(2^16 / runs_per_row)
   double xy_weight;
   float w32, k_mp, k_mc, k_xy, k_const, k_rel;
   float tau;               // certified-sum lower magnitude
@@ -135,8 +131,10 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   const int ci = lane / lpc, ll = lane % lpc;  // cell within warp, lane within cell
   const int S = p.s;
   const int K = p.ns_r * p.ns_c;
-  const long long gcell = ((long long)blockIdx.x * kWarps + warp) * cpw + ci;
-  const long long total_cells = (long long)K * p.frames;
+  // grid: x = cell groups of one frame, y = frame (no 64-bit divisions)
+  const int f = blockIdx.y;
+  const int cell = (blockIdx.x * kWarps + warp) * cpw + ci;
+  const long long gcell = (long long)f * K + cell;
   unsigned char* wbase = smem + (size_t)warp * (ACC ? kWarpSmemAcc : kWarpSmemNoAcc);
   CandPairs* cand = reinterpret_cast<CandPairs*>(wbase) + ci * 9;
   int* cand_k = reinterpret_cast<int*>(wbase + sizeof(CandPairs) * 18) + ci * 9;
@@ -144,14 +142,11 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   unsigned long long* acci =
       reinterpret_cast<unsigned long long*>(wbase + kCandBytes + 9 * 3 * 32 * sizeof(double));
 
-  bool active = gcell < total_cells;
-  int f = 0, cr = 0, cc = 0;
+  bool active = cell < K && !(p.done && p.done[f] == 1);
+  int cr = 0, cc = 0;
   if (active) {
-    f = (int)(gcell / K);
-    const int cell = (int)(gcell % K);
     cr = cell / p.ns_c;
-    cc = cell % p.ns_c;
-    if (p.done && p.done[f] == 1) active = false;
+    cc = cell - cr * p.ns_c;
   }
 
   // ---- stage the 9 candidates (lanes ll < 9 of each cell) ------------------
@@ -197,14 +192,10 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   mxy = __shfl_sync(0xFFFFFFFFu, mxy, ci * lpc);
   okf = __shfl_sync(0xFFFFFFFFu, okf, ci * lpc);
   if (ACC) {
-    // zero this lane's private accumulators
+    // zero the warp's accumulator block cooperatively with 16-byte stores
+    float4* z = reinterpret_cast<float4*>(accd);
 #pragma unroll
-    for (int t = 0; t < 9; ++t) {
-      accd[(t * 3 + 0) * 32 + lane] = 0.0;
-      accd[(t * 3 + 1) * 32 + lane] = 0.0;
-      accd[(t * 3 + 2) * 32 + lane] = 0.0;
-      acci[t * 32 + lane] = 0ull;
-    }
+    for (int i = lane; i < (int)(kAccBytes / 16); i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncwarp();
 
@@ -216,17 +207,39 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   const long long img_base = (long long)f * p.h * p.w;
 
   if (active) {
+    const long long hw = (long long)p.h * p.w;
+    const float* fimg = p.img + (long long)f * 3 * hw;
+    // row = j / runs_per_row via a 16-bit reciprocal (exact for j <= 256, rpr <= 8)
+    const unsigned rmag = p.row_magic;
+    auto run_ok = [&](int jj, int& row, int& c4) {
+      row = (int)(((unsigned)jj * rmag) >> 16);
+      c4 = (jj - row * p.runs_per_row) * 4;
+      return jj < p.runs && y_cell + row < p.h && x_cell + c4 < p.w;
+    };
+    int row_n, c4_n;
+    bool ok_n = run_ok(ll, row_n, c4_n);
+    float4 Ln = make_float4(0.f, 0.f, 0.f, 0.f), An = Ln, Bn = Ln;
+    if (ok_n) {
+      const float* q = fimg + (long long)(y_cell + row_n) * p.w + x_cell + c4_n;
+      Ln = __ldg(reinterpret_cast<const float4*>(q));
+      An = __ldg(reinterpret_cast<const float4*>(q + hw));
+      Bn = __ldg(reinterpret_cast<const float4*>(q + 2 * hw));
+    }
     for (int j = ll; j < p.runs; j += lpc) {
-      const int row = j / p.runs_per_row;
-      const int c4 = (j - row * p.runs_per_row) * 4;
+      const int row = row_n, c4 = c4_n;
+      const bool ok = ok_n;
+      const float4 Lv = Ln, Av = An, Bv = Bn;
+      // prefetch the next run of this lane (software pipelining)
+      ok_n = run_ok(j + lpc, row_n, c4_n);
+      if (ok_n) {
+        const float* q = fimg + (long long)(y_cell + row_n) * p.w + x_cell + c4_n;
+        Ln = __ldg(reinterpret_cast<const float4*>(q));
+        An = __ldg(reinterpret_cast<const float4*>(q + hw));
+        Bn = __ldg(reinterpret_cast<const float4*>(q + 2 * hw));
+      }
+      if (!ok) continue;
       const int y = y_cell + row, x = x_cell + c4;
-      if (y >= p.h || x >= p.w) continue;
       const long long pix = img_base + (long long)y * p.w + x;   // label index
-      const long long pl = (long long)f * 3 * p.h * p.w + (long long)y * p.w + x;  // planar Lab
-      const long long hw = (long long)p.h * p.w;
-      const float4 Lv = __ldg(reinterpret_cast<const float4*>(p.img + pl));
-      const float4 Av = __ldg(reinterpret_cast<const float4*>(p.img + pl + hw));
-      const float4 Bv = __ldg(reinterpret_cast<const float4*>(p.img + pl + 2 * hw));
       const float L[4] = {Lv.x, Lv.y, Lv.z, Lv.w};
       const float A[4] = {Av.x, Av.y, Av.z, Av.w};
       const float B[4] = {Bv.x, Bv.y, Bv.z, Bv.w};
@@ -371,6 +384,8 @@ struct ReduceParams {
   int64_t* counts;
   CRec* rec;
   const int32_t* done;
+  int32_t* worklist;       // flagged clusters (global index f*K + k)
+  int32_t* worklist_n;
   int h, w, s, ns_r, ns_c, frames, n_bl, tile_len;
 };
 
@@ -413,8 +428,6 @@ __device__ __forceinline__ void write_centre(const ReduceParams& p, long long gk
 // belong to it.  Clusters with a flagged member are recomputed by the whole
 // warp with the reference strip folds + pairwise strip tree (_core.pyx:300-311).
 __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
-  __shared__ double strips[4][32][6];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.ns_r * p.ns_c;
   const long long gk = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in = gk < (long long)K * p.frames;
@@ -452,15 +465,22 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
     if (!flagged)
       write_centre(p, gk, kr, kc, (double)cnt, s0, s1, s2, (double)sx, (double)sy);
   }
-  // exact fallback for flagged clusters, one at a time per warp: the warp
-  // scans each strip row 32 labels at a time (coalesced) and lane 0 folds the
-  // matches in the reference's row-major order (_core.pyx:233-243).
-  unsigned need = __ballot_sync(0xFFFFFFFFu, flagged);
-  while (need) {
-    const int src = __ffs(need) - 1;
-    need &= need - 1;
-    const int fk = __shfl_sync(0xFFFFFFFFu, k, src);
-    const int ff = __shfl_sync(0xFFFFFFFFu, f, src);
+  if (flagged) p.worklist[atomicAdd(p.worklist_n, 1)] = (int32_t)gk;
+}
+
+// Exact recomputation of flagged clusters (certificate failed): one warp per
+// cluster.  The warp scans each strip row 32 labels at a time (coalesced) and
+// lane 0 folds the matches in the reference's row-major order
+// (_core.pyx:233-243), then applies the pairwise strip tree (_core.pyx:300-311).
+__global__ void __launch_bounds__(128) k_exact_clusters(ReduceParams p) {
+  __shared__ double strips[4][32][6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = p.ns_r * p.ns_c;
+  const int n = *p.worklist_n;
+  const int nwarps = gridDim.x * 4;
+  for (int item = blockIdx.x * 4 + warp; item < n; item += nwarps) {
+    const int gk = p.worklist[item];
+    const int ff = gk / K, fk = gk - ff * K;
     const LabView im{p.img + (long long)ff * p.h * p.w * 3, p.w, (long long)p.h * p.w, true};
     const int32_t* lb = p.labels + (long long)ff * p.h * p.w;
     const int r = fk / p.ns_c, c = fk % p.ns_c;
@@ -509,7 +529,7 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
     __syncwarp();
     if (lane == 0) {
       int m = p.n_bl;
-      while (m > 1) {  // pairwise tree, _core.pyx:301-311
+      while (m > 1) {
         int half = m >> 1;
         for (int i = 0; i < half; ++i)
           for (int comp = 0; comp < 6; ++comp) sk[i][comp] = dadd(sk[2 * i][comp], sk[2 * i + 1][comp]);
@@ -517,8 +537,7 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
           for (int comp = 0; comp < 6; ++comp) sk[half][comp] = sk[m - 1][comp];
         m = half + (m & 1);
       }
-      write_centre(p, (long long)ff * K + fk, r, c, sk[0][5], sk[0][0], sk[0][1], sk[0][2],
-                   sk[0][3], sk[0][4]);
+      write_centre(p, gk, r, c, sk[0][5], sk[0][0], sk[0][1], sk[0][2], sk[0][3], sk[0][4]);
     }
     __syncwarp();
   }
@@ -567,7 +586,8 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.frames = frames;
   p.runs = (int)(s * s / 4);
   p.runs_per_row = (int)(s / 4);
-  p.lanes_per_cell = p.runs >= 32 ? 32 : 16;
+  p.row_magic = (unsigned)((65536 + p.runs_per_row - 1) / p.runs_per_row);
+  p.lanes_per_cell = 16;  // two cells per warp; 9 staging lanes per cell
   p.xy_weight = xy_weight;
   assoc_bound_coefficients(xy_weight, p.w32, p.k_mp, p.k_mc, p.k_xy, p.k_const, p.k_rel);
   // tau = 2^k with 9 S^2 <= 2^(23 + k)  (certified sums, see header)
@@ -575,9 +595,12 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   while ((double)std::ldexp(1.0, 23 + kexp) < 9.0 * (double)(s * s)) ++kexp;
   p.tau = (float)std::ldexp(1.0, kexp);
   const int cpw = 32 / p.lanes_per_cell;
-  const long long cells = ns_r * ns_c * (long long)frames;
-  const long long warps = ceil_div(cells, cpw);
-  const unsigned blocks = (unsigned)ceil_div(warps, kWarps);
+  const long long warps = ceil_div(ns_r * ns_c, cpw);
+  const dim3 blocks((unsigned)ceil_div(warps, kWarps), (unsigned)frames);
+  if (frames > 65535) {
+    set_error("k_cell: at most 65535 frames per launch");
+    return SPX_ERR_VALUE;
+  }
   const size_t smem = cell_smem_bytes(s, acc);
   if (acc) {
     static size_t configured = 0;
@@ -606,8 +629,9 @@ int launch_records(const double* cxy, const double* clab, CRec* rec, int64_t ns_
 int launch_reduce_cells(const Part* part, const float* img, const int32_t* labels,
                         const double* prev_xy, const double* prev_lab, double* out_xy,
                         double* out_lab, int64_t* counts, CRec* rec, const int32_t* done,
-                        int64_t h, int64_t w, int64_t s, int64_t ns_r, int64_t ns_c,
-                        int64_t tile_len, int frames, cudaStream_t st) {
+                        int32_t* worklist, int32_t* worklist_n, int64_t h, int64_t w, int64_t s,
+                        int64_t ns_r, int64_t ns_c, int64_t tile_len, int frames,
+                        cudaStream_t st) {
   ReduceParams p;
   p.part = part;
   p.img = img;
@@ -619,6 +643,8 @@ int launch_reduce_cells(const Part* part, const float* img, const int32_t* label
   p.counts = counts;
   p.rec = rec;
   p.done = done;
+  p.worklist = worklist;
+  p.worklist_n = worklist_n;
   p.h = (int)h;
   p.w = (int)w;
   p.s = (int)s;
@@ -628,8 +654,11 @@ int launch_reduce_cells(const Part* part, const float* img, const int32_t* label
   p.n_bl = (int)ceil_div(3 * s, tile_len);
   p.tile_len = (int)tile_len;
   long long n = ns_r * ns_c * (long long)frames;
+  SPX_CUDA(cudaMemsetAsync(worklist_n, 0, sizeof(int32_t), st));
   k_reduce_cells<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_reduce_cells");
+  k_exact_clusters<<<(unsigned)num_sms() * 8, 128, 0, st>>>(p);
+  SPX_LAUNCH_CHECK("k_exact_clusters");
   return SPX_OK;
 }
 

@@ -35,8 +35,8 @@ int launch_cell(const float*, const double*, const double*, const CRec*, int32_t
 int launch_records(const double*, const double*, CRec*, int64_t, int64_t, int64_t, int,
                    cudaStream_t);
 int launch_reduce_cells(const Part*, const float*, const int32_t*, const double*, const double*,
-                        double*, double*, int64_t*, CRec*, const int32_t*, int64_t, int64_t,
-                        int64_t, int64_t, int64_t, int64_t, int, cudaStream_t);
+                        double*, double*, int64_t*, CRec*, const int32_t*, int32_t*, int32_t*,
+                        int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t);
 int launch_fill_i32(int32_t*, int, int, cudaStream_t);
 
 namespace {
@@ -78,6 +78,7 @@ struct Engine {
   int32_t *cc_parent = nullptr, *cc_size = nullptr, *cc_nxt = nullptr, *cc_first = nullptr;
   CRec* rec = nullptr;   // fp32 filter records of the current centres (cell path)
   Part* part = nullptr;  // per (cell, slot) partial sums (cell path)
+  int32_t* worklist = nullptr;  // flagged clusters for the exact fallback (cell path)
   bool use_cell = false;
   uint8_t* d_rgb = nullptr;  // staging for the host-buffer entry point
   int32_t* d_labels = nullptr;
@@ -95,7 +96,7 @@ struct Engine {
     for (void* p : {(void*)lab, (void*)labels, (void*)scratch, (void*)cxy[0], (void*)cxy[1],
                     (void*)clab[0], (void*)clab[1], (void*)slab, (void*)done, (void*)passes,
                     (void*)cc_parent, (void*)cc_size, (void*)cc_nxt, (void*)cc_first,
-                    (void*)rec, (void*)part, (void*)d_rgb, (void*)d_labels, (void*)d_cxy, (void*)d_clab, (void*)d_counts,
+                    (void*)rec, (void*)part, (void*)worklist, (void*)d_rgb, (void*)d_labels, (void*)d_cxy, (void*)d_clab, (void*)d_counts,
                     (void*)d_passes})
       if (p) cudaFree(p);
     for (auto& e : ev)
@@ -134,6 +135,7 @@ struct Engine {
     if (use_cell) {
       SPX_CUDA(cudaMalloc(&rec, B * K * sizeof(CRec)));
       SPX_CUDA(cudaMalloc(&part, B * K * 9 * sizeof(Part)));
+      SPX_CUDA(cudaMalloc(&worklist, (B * K + 1) * sizeof(int32_t)));
     } else {
       SPX_CUDA(cudaMalloc(&slab, B * K * n_bl * 6 * sizeof(double)));
     }
@@ -214,10 +216,11 @@ struct Engine {
       cudaEventRecord(pass_event(ev_update, 2 * n_update), s);
       if (use_cell) {
         if ((rc = launch_reduce_cells(part, lab, labels, cxy[cur], clab[cur], cxy[nxt], clab[nxt],
-                                      out_counts, rec, dn, st.height, st.width, st.s, st.ns_r,
-                                      st.ns_c, st.tile_len, B, s)))
+                                      out_counts, rec, dn, worklist, worklist + max_batch * K,
+                                      st.height, st.width, st.s, st.ns_r, st.ns_c, st.tile_len, B,
+                                      s)))
           return rc;
-        launches += 1;
+        launches += 2;
       } else {
         if ((rc = launch_accum_range(lab, labels, st.height, st.width, slab, n_bl, st.s, st.ns_c,
                                      st.tile_len, 0, K, K, B, dn, s)))
