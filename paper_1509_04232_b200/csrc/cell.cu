@@ -469,65 +469,93 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
 }
 
 // Exact recomputation of flagged clusters (certificate failed): one warp per
-// cluster.  The warp scans each strip row 32 labels at a time (coalesced) and
-// lane 0 folds the matches in the reference's row-major order
-// (_core.pyx:233-243), then applies the pairwise strip tree (_core.pyx:300-311).
+// cluster.  The cluster's 3Sx3S window is processed in chunks of up to
+// kExactChunk pixels: all lanes load labels and, for matches, the Lab values
+// into shared memory in parallel (one memory round trip per chunk); then
+// lane 0 folds the matches in the reference's row-major order into the
+// strip sums (_core.pyx:221-255) and finally applies the pairwise strip tree
+// (_core.pyx:300-311).  Labels come from the same association pass, so the
+// window contains every member (no spill on pipeline labels).
+constexpr int kExactChunk = 512;
+
 __global__ void __launch_bounds__(128) k_exact_clusters(ReduceParams p) {
   __shared__ double strips[4][32][6];
+  __shared__ float4 vals[4][kExactChunk];
+  __shared__ unsigned masks[4][kExactChunk / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.ns_r * p.ns_c;
   const int n = *p.worklist_n;
   const int nwarps = gridDim.x * 4;
+  double (*sk)[6] = strips[warp];
   for (int item = blockIdx.x * 4 + warp; item < n; item += nwarps) {
     const int gk = p.worklist[item];
     const int ff = gk / K, fk = gk - ff * K;
-    const LabView im{p.img + (long long)ff * p.h * p.w * 3, p.w, (long long)p.h * p.w, true};
-    const int32_t* lb = p.labels + (long long)ff * p.h * p.w;
+    const float* im = p.img + (long long)ff * p.h * p.w * 3;  // planar [3][H][W]
+    const long long hw = (long long)p.h * p.w;
+    const int32_t* lb = p.labels + (long long)ff * hw;
     const int r = fk / p.ns_c, c = fk % p.ns_c;
     const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
     const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
-    double (*sk)[6] = strips[warp];
-    for (int j = 0; j < p.n_bl; ++j) {
-      const int sy0 = max(ry0 + j * p.tile_len, 0), sy1 = min(ry0 + (j + 1) * p.tile_len, ry1);
-      double sl = 0.0, sa = 0.0, sb = 0.0;
-      long long sx = 0, sy = 0, cnt = 0;
-      for (int y = sy0; y < sy1; ++y) {
-        for (int x0 = wx0; x0 < wx1; x0 += 32) {
-          const int x = x0 + lane;
-          const bool match = x < wx1 && __ldg(lb + (long long)y * p.w + x) == fk;
-          unsigned m = __ballot_sync(0xFFFFFFFFu, match);
-          float vl = 0.f, va = 0.f, vb = 0.f;
-          if (match) {
-            vl = im.get(y, x, 0);
-            va = im.get(y, x, 1);
-            vb = im.get(y, x, 2);
-          }
-          while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            const float ql = __shfl_sync(0xFFFFFFFFu, vl, b);
-            const float qa = __shfl_sync(0xFFFFFFFFu, va, b);
-            const float qb = __shfl_sync(0xFFFFFFFFu, vb, b);
-            sl = dadd(sl, (double)ql);
-            sa = dadd(sa, (double)qa);
-            sb = dadd(sb, (double)qb);
-            sx += x0 + b;
+    const int ya = max(ry0, 0);
+    const int ww = wx1 - wx0;
+    const int rows_per_chunk = max(1, kExactChunk / ww);
+    if (lane < p.n_bl)
+      for (int comp = 0; comp < 6; ++comp) sk[lane][comp] = 0.0;
+    // running strip state lives in lane 0's registers
+    int cur_j = -1;
+    double sl = 0.0, sa = 0.0, sb = 0.0;
+    long long sx = 0, sy = 0, cnt = 0;
+    for (int yc = ya; yc < ry1; yc += rows_per_chunk) {
+      const int rows = min(rows_per_chunk, ry1 - yc);
+      const int npx = rows * ww;
+      for (int base = 0; base < npx; base += 32) {
+        const int idx = base + lane;
+        bool m = false;
+        if (idx < npx) {
+          const int y = yc + idx / ww, x = wx0 + idx % ww;
+          const long long q = (long long)y * p.w + x;
+          m = __ldg(lb + q) == fk;
+          if (m) vals[warp][idx] = make_float4(__ldg(im + q), __ldg(im + hw + q), __ldg(im + 2 * hw + q), 0.f);
+        }
+        const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
+        if (lane == 0) masks[warp][base >> 5] = bm;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        for (int wv = 0; wv * 32 < npx; ++wv) {
+          unsigned bm = masks[warp][wv];
+          while (bm) {
+            const int b = __ffs(bm) - 1;
+            bm &= bm - 1;
+            const int idx = wv * 32 + b;
+            const int y = yc + idx / ww, x = wx0 + idx % ww;
+            const int j = (y - ry0) / p.tile_len;
+            if (j != cur_j) {
+              if (cur_j >= 0) {
+                sk[cur_j][0] = sl; sk[cur_j][1] = sa; sk[cur_j][2] = sb;
+                sk[cur_j][3] = (double)sx; sk[cur_j][4] = (double)sy; sk[cur_j][5] = (double)cnt;
+              }
+              cur_j = j;
+              sl = sa = sb = 0.0;
+              sx = sy = cnt = 0;
+            }
+            const float4 v = vals[warp][idx];
+            sl = dadd(sl, (double)v.x);
+            sa = dadd(sa, (double)v.y);
+            sb = dadd(sb, (double)v.z);
+            sx += x;
             sy += y;
             cnt += 1;
           }
         }
       }
-      if (lane == 0) {
-        sk[j][0] = sl;
-        sk[j][1] = sa;
-        sk[j][2] = sb;
-        sk[j][3] = (double)sx;
-        sk[j][4] = (double)sy;
-        sk[j][5] = (double)cnt;
-      }
+      __syncwarp();
     }
-    __syncwarp();
     if (lane == 0) {
+      if (cur_j >= 0) {
+        sk[cur_j][0] = sl; sk[cur_j][1] = sa; sk[cur_j][2] = sb;
+        sk[cur_j][3] = (double)sx; sk[cur_j][4] = (double)sy; sk[cur_j][5] = (double)cnt;
+      }
       int m = p.n_bl;
       while (m > 1) {
         int half = m >> 1;

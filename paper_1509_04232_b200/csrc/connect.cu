@@ -65,35 +65,77 @@ __global__ void __launch_bounds__(WTW* WTH) k_weak1(const int32_t* __restrict__ 
   dst[y * w + x] = weak_rule(t, w, h, x, y, P, threadIdx.x + 1, threadIdx.y + 1);
 }
 
-// Both passes fused; frames of a batch along blockIdx.z.
-__global__ void __launch_bounds__(WTW* WTH) k_weak2(const int32_t* __restrict__ src,
-                                                     int32_t* __restrict__ dst, int64_t h,
-                                                     int64_t w) {
-  constexpr int P0 = WTW + 4, R0 = WTH + 4;  // source tile, 2-px halo
-  constexpr int P1 = WTW + 2, R1 = WTH + 2;  // pass-1 tile, 1-px halo
-  __shared__ int32_t t0[R0 * P0];
+// Both passes fused; frames of a batch along blockIdx.z.  Output tile
+// WT2W x WT2H per CTA of 256 threads; the source tile (2-pixel halo) is
+// loaded with 16-byte loads for the aligned interior, pass 1 is evaluated on
+// the tile plus a 1-pixel halo in shared memory, pass 2 on the tile, and the
+// result leaves as 16-byte stores.  32-bit indexing (frames < 2^31 px).
+constexpr int WT2W = 128, WT2H = 16;
+
+__device__ __forceinline__ int32_t weak_rule_g(const int32_t* t, int pitch, int lx, int ly, int x,
+                                               int y, int w, int h) {
+  const int32_t v = t[ly * pitch + lx];
+  const int32_t left = t[ly * pitch + lx - 1], right = t[ly * pitch + lx + 1];
+  const int32_t up = t[(ly - 1) * pitch + lx], down = t[(ly + 1) * pitch + lx];
+  const bool hl = x > 0, hr = x < w - 1, hu = y > 0, hd = y < h - 1;
+  if ((hl && left == v) || (hr && right == v) || (hu && up == v) || (hd && down == v)) return v;
+  return hl ? left : (hu ? up : v);
+}
+
+__global__ void __launch_bounds__(256) k_weak2(const int32_t* __restrict__ src,
+                                               int32_t* __restrict__ dst, int h, int w) {
+  constexpr int P0 = WT2W + 8, R0 = WT2H + 4;  // source tile: 4-col / 2-row halo
+  constexpr int P1 = WT2W + 2, R1 = WT2H + 2;  // pass-1 tile: 1-px halo
+  __shared__ __align__(16) int32_t t0[R0 * P0];
   __shared__ int32_t t1[R1 * P1];
-  const int64_t f = blockIdx.z;
-  const int32_t* s = src + f * h * w;
-  int32_t* d = dst + f * h * w;
-  int64_t tx0 = (int64_t)blockIdx.x * WTW, ty0 = (int64_t)blockIdx.y * WTH;
-  const int tid = threadIdx.y * WTW + threadIdx.x;
-  for (int i = tid; i < R0 * P0; i += WTW * WTH) {
-    int ly = i / P0, lx = i % P0;
-    int64_t y = ty0 + ly - 2, x = tx0 + lx - 2;
-    t0[i] = (y >= 0 && y < h && x >= 0 && x < w) ? __ldg(s + y * w + x) : 0;
+  const long long fo = (long long)blockIdx.z * h * w;
+  const int32_t* s = src + fo;
+  int32_t* d = dst + fo;
+  const int tx0 = blockIdx.x * WT2W, ty0 = blockIdx.y * WT2H;
+  const int tid = threadIdx.x;
+  const bool vec = (w & 3) == 0;
+  // load: tile columns [tx0-4, tx0+WT2W+4), rows [ty0-2, ty0+WT2H+2)
+  for (int i = tid; i < R0 * (P0 / 4); i += 256) {
+    const int ly = i / (P0 / 4), lq = i % (P0 / 4);
+    const int y = ty0 + ly - 2, x = tx0 - 4 + lq * 4;
+    int4 v = make_int4(0, 0, 0, 0);
+    if (y >= 0 && y < h) {
+      if (vec && x >= 0 && x + 4 <= w) {
+        v = __ldg(reinterpret_cast<const int4*>(s + (long long)y * w + x));
+      } else {
+        const int32_t* row = s + (long long)y * w;
+        v.x = (x >= 0 && x < w) ? __ldg(row + x) : 0;
+        v.y = (x + 1 >= 0 && x + 1 < w) ? __ldg(row + x + 1) : 0;
+        v.z = (x + 2 >= 0 && x + 2 < w) ? __ldg(row + x + 2) : 0;
+        v.w = (x + 3 >= 0 && x + 3 < w) ? __ldg(row + x + 3) : 0;
+      }
+    }
+    *reinterpret_cast<int4*>(t0 + ly * P0 + lq * 4) = v;
   }
   __syncthreads();
-  for (int i = tid; i < R1 * P1; i += WTW * WTH) {
-    int ly = i / P1, lx = i % P1;
-    int64_t y = ty0 + ly - 1, x = tx0 + lx - 1;
-    t1[i] = (y >= 0 && y < h && x >= 0 && x < w) ? weak_rule(t0, w, h, x, y, P0, lx + 1, ly + 1)
-                                                 : 0;
+  for (int i = tid; i < R1 * P1; i += 256) {
+    const int ly = i / P1, lx = i % P1;
+    const int y = ty0 + ly - 1, x = tx0 + lx - 1;
+    t1[i] = (y >= 0 && y < h && x >= 0 && x < w) ? weak_rule_g(t0, P0, lx + 3, ly + 1, x, y, w, h) : 0;
   }
   __syncthreads();
-  int64_t x = tx0 + threadIdx.x, y = ty0 + threadIdx.y;
-  if (x >= w || y >= h) return;
-  d[y * w + x] = weak_rule(t1, w, h, x, y, P1, threadIdx.x + 1, threadIdx.y + 1);
+  // pass 2: each thread writes 4 consecutive pixels of one row (x2 rows)
+  for (int i = tid; i < WT2H * (WT2W / 4); i += 256) {
+    const int ly = i / (WT2W / 4), lq = i % (WT2W / 4);
+    const int y = ty0 + ly, x = tx0 + lq * 4;
+    if (y >= h) continue;
+    int o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      o[k] = (x + k < w) ? weak_rule_g(t1, P1, lq * 4 + k + 1, ly + 1, x + k, y, w, h) : 0;
+    int32_t* out = d + (long long)y * w + x;
+    if (vec && x + 4 <= w) {
+      *reinterpret_cast<int4*>(out) = make_int4(o[0], o[1], o[2], o[3]);
+    } else {
+      for (int k = 0; k < 4; ++k)
+        if (x + k < w) out[k] = o[k];
+    }
+  }
 }
 
 // ---- strict -------------------------------------------------------------------
@@ -212,8 +254,12 @@ int launch_weak1(const int32_t* src, int32_t* dst, int64_t h, int64_t w, int64_t
 int launch_weak2(const int32_t* src, int32_t* dst, int64_t h, int64_t w, int frames,
                  cudaStream_t st) {
   if (h <= 0 || w <= 0 || frames <= 0) return SPX_OK;
-  dim3 grid((unsigned)ceil_div(w, WTW), (unsigned)ceil_div(h, WTH), (unsigned)frames);
-  k_weak2<<<grid, dim3(WTW, WTH), 0, st>>>(src, dst, h, w);
+  if (h * w >= (int64_t)1 << 31 || frames > 65535) {
+    set_error("weak: frame too large for the fused kernel");
+    return SPX_ERR_VALUE;
+  }
+  dim3 grid((unsigned)ceil_div(w, WT2W), (unsigned)ceil_div(h, WT2H), (unsigned)frames);
+  k_weak2<<<grid, 256, 0, st>>>(src, dst, (int)h, (int)w);
   SPX_LAUNCH_CHECK("k_weak2");
   return SPX_OK;
 }
