@@ -43,25 +43,23 @@ __device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigne
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b,
                                                    unsigned long long c) {
   unsigned long long r;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
-__device__ __forceinline__ float rsq(float x) {
+__device__ __forceinline__ float sqa(float x) {
   float r;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 __device__ __forceinline__ bool fin_small(double v) { return fabs(v) < 1e15; }
-
-// Out-of-range flag for the certified sums: nonzero |v| < tau or |v| >= 128
-// (NaN/inf included).
-__device__ __forceinline__ unsigned sum_flag(float v, float tau) {
-  float a = fabsf(v);
-  return (a != 0.f && a < tau) || !(a < 128.f) ? 1u : 0u;
-}
 
 }  // namespace
 
@@ -80,7 +78,6 @@ struct CellParams {
   unsigned row_magic;      // ceil(2^16 / runs_per_row)
   double xy_weight;
   float w32, k_mp, k_mc, k_xy, k_const, k_rel;
-  float tau;               // certified-sum lower magnitude
 };
 
 // Exact binary64 argmin over the candidates in reference order (_core.pyx:181-197).
@@ -202,7 +199,6 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   // Cell constant of 2A: k_mc*Mc + k_xy*(3*Mxy + 2S) + k_const
   float two_a_cell = __fmaf_rn(mc, p.k_mc, __fmaf_rn(__fmaf_rn(3.f, mxy, 2.f * S), p.k_xy, p.k_const));
   if (okf == 0.f) two_a_cell = INFINITY;
-  const unsigned long long TINY2 = f2_pack(1e-30f, 1e-30f);
   const int x_cell = cc * S, y_cell = cr * S;
   const long long img_base = (long long)f * p.h * p.w;
 
@@ -240,10 +236,14 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
       if (!ok) continue;
       const int y = y_cell + row, x = x_cell + c4;
       const long long pix = img_base + (long long)y * p.w + x;   // label index
-      const float L[4] = {Lv.x, Lv.y, Lv.z, Lv.w};
+      // Channel 0 carries the certified-sum flag in its sign bit (set by the
+      // engine's planar convert; channel 0 is never negative): strip it.
+      const unsigned fl4 = (__float_as_uint(Lv.x) >> 31) | ((__float_as_uint(Lv.y) >> 31) << 1) |
+                           ((__float_as_uint(Lv.z) >> 31) << 2) | ((__float_as_uint(Lv.w) >> 31) << 3);
+      const float L[4] = {fabsf(Lv.x), fabsf(Lv.y), fabsf(Lv.z), fabsf(Lv.w)};
       const float A[4] = {Av.x, Av.y, Av.z, Av.w};
       const float B[4] = {Bv.x, Bv.y, Bv.z, Bv.w};
-      const unsigned long long L01 = f2_pack(Lv.x, Lv.y), L23 = f2_pack(Lv.z, Lv.w);
+      const unsigned long long L01 = f2_pack(L[0], L[1]), L23 = f2_pack(L[2], L[3]);
       const unsigned long long A01 = f2_pack(Av.x, Av.y), A23 = f2_pack(Av.z, Av.w);
       const unsigned long long B01 = f2_pack(Bv.x, Bv.y), B23 = f2_pack(Bv.z, Bv.w);
       const float xr0 = (float)c4;
@@ -258,11 +258,11 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
       for (int t = 0; t < 9; ++t) {
         const CandPairs c = cand[t];
         const unsigned long long dy = sub2(c.y, Y2);
-        const unsigned long long dyy = fma2(dy, dy, TINY2);
+        const unsigned long long dyy = mul2(dy, dy);
         float Q[4], R[4];
         {
           unsigned long long dl = sub2(c.l, L01), da = sub2(c.a, A01), db = sub2(c.b, B01);
-          unsigned long long q = fma2(db, db, fma2(da, da, fma2(dl, dl, TINY2)));
+          unsigned long long q = fma2(db, db, fma2(da, da, mul2(dl, dl)));
           unsigned long long dx = sub2(c.x, X01);
           unsigned long long r = fma2(dx, dx, dyy);
           f2_unpack(q, Q[0], Q[1]);
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
         }
         {
           unsigned long long dl = sub2(c.l, L23), da = sub2(c.a, A23), db = sub2(c.b, B23);
-          unsigned long long q = fma2(db, db, fma2(da, da, fma2(dl, dl, TINY2)));
+          unsigned long long q = fma2(db, db, fma2(da, da, mul2(dl, dl)));
           unsigned long long dx = sub2(c.x, X23);
           unsigned long long r = fma2(dx, dx, dyy);
           f2_unpack(q, Q[2], Q[3]);
@@ -278,9 +278,8 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          // D = sqrt(q) + w * sqrt(r), both square roots as v * rsqrt(v)
-          const float s1 = __fmul_rn(Q[i], rsq(Q[i]));
-          const float d = __fmaf_rn(w32, __fmul_rn(R[i], rsq(R[i])), s1);
+          // D = sqrt(q) + w * sqrt(r) (MUFU.SQRT; error bound in DESIGN.md)
+          const float d = __fmaf_rn(w32, sqa(R[i]), sqa(Q[i]));
           const unsigned key = (__float_as_uint(d) & ~15u) | (unsigned)t;
           k2[i] = min(k2[i], max(k1[i], key));
           k1[i] = min(k1[i], key);
@@ -303,7 +302,7 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
         }
         lab4[i] = k;
         if (ACC) {
-          const unsigned fl = sum_flag(L[i], p.tau) | sum_flag(A[i], p.tau) | sum_flag(B[i], p.tau);
+          const unsigned fl = (fl4 >> i) & 1u;
           double* d = accd + t * 96 + lane;
           d[0] = dadd(d[0], (double)L[i]);
           d[32] = dadd(d[32], (double)A[i]);
@@ -508,17 +507,30 @@ __global__ void __launch_bounds__(128) k_exact_clusters(ReduceParams p) {
     for (int yc = ya; yc < ry1; yc += rows_per_chunk) {
       const int rows = min(rows_per_chunk, ry1 - yc);
       const int npx = rows * ww;
-      for (int base = 0; base < npx; base += 32) {
-        const int idx = base + lane;
-        bool m = false;
-        if (idx < npx) {
-          const int y = yc + idx / ww, x = wx0 + idx % ww;
-          const long long q = (long long)y * p.w + x;
-          m = __ldg(lb + q) == fk;
-          if (m) vals[warp][idx] = make_float4(__ldg(im + q), __ldg(im + hw + q), __ldg(im + 2 * hw + q), 0.f);
+      // 8 independent label loads per lane in flight, then the value loads
+      for (int base = 0; base < npx; base += 32 * 8) {
+        int32_t labv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = base + 32 * u + lane;
+          labv[u] = -1;
+          if (idx < npx) {
+            const int y = yc + idx / ww, x = wx0 + idx % ww;
+            labv[u] = __ldg(lb + (long long)y * p.w + x);
+          }
         }
-        const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
-        if (lane == 0) masks[warp][base >> 5] = bm;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = base + 32 * u + lane;
+          const bool m = labv[u] == fk;
+          if (m) {
+            const int y = yc + idx / ww, x = wx0 + idx % ww;
+            const long long q = (long long)y * p.w + x;
+            vals[warp][idx] = make_float4(fabsf(__ldg(im + q)), __ldg(im + hw + q), __ldg(im + 2 * hw + q), 0.f);
+          }
+          const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
+          if (lane == 0 && base + 32 * u < npx) masks[warp][(base >> 5) + u] = bm;
+        }
       }
       __syncwarp();
       if (lane == 0) {
@@ -618,10 +630,6 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.lanes_per_cell = 16;  // two cells per warp; 9 staging lanes per cell
   p.xy_weight = xy_weight;
   assoc_bound_coefficients(xy_weight, p.w32, p.k_mp, p.k_mc, p.k_xy, p.k_const, p.k_rel);
-  // tau = 2^k with 9 S^2 <= 2^(23 + k)  (certified sums, see header)
-  int kexp = -23;
-  while ((double)std::ldexp(1.0, 23 + kexp) < 9.0 * (double)(s * s)) ++kexp;
-  p.tau = (float)std::ldexp(1.0, kexp);
   const int cpw = 32 / p.lanes_per_cell;
   const long long warps = ceil_div(ns_r * ns_c, cpw);
   const dim3 blocks((unsigned)ceil_div(warps, kWarps), (unsigned)frames);

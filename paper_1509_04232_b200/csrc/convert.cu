@@ -129,10 +129,21 @@ __device__ __forceinline__ void convert_px(const double* lut, uint32_t R, uint32
 // a batch is one range).  `vec` requires rgb 4-byte and out 16-byte aligned.
 // PLANAR: out is [frames][3][hw] (the engine's internal layout) instead of
 // HWC; requires hw % 4 == 0 so a 4-pixel group never straddles frames.
+// Certified-sum flag of one output pixel (cell.cu): some channel is nonzero
+// with |v| < tau, or |v| >= 128 / non-finite.
+__device__ __forceinline__ bool sum_flag(float v, float tau) {
+  const float a = fabsf(v);
+  return (a != 0.f && a < tau) || !(a < 128.f);
+}
+__device__ __forceinline__ float with_flag(float o0, float o1, float o2, float tau) {
+  const bool f = sum_flag(o0, tau) || sum_flag(o1, tau) || sum_flag(o2, tau);
+  return f ? __uint_as_float(__float_as_uint(o0) | 0x80000000u) : o0;
+}
+
 template <int SPACE, bool PLANAR>
 __global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb,
                                                  float* __restrict__ out, int64_t p0,
-                                                 int64_t p1, int vec, int64_t hw) {
+                                                 int64_t p1, int vec, int64_t hw, float tau) {
   __shared__ double lut[256];
   if (SPACE != 0) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = g_lut[i];
@@ -160,7 +171,9 @@ __global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb
       if (PLANAR) {
         const int64_t f = q / hw, r = q - f * hw;
         float* base = out + f * 3 * hw + r;
-        *reinterpret_cast<float4*>(base) = make_float4(o[0], o[3], o[6], o[9]);
+        *reinterpret_cast<float4*>(base) =
+            make_float4(with_flag(o[0], o[1], o[2], tau), with_flag(o[3], o[4], o[5], tau),
+                        with_flag(o[6], o[7], o[8], tau), with_flag(o[9], o[10], o[11], tau));
         *reinterpret_cast<float4*>(base + hw) = make_float4(o[1], o[4], o[7], o[10]);
         *reinterpret_cast<float4*>(base + 2 * hw) = make_float4(o[2], o[5], o[8], o[11]);
       } else {
@@ -176,7 +189,7 @@ __global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb
         convert_px<SPACE>(lut, rgb[p * 3], rgb[p * 3 + 1], rgb[p * 3 + 2], o0, o1, o2);
         if (PLANAR) {
           const int64_t f = p / hw, r = p - f * hw;
-          out[f * 3 * hw + r] = o0;
+          out[f * 3 * hw + r] = with_flag(o0, o1, o2, tau);
           out[f * 3 * hw + hw + r] = o1;
           out[f * 3 * hw + 2 * hw + r] = o2;
         } else {
@@ -189,8 +202,11 @@ __global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb
   }
 }
 
+// planar_hw > 0: the engine's planar layout with the certified-sum flag of
+// grid interval `s` in channel 0's sign bit.
 int launch_convert(const uint8_t* rgb, float* out, int64_t p0, int64_t p1, int space,
-                   cudaStream_t st, int64_t planar_hw) {
+                   cudaStream_t st, int64_t planar_hw, int64_t s) {
+  const float tau = planar_hw > 0 ? certified_tau(s) : 0.f;
   if (p1 <= p0) return SPX_OK;
   int rc = upload_tables();
   if (rc) return rc;
@@ -206,8 +222,9 @@ int launch_convert(const uint8_t* rgb, float* out, int64_t p0, int64_t p1, int s
   if (blocks > cap) blocks = cap;
 #define SPX_CONVERT(SP)                                                                  \
   (planar ? k_convert<SP, true><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec,  \
-                                                                  planar_hw)              \
-          : k_convert<SP, false><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec, 1))
+                                                                  planar_hw, tau)         \
+          : k_convert<SP, false><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec, 1, \
+                                                                   0.f))
   switch (space) {
     case 0: SPX_CONVERT(0); break;
     case 1: SPX_CONVERT(1); break;
@@ -229,5 +246,5 @@ extern "C" int32_t spx_convert_band(const uint8_t* rgb, float* out, int64_t h, i
                    (long long)y0, (long long)y1, (long long)h);
     return SPX_ERR_DIMENSION;
   }
-  return spx::launch_convert(rgb, out, y0 * w, y1 * w, space, spx::as_stream(stream), 0);
+  return spx::launch_convert(rgb, out, y0 * w, y1 * w, space, spx::as_stream(stream), 0, 1);
 }
