@@ -152,8 +152,11 @@ SPX_API int32_t spx_engine_segment(spx_engine *eng, const uint8_t *rgb_dev, int6
                            int32_t *labels_dev, double *cxy_dev, double *clab_dev,
                            int64_t *counts_dev, int32_t *passes_dev, void *stream);
 
-/* Same with HOST buffers: H2D copy of rgb, pipeline, D2H copy of results,
- * through the engine's pinned staging.  Synchronous. */
+/* Same with HOST buffers (any batch size): frames are processed in chunks of
+ * up to 32 through double-buffered device staging on three streams, so the
+ * H2D copy of the next chunk and the D2H copy of the previous one overlap the
+ * compute of the current one.  Pinned host buffers make the copies
+ * asynchronous (pageable ones are correct but serialised).  Synchronous. */
 SPX_API int32_t spx_engine_segment_host(spx_engine *eng, const uint8_t *rgb_host, int64_t batch,
                                 int32_t *labels_host, double *cxy_host, double *clab_host,
                                 int64_t *counts_host, int32_t *passes_host);

@@ -479,7 +479,7 @@ constexpr int kExactChunk = 512;
 
 __global__ void __launch_bounds__(128) k_exact_clusters(ReduceParams p) {
   __shared__ double strips[4][32][6];
-  __shared__ float4 vals[4][kExactChunk];
+  __shared__ float4 vals[4][kExactChunk];     // (l, a, b, meta) of matched pixels
   __shared__ unsigned masks[4][kExactChunk / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.ns_r * p.ns_c;
@@ -500,14 +500,14 @@ __global__ void __launch_bounds__(128) k_exact_clusters(ReduceParams p) {
     const int rows_per_chunk = max(1, kExactChunk / ww);
     if (lane < p.n_bl)
       for (int comp = 0; comp < 6; ++comp) sk[lane][comp] = 0.0;
-    // running strip state lives in lane 0's registers
+    // Lanes 0..2 each fold one colour channel in the reference order; lane 0
+    // also carries x / y / count.  The strip of every pixel is precomputed.
     int cur_j = -1;
-    double sl = 0.0, sa = 0.0, sb = 0.0;
+    double acc = 0.0;
     long long sx = 0, sy = 0, cnt = 0;
     for (int yc = ya; yc < ry1; yc += rows_per_chunk) {
       const int rows = min(rows_per_chunk, ry1 - yc);
       const int npx = rows * ww;
-      // 8 independent label loads per lane in flight, then the value loads
       for (int base = 0; base < npx; base += 32 * 8) {
         int32_t labv[8];
 #pragma unroll
@@ -524,52 +524,62 @@ __global__ void __launch_bounds__(128) k_exact_clusters(ReduceParams p) {
           const int idx = base + 32 * u + lane;
           const bool m = labv[u] == fk;
           if (m) {
-            const int y = yc + idx / ww, x = wx0 + idx % ww;
+            const int dy = idx / ww, dx = idx % ww;
+            const int y = yc + dy, x = wx0 + dx;
             const long long q = (long long)y * p.w + x;
-            vals[warp][idx] = make_float4(fabsf(__ldg(im + q)), __ldg(im + hw + q), __ldg(im + 2 * hw + q), 0.f);
+            const unsigned strip = (unsigned)((y - ry0) / p.tile_len);
+            const unsigned meta = (strip << 24) | ((unsigned)(y - ya) << 12) | (unsigned)(x - wx0);
+            vals[warp][idx] = make_float4(fabsf(__ldg(im + q)), __ldg(im + hw + q),
+                                          __ldg(im + 2 * hw + q), __uint_as_float(meta));
           }
           const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
           if (lane == 0 && base + 32 * u < npx) masks[warp][(base >> 5) + u] = bm;
         }
       }
       __syncwarp();
-      if (lane == 0) {
+      if (lane < 3) {
         for (int wv = 0; wv * 32 < npx; ++wv) {
           unsigned bm = masks[warp][wv];
           while (bm) {
             const int b = __ffs(bm) - 1;
             bm &= bm - 1;
-            const int idx = wv * 32 + b;
-            const int y = yc + idx / ww, x = wx0 + idx % ww;
-            const int j = (y - ry0) / p.tile_len;
+            const float4 v = vals[warp][wv * 32 + b];
+            const unsigned meta = __float_as_uint(v.w);
+            const int j = (int)(meta >> 24);
             if (j != cur_j) {
               if (cur_j >= 0) {
-                sk[cur_j][0] = sl; sk[cur_j][1] = sa; sk[cur_j][2] = sb;
-                sk[cur_j][3] = (double)sx; sk[cur_j][4] = (double)sy; sk[cur_j][5] = (double)cnt;
+                sk[cur_j][lane] = acc;
+                if (lane == 0) {
+                  sk[cur_j][3] = (double)sx;
+                  sk[cur_j][4] = (double)sy;
+                  sk[cur_j][5] = (double)cnt;
+                }
               }
               cur_j = j;
-              sl = sa = sb = 0.0;
+              acc = 0.0;
               sx = sy = cnt = 0;
             }
-            const float4 v = vals[warp][idx];
-            sl = dadd(sl, (double)v.x);
-            sa = dadd(sa, (double)v.y);
-            sb = dadd(sb, (double)v.z);
-            sx += x;
-            sy += y;
+            acc = dadd(acc, (double)(lane == 0 ? v.x : (lane == 1 ? v.y : v.z)));
+            sx += wx0 + (int)(meta & 0xFFFu);
+            sy += ya + (int)((meta >> 12) & 0xFFFu);
             cnt += 1;
           }
         }
       }
       __syncwarp();
     }
-    if (lane == 0) {
-      if (cur_j >= 0) {
-        sk[cur_j][0] = sl; sk[cur_j][1] = sa; sk[cur_j][2] = sb;
-        sk[cur_j][3] = (double)sx; sk[cur_j][4] = (double)sy; sk[cur_j][5] = (double)cnt;
+    if (lane < 3 && cur_j >= 0) {
+      sk[cur_j][lane] = acc;
+      if (lane == 0) {
+        sk[cur_j][3] = (double)sx;
+        sk[cur_j][4] = (double)sy;
+        sk[cur_j][5] = (double)cnt;
       }
+    }
+    __syncwarp();
+    if (lane == 0) {
       int m = p.n_bl;
-      while (m > 1) {
+      while (m > 1) {  // pairwise strip tree, _core.pyx:300-311
         int half = m >> 1;
         for (int i = 0; i < half; ++i)
           for (int comp = 0; comp < 6; ++comp) sk[i][comp] = dadd(sk[2 * i][comp], sk[2 * i + 1][comp]);

@@ -80,12 +80,6 @@ struct Engine {
   Part* part = nullptr;  // per (cell, slot) partial sums (cell path)
   int32_t* worklist = nullptr;  // flagged clusters for the exact fallback (cell path)
   bool use_cell = false;
-  uint8_t* d_rgb = nullptr;  // staging for the host-buffer entry point
-  int32_t* d_labels = nullptr;
-  double *d_cxy = nullptr, *d_clab = nullptr;
-  int64_t* d_counts = nullptr;
-  int32_t* d_passes = nullptr;
-  cudaStream_t own_stream = nullptr;
   cudaEvent_t ev[EV_FIXED] = {};
   std::vector<cudaEvent_t> ev_assoc, ev_update;  // start/end pairs
   int n_assoc = 0, n_update = 0;
@@ -96,14 +90,13 @@ struct Engine {
     for (void* p : {(void*)lab, (void*)labels, (void*)scratch, (void*)cxy[0], (void*)cxy[1],
                     (void*)clab[0], (void*)clab[1], (void*)slab, (void*)done, (void*)passes,
                     (void*)cc_parent, (void*)cc_size, (void*)cc_nxt, (void*)cc_first,
-                    (void*)rec, (void*)part, (void*)worklist, (void*)d_rgb, (void*)d_labels, (void*)d_cxy, (void*)d_clab, (void*)d_counts,
-                    (void*)d_passes})
+                    (void*)rec, (void*)part, (void*)worklist})
       if (p) cudaFree(p);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto e : ev_assoc) cudaEventDestroy(e);
     for (auto e : ev_update) cudaEventDestroy(e);
-    if (own_stream) cudaStreamDestroy(own_stream);
+    free_staging();
   }
 
   int init(const spx_settings& s, int64_t mb, int dev) {
@@ -296,17 +289,51 @@ struct Engine {
     return SPX_OK;
   }
 
+  // ---- host-buffer entry point: chunked, double-buffered, three streams -------
+  // H2D of chunk c+1 and D2H of chunk c-1 overlap the compute of chunk c
+  // (copy engines run both directions concurrently with the SMs).  Host
+  // buffers must be pinned for the copies to be asynchronous; pageable
+  // buffers still give correct results, serialised.
+  int64_t chunk = 0;
+  uint8_t* h_rgb[2] = {nullptr, nullptr};
+  int32_t* h_lab[2] = {nullptr, nullptr};
+  double* h_xy[2] = {nullptr, nullptr};
+  double* h_cl[2] = {nullptr, nullptr};
+  int64_t* h_cnt[2] = {nullptr, nullptr};
+  int32_t* h_pass[2] = {nullptr, nullptr};
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+
   int ensure_staging() {
-    if (d_rgb) return SPX_OK;
-    size_t B = (size_t)max_batch;
-    SPX_CUDA(cudaMalloc(&d_rgb, B * hw * 3));
-    SPX_CUDA(cudaMalloc(&d_labels, B * hw * sizeof(int32_t)));
-    SPX_CUDA(cudaMalloc(&d_cxy, B * K * 2 * sizeof(double)));
-    SPX_CUDA(cudaMalloc(&d_clab, B * K * 3 * sizeof(double)));
-    SPX_CUDA(cudaMalloc(&d_counts, B * K * sizeof(int64_t)));
-    SPX_CUDA(cudaMalloc(&d_passes, B * sizeof(int32_t)));
-    SPX_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+    if (s_comp) return SPX_OK;
+    chunk = std::max<int64_t>(1, std::min<int64_t>(max_batch, 32));
+    for (int i = 0; i < 2; ++i) {
+      SPX_CUDA(cudaMalloc(&h_rgb[i], chunk * hw * 3));
+      SPX_CUDA(cudaMalloc(&h_lab[i], chunk * hw * sizeof(int32_t)));
+      SPX_CUDA(cudaMalloc(&h_xy[i], chunk * K * 2 * sizeof(double)));
+      SPX_CUDA(cudaMalloc(&h_cl[i], chunk * K * 3 * sizeof(double)));
+      SPX_CUDA(cudaMalloc(&h_cnt[i], chunk * K * sizeof(int64_t)));
+      SPX_CUDA(cudaMalloc(&h_pass[i], chunk * sizeof(int32_t)));
+      SPX_CUDA(cudaEventCreateWithFlags(&ev_h2d[i], cudaEventDisableTiming));
+      SPX_CUDA(cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming));
+      SPX_CUDA(cudaEventCreateWithFlags(&ev_d2h[i], cudaEventDisableTiming));
+    }
+    SPX_CUDA(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
+    SPX_CUDA(cudaStreamCreateWithFlags(&s_comp, cudaStreamNonBlocking));
+    SPX_CUDA(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
     return SPX_OK;
+  }
+
+  void free_staging() {
+    for (int i = 0; i < 2; ++i) {
+      for (void* q : {(void*)h_rgb[i], (void*)h_lab[i], (void*)h_xy[i], (void*)h_cl[i],
+                      (void*)h_cnt[i], (void*)h_pass[i]})
+        if (q) cudaFree(q);
+      for (cudaEvent_t e : {ev_h2d[i], ev_comp[i], ev_d2h[i]})
+        if (e) cudaEventDestroy(e);
+    }
+    for (cudaStream_t q : {s_h2d, s_comp, s_d2h})
+      if (q) cudaStreamDestroy(q);
   }
 
   int segment_host(const uint8_t* rgb, int64_t batch, int32_t* out_labels, double* out_xy,
@@ -314,23 +341,43 @@ struct Engine {
     SPX_CUDA(cudaSetDevice(device));
     int rc = ensure_staging();
     if (rc) return rc;
-    if (batch < 1 || batch > max_batch) {
-      set_error("batch %lld outside [1, %lld]", (long long)batch, (long long)max_batch);
+    if (batch < 1) {
+      set_error("batch must be >= 1");
       return SPX_ERR_VALUE;
     }
-    cudaStream_t s = own_stream;
-    size_t B = (size_t)batch;
-    SPX_CUDA(cudaMemcpyAsync(d_rgb, rgb, B * hw * 3, cudaMemcpyHostToDevice, s));
-    if ((rc = segment(d_rgb, batch, d_labels, d_cxy, d_clab, d_counts, d_passes, s))) return rc;
-    if (out_labels)
-      SPX_CUDA(cudaMemcpyAsync(out_labels, d_labels, B * hw * 4, cudaMemcpyDeviceToHost, s));
-    if (out_xy) SPX_CUDA(cudaMemcpyAsync(out_xy, d_cxy, B * K * 16, cudaMemcpyDeviceToHost, s));
-    if (out_lab) SPX_CUDA(cudaMemcpyAsync(out_lab, d_clab, B * K * 24, cudaMemcpyDeviceToHost, s));
-    if (out_counts)
-      SPX_CUDA(cudaMemcpyAsync(out_counts, d_counts, B * K * 8, cudaMemcpyDeviceToHost, s));
-    if (out_passes)
-      SPX_CUDA(cudaMemcpyAsync(out_passes, d_passes, B * 4, cudaMemcpyDeviceToHost, s));
-    SPX_CUDA(cudaStreamSynchronize(s));
+    const int64_t nchunks = ceil_div(batch, chunk);
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int sl = (int)(c & 1);
+      const int64_t f0 = c * chunk, nb = std::min(chunk, batch - f0);
+      if (c >= 2) SPX_CUDA(cudaStreamWaitEvent(s_h2d, ev_comp[sl], 0));
+      SPX_CUDA(cudaMemcpyAsync(h_rgb[sl], rgb + f0 * hw * 3, nb * hw * 3, cudaMemcpyHostToDevice,
+                               s_h2d));
+      SPX_CUDA(cudaEventRecord(ev_h2d[sl], s_h2d));
+      SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_h2d[sl], 0));
+      if (c >= 2) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
+      if ((rc = segment(h_rgb[sl], nb, h_lab[sl], h_xy[sl], h_cl[sl], h_cnt[sl], h_pass[sl],
+                        s_comp)))
+        return rc;
+      SPX_CUDA(cudaEventRecord(ev_comp[sl], s_comp));
+      SPX_CUDA(cudaStreamWaitEvent(s_d2h, ev_comp[sl], 0));
+      if (out_labels)
+        SPX_CUDA(cudaMemcpyAsync(out_labels + f0 * hw, h_lab[sl], nb * hw * 4,
+                                 cudaMemcpyDeviceToHost, s_d2h));
+      if (out_xy)
+        SPX_CUDA(cudaMemcpyAsync(out_xy + f0 * K * 2, h_xy[sl], nb * K * 16, cudaMemcpyDeviceToHost,
+                                 s_d2h));
+      if (out_lab)
+        SPX_CUDA(cudaMemcpyAsync(out_lab + f0 * K * 3, h_cl[sl], nb * K * 24,
+                                 cudaMemcpyDeviceToHost, s_d2h));
+      if (out_counts)
+        SPX_CUDA(cudaMemcpyAsync(out_counts + f0 * K, h_cnt[sl], nb * K * 8,
+                                 cudaMemcpyDeviceToHost, s_d2h));
+      if (out_passes)
+        SPX_CUDA(cudaMemcpyAsync(out_passes + f0, h_pass[sl], nb * 4, cudaMemcpyDeviceToHost,
+                                 s_d2h));
+      SPX_CUDA(cudaEventRecord(ev_d2h[sl], s_d2h));
+    }
+    SPX_CUDA(cudaStreamSynchronize(s_d2h));
     return SPX_OK;
   }
 };
