@@ -468,103 +468,102 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
 }
 
 // Exact recomputation of flagged clusters (certificate failed): one warp per
-// cluster.  The cluster's 3Sx3S window is processed in chunks of up to
-// kExactChunk pixels: all lanes load labels and, for matches, the Lab values
-// into shared memory in parallel (one memory round trip per chunk); then
-// lane 0 folds the matches in the reference's row-major order into the
-// strip sums (_core.pyx:221-255) and finally applies the pairwise strip tree
-// (_core.pyx:300-311).  Labels come from the same association pass, so the
-// window contains every member (no spill on pipeline labels).
-constexpr int kExactChunk = 512;
+// cluster.  The 3Sx3S window is walked in blocks of kRows rows: lanes own
+// columns (lane, lane+32, lane+64), so all label loads of a block are in
+// flight together and no index division is needed; matches stage their Lab
+// values and strip metadata in shared memory.  Lanes 0..2 then fold the three
+// colour channels in the reference's row-major order (_core.pyx:233-243),
+// lane 0 also x / y / count, and lane 0 finally applies the pairwise strip
+// tree (_core.pyx:300-311).  Labels come from the same association pass, so
+// the window contains every member (no spill on pipeline labels).
+constexpr int kRows = 6;
+constexpr int kCols = 96;  // window width 3S <= 96 (S <= 32)
 
 __global__ void __launch_bounds__(128) k_exact_clusters(ReduceParams p) {
   __shared__ double strips[4][32][6];
-  __shared__ float4 vals[4][kExactChunk];     // (l, a, b, meta) of matched pixels
-  __shared__ unsigned masks[4][kExactChunk / 32];
+  __shared__ float4 vals[4][kRows * kCols];        // (l, a, b, meta)
+  __shared__ unsigned masks[4][kRows][kCols / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.ns_r * p.ns_c;
   const int n = *p.worklist_n;
   const int nwarps = gridDim.x * 4;
   double (*sk)[6] = strips[warp];
+  const long long hw = (long long)p.h * p.w;
   for (int item = blockIdx.x * 4 + warp; item < n; item += nwarps) {
     const int gk = p.worklist[item];
     const int ff = gk / K, fk = gk - ff * K;
-    const float* im = p.img + (long long)ff * p.h * p.w * 3;  // planar [3][H][W]
-    const long long hw = (long long)p.h * p.w;
+    const float* im = p.img + (long long)ff * 3 * hw;  // planar [3][H][W]
     const int32_t* lb = p.labels + (long long)ff * hw;
-    const int r = fk / p.ns_c, c = fk % p.ns_c;
+    const int r = fk / p.ns_c, c = fk - (fk / p.ns_c) * p.ns_c;
     const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
     const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
     const int ya = max(ry0, 0);
     const int ww = wx1 - wx0;
-    const int rows_per_chunk = max(1, kExactChunk / ww);
+    const int ncb = (ww + 31) >> 5;  // column blocks of 32
     if (lane < p.n_bl)
       for (int comp = 0; comp < 6; ++comp) sk[lane][comp] = 0.0;
-    // Lanes 0..2 each fold one colour channel in the reference order; lane 0
-    // also carries x / y / count.  The strip of every pixel is precomputed.
     int cur_j = -1;
     double acc = 0.0;
     long long sx = 0, sy = 0, cnt = 0;
-    for (int yc = ya; yc < ry1; yc += rows_per_chunk) {
-      const int rows = min(rows_per_chunk, ry1 - yc);
-      const int npx = rows * ww;
-      for (int base = 0; base < npx; base += 32 * 8) {
-        int32_t labv[8];
+    for (int yb = ya; yb < ry1; yb += kRows) {
+      const int rows = min(kRows, ry1 - yb);
+      int32_t lv[kRows][3];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int idx = base + 32 * u + lane;
-          labv[u] = -1;
-          if (idx < npx) {
-            const int y = yc + idx / ww, x = wx0 + idx % ww;
-            labv[u] = __ldg(lb + (long long)y * p.w + x);
-          }
+      for (int rr = 0; rr < kRows; ++rr)
+#pragma unroll
+        for (int cb = 0; cb < 3; ++cb) {
+          const int col = cb * 32 + lane;
+          lv[rr][cb] = (rr < rows && col < ww) ? __ldg(lb + (long long)(yb + rr) * p.w + wx0 + col)
+                                               : -1;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int idx = base + 32 * u + lane;
-          const bool m = labv[u] == fk;
+      for (int rr = 0; rr < kRows; ++rr) {
+        const int y = yb + rr;
+        const unsigned strip = rr < rows ? (unsigned)((y - ry0) / p.tile_len) : 0u;
+#pragma unroll
+        for (int cb = 0; cb < 3; ++cb) {
+          const int col = cb * 32 + lane;
+          const bool m = lv[rr][cb] == fk;
           if (m) {
-            const int dy = idx / ww, dx = idx % ww;
-            const int y = yc + dy, x = wx0 + dx;
-            const long long q = (long long)y * p.w + x;
-            const unsigned strip = (unsigned)((y - ry0) / p.tile_len);
-            const unsigned meta = (strip << 24) | ((unsigned)(y - ya) << 12) | (unsigned)(x - wx0);
-            vals[warp][idx] = make_float4(fabsf(__ldg(im + q)), __ldg(im + hw + q),
-                                          __ldg(im + 2 * hw + q), __uint_as_float(meta));
+            const long long q = (long long)y * p.w + wx0 + col;
+            const unsigned meta = (strip << 24) | ((unsigned)(y - ya) << 12) | (unsigned)col;
+            vals[warp][rr * kCols + col] = make_float4(fabsf(__ldg(im + q)), __ldg(im + hw + q),
+                                                       __ldg(im + 2 * hw + q), __uint_as_float(meta));
           }
           const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
-          if (lane == 0 && base + 32 * u < npx) masks[warp][(base >> 5) + u] = bm;
+          if (lane == 0 && cb < ncb) masks[warp][rr][cb] = bm;
         }
       }
       __syncwarp();
       if (lane < 3) {
-        for (int wv = 0; wv * 32 < npx; ++wv) {
-          unsigned bm = masks[warp][wv];
-          while (bm) {
-            const int b = __ffs(bm) - 1;
-            bm &= bm - 1;
-            const float4 v = vals[warp][wv * 32 + b];
-            const unsigned meta = __float_as_uint(v.w);
-            const int j = (int)(meta >> 24);
-            if (j != cur_j) {
-              if (cur_j >= 0) {
-                sk[cur_j][lane] = acc;
-                if (lane == 0) {
-                  sk[cur_j][3] = (double)sx;
-                  sk[cur_j][4] = (double)sy;
-                  sk[cur_j][5] = (double)cnt;
+        for (int rr = 0; rr < rows; ++rr)
+          for (int cb = 0; cb < ncb; ++cb) {
+            unsigned bm = masks[warp][rr][cb];
+            while (bm) {
+              const int b = __ffs(bm) - 1;
+              bm &= bm - 1;
+              const float4 v = vals[warp][rr * kCols + cb * 32 + b];
+              const unsigned meta = __float_as_uint(v.w);
+              const int j = (int)(meta >> 24);
+              if (j != cur_j) {
+                if (cur_j >= 0) {
+                  sk[cur_j][lane] = acc;
+                  if (lane == 0) {
+                    sk[cur_j][3] = (double)sx;
+                    sk[cur_j][4] = (double)sy;
+                    sk[cur_j][5] = (double)cnt;
+                  }
                 }
+                cur_j = j;
+                acc = 0.0;
+                sx = sy = cnt = 0;
               }
-              cur_j = j;
-              acc = 0.0;
-              sx = sy = cnt = 0;
+              acc = dadd(acc, (double)(lane == 0 ? v.x : (lane == 1 ? v.y : v.z)));
+              sx += wx0 + (int)(meta & 0xFFFu);
+              sy += ya + (int)((meta >> 12) & 0xFFFu);
+              cnt += 1;
             }
-            acc = dadd(acc, (double)(lane == 0 ? v.x : (lane == 1 ? v.y : v.z)));
-            sx += wx0 + (int)(meta & 0xFFFu);
-            sy += ya + (int)((meta >> 12) & 0xFFFu);
-            cnt += 1;
           }
-        }
       }
       __syncwarp();
     }

@@ -5,6 +5,7 @@
 // are allocated once per engine (engine.py:110-119) and stay resident in HBM,
 // and stage boundaries are CUDA events instead of perf_counter calls.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -346,20 +347,35 @@ struct Engine {
       return SPX_ERR_VALUE;
     }
     const int64_t nchunks = ceil_div(batch, chunk);
+    // optional per-chunk timeline (diagnostics): SPX_DEBUG_TIMELINE=1
+    static const bool dbg = getenv("SPX_DEBUG_TIMELINE") != nullptr;
+    std::vector<cudaEvent_t> tl;
+    auto mark = [&](cudaStream_t q) {
+      if (!dbg) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, q);
+      tl.push_back(e);
+    };
     for (int64_t c = 0; c < nchunks; ++c) {
       const int sl = (int)(c & 1);
       const int64_t f0 = c * chunk, nb = std::min(chunk, batch - f0);
       if (c >= 2) SPX_CUDA(cudaStreamWaitEvent(s_h2d, ev_comp[sl], 0));
+      mark(s_h2d);
       SPX_CUDA(cudaMemcpyAsync(h_rgb[sl], rgb + f0 * hw * 3, nb * hw * 3, cudaMemcpyHostToDevice,
                                s_h2d));
+      mark(s_h2d);
       SPX_CUDA(cudaEventRecord(ev_h2d[sl], s_h2d));
       SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_h2d[sl], 0));
       if (c >= 2) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
+      mark(s_comp);
       if ((rc = segment(h_rgb[sl], nb, h_lab[sl], h_xy[sl], h_cl[sl], h_cnt[sl], h_pass[sl],
                         s_comp)))
         return rc;
+      mark(s_comp);
       SPX_CUDA(cudaEventRecord(ev_comp[sl], s_comp));
       SPX_CUDA(cudaStreamWaitEvent(s_d2h, ev_comp[sl], 0));
+      mark(s_d2h);
       if (out_labels)
         SPX_CUDA(cudaMemcpyAsync(out_labels + f0 * hw, h_lab[sl], nb * hw * 4,
                                  cudaMemcpyDeviceToHost, s_d2h));
@@ -375,9 +391,25 @@ struct Engine {
       if (out_passes)
         SPX_CUDA(cudaMemcpyAsync(out_passes + f0, h_pass[sl], nb * 4, cudaMemcpyDeviceToHost,
                                  s_d2h));
+      mark(s_d2h);
       SPX_CUDA(cudaEventRecord(ev_d2h[sl], s_d2h));
     }
     SPX_CUDA(cudaStreamSynchronize(s_d2h));
+    if (dbg && !tl.empty()) {
+      cudaDeviceSynchronize();
+      for (size_t i = 0; i < tl.size(); i += 6) {
+        float a0, a1, b0, b1, c0, c1;
+        cudaEventElapsedTime(&a0, tl[0], tl[i]);
+        cudaEventElapsedTime(&a1, tl[0], tl[i + 1]);
+        cudaEventElapsedTime(&b0, tl[0], tl[i + 2]);
+        cudaEventElapsedTime(&b1, tl[0], tl[i + 3]);
+        cudaEventElapsedTime(&c0, tl[0], tl[i + 4]);
+        cudaEventElapsedTime(&c1, tl[0], tl[i + 5]);
+        fprintf(stderr, "chunk %zu: h2d %.2f-%.2f comp %.2f-%.2f d2h %.2f-%.2f ms\n", i / 6, a0, a1,
+                b0, b1, c0, c1);
+      }
+      for (auto e : tl) cudaEventDestroy(e);
+    }
     return SPX_OK;
   }
 };
