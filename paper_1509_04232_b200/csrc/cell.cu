@@ -468,112 +468,138 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
 }
 
 // Exact recomputation of flagged clusters (certificate failed): one warp per
-// cluster.  The 3Sx3S window is walked in blocks of kRows rows: lanes own
-// columns (lane, lane+32, lane+64), so all label loads of a block are in
-// flight together and no index division is needed; matches stage their Lab
-// values and strip metadata in shared memory.  Lanes 0..2 then fold the three
-// colour channels in the reference's row-major order (_core.pyx:233-243),
-// lane 0 also x / y / count, and lane 0 finally applies the pairwise strip
-// tree (_core.pyx:300-311).  Labels come from the same association pass, so
-// the window contains every member (no spill on pipeline labels).
-constexpr int kRows = 6;
+// cluster, latency-oriented (a handful of clusters per frame are flagged, so
+// this kernel's duration is one cluster's latency).  The 3Sx3S window is
+// walked in blocks of kRows rows with the next block's label loads in flight
+// while the current one is folded.  Per row, lanes own columns; matches are
+// compacted in row-major order into shared memory (ballot + popc), x / y /
+// count are reduced per row with REDUX.  Lanes 0..2 then fold the three
+// colour channels in exactly the reference's order (_core.pyx:233-243), each
+// strip from 0.0, and lane 0 applies the pairwise strip tree
+// (_core.pyx:300-311).  Pipeline labels never spill, so the window holds
+// every member.
+constexpr int kRows = 8;
 constexpr int kCols = 96;  // window width 3S <= 96 (S <= 32)
+constexpr int kExWarps = 2;
 
-__global__ void __launch_bounds__(128) k_exact_clusters(ReduceParams p) {
-  __shared__ double strips[4][32][6];
-  __shared__ float4 vals[4][kRows * kCols];        // (l, a, b, meta)
-  __shared__ unsigned masks[4][kRows][kCols / 32];
+__global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p) {
+  __shared__ double strips[kExWarps][32][6];
+  __shared__ float cv[kExWarps][3][kRows * kCols];  // compacted l / a / b
+  __shared__ int rstart[kExWarps][kRows + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.ns_r * p.ns_c;
   const int n = *p.worklist_n;
-  const int nwarps = gridDim.x * 4;
+  const int nwarps = gridDim.x * kExWarps;
   double (*sk)[6] = strips[warp];
   const long long hw = (long long)p.h * p.w;
-  for (int item = blockIdx.x * 4 + warp; item < n; item += nwarps) {
+  const unsigned lt = (1u << lane) - 1u;
+  for (int item = blockIdx.x * kExWarps + warp; item < n; item += nwarps) {
     const int gk = p.worklist[item];
     const int ff = gk / K, fk = gk - ff * K;
     const float* im = p.img + (long long)ff * 3 * hw;  // planar [3][H][W]
     const int32_t* lb = p.labels + (long long)ff * hw;
-    const int r = fk / p.ns_c, c = fk - (fk / p.ns_c) * p.ns_c;
+    const int r = fk / p.ns_c, c = fk - r * p.ns_c;
     const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
     const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
     const int ya = max(ry0, 0);
     const int ww = wx1 - wx0;
-    const int ncb = (ww + 31) >> 5;  // column blocks of 32
+    const int ncb = (ww + 31) >> 5;  // column blocks of 32 (<= 3)
     if (lane < p.n_bl)
       for (int comp = 0; comp < 6; ++comp) sk[lane][comp] = 0.0;
-    int cur_j = -1;
+    int cur_j = -1, fold_j = -1;
     double acc = 0.0;
-    long long sx = 0, sy = 0, cnt = 0;
-    for (int yb = ya; yb < ry1; yb += kRows) {
-      const int rows = min(kRows, ry1 - yb);
-      int32_t lv[kRows][3];
+    long long sx = 0, sy = 0, cnt = 0;  // lane 0: running strip totals
+    int32_t nxt[kRows][3];
+    auto load_block = [&](int yb, int32_t (&lv)[kRows][3]) {
 #pragma unroll
       for (int rr = 0; rr < kRows; ++rr)
 #pragma unroll
         for (int cb = 0; cb < 3; ++cb) {
           const int col = cb * 32 + lane;
-          lv[rr][cb] = (rr < rows && col < ww) ? __ldg(lb + (long long)(yb + rr) * p.w + wx0 + col)
-                                               : -1;
+          lv[rr][cb] = (yb + rr < ry1 && col < ww)
+                           ? __ldg(lb + (long long)(yb + rr) * p.w + wx0 + col)
+                           : -1;
         }
+    };
+    load_block(ya, nxt);
+    for (int yb = ya; yb < ry1; yb += kRows) {
+      int32_t lv[kRows][3];
+#pragma unroll
+      for (int rr = 0; rr < kRows; ++rr)
+#pragma unroll
+        for (int cb = 0; cb < 3; ++cb) lv[rr][cb] = nxt[rr][cb];
+      if (yb + kRows < ry1) load_block(yb + kRows, nxt);  // prefetch the next block
+      const int rows = min(kRows, ry1 - yb);
+      int base = 0;
 #pragma unroll
       for (int rr = 0; rr < kRows; ++rr) {
+        if (rr >= rows) break;
         const int y = yb + rr;
-        const unsigned strip = rr < rows ? (unsigned)((y - ry0) / p.tile_len) : 0u;
+        if (lane == 0) rstart[warp][rr] = base;
+        int rx = 0, rn = 0;
 #pragma unroll
         for (int cb = 0; cb < 3; ++cb) {
+          if (cb >= ncb) break;
           const int col = cb * 32 + lane;
           const bool m = lv[rr][cb] == fk;
-          if (m) {
-            const long long q = (long long)y * p.w + wx0 + col;
-            const unsigned meta = (strip << 24) | ((unsigned)(y - ya) << 12) | (unsigned)col;
-            vals[warp][rr * kCols + col] = make_float4(fabsf(__ldg(im + q)), __ldg(im + hw + q),
-                                                       __ldg(im + 2 * hw + q), __uint_as_float(meta));
-          }
           const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
-          if (lane == 0 && cb < ncb) masks[warp][rr][cb] = bm;
+          if (m) {
+            const int pos = base + __popc(bm & lt);
+            const long long q = (long long)y * p.w + wx0 + col;
+            cv[warp][0][pos] = fabsf(__ldg(im + q));
+            cv[warp][1][pos] = __ldg(im + hw + q);
+            cv[warp][2][pos] = __ldg(im + 2 * hw + q);
+          }
+          rx += (int)__reduce_add_sync(0xFFFFFFFFu, m ? (unsigned)(wx0 + col) : 0u);
+          rn += __popc(bm);
+          base += __popc(bm);
+        }
+        if (lane == 0 && rn) {
+          const int j = (y - ry0) / p.tile_len;
+          if (j != cur_j && cur_j >= 0) {
+            sk[cur_j][3] = (double)sx;
+            sk[cur_j][4] = (double)sy;
+            sk[cur_j][5] = (double)cnt;
+            sx = sy = cnt = 0;
+          }
+          if (j != cur_j) cur_j = j;  // lanes 1, 2 track cur_j below
+          sx += rx;
+          sy += (long long)y * rn;
+          cnt += rn;
         }
       }
+      if (lane == 0) rstart[warp][rows] = base;
       __syncwarp();
       if (lane < 3) {
-        for (int rr = 0; rr < rows; ++rr)
-          for (int cb = 0; cb < ncb; ++cb) {
-            unsigned bm = masks[warp][rr][cb];
-            while (bm) {
-              const int b = __ffs(bm) - 1;
-              bm &= bm - 1;
-              const float4 v = vals[warp][rr * kCols + cb * 32 + b];
-              const unsigned meta = __float_as_uint(v.w);
-              const int j = (int)(meta >> 24);
-              if (j != cur_j) {
-                if (cur_j >= 0) {
-                  sk[cur_j][lane] = acc;
-                  if (lane == 0) {
-                    sk[cur_j][3] = (double)sx;
-                    sk[cur_j][4] = (double)sy;
-                    sk[cur_j][5] = (double)cnt;
-                  }
-                }
-                cur_j = j;
-                acc = 0.0;
-                sx = sy = cnt = 0;
-              }
-              acc = dadd(acc, (double)(lane == 0 ? v.x : (lane == 1 ? v.y : v.z)));
-              sx += wx0 + (int)(meta & 0xFFFu);
-              sy += ya + (int)((meta >> 12) & 0xFFFu);
-              cnt += 1;
-            }
+        // fold this block's rows in order; strips change only at row boundaries
+        for (int rr = 0; rr < rows; ++rr) {
+          const int b0 = rstart[warp][rr], b1 = rstart[warp][rr + 1];
+          if (b0 == b1) continue;
+          const int j = (yb + rr - ry0) / p.tile_len;
+          if (j != fold_j) {
+            if (fold_j >= 0) sk[fold_j][lane] = acc;
+            fold_j = j;
+            acc = 0.0;
           }
+          const float* src = cv[warp][lane];
+          int i = b0;
+          for (; i + 4 <= b1; i += 4) {
+            const float v0 = src[i], v1 = src[i + 1], v2 = src[i + 2], v3 = src[i + 3];
+            acc = dadd(acc, (double)v0);
+            acc = dadd(acc, (double)v1);
+            acc = dadd(acc, (double)v2);
+            acc = dadd(acc, (double)v3);
+          }
+          for (; i < b1; ++i) acc = dadd(acc, (double)src[i]);
+        }
       }
       __syncwarp();
     }
-    if (lane < 3 && cur_j >= 0) {
-      sk[cur_j][lane] = acc;
-      if (lane == 0) {
-        sk[cur_j][3] = (double)sx;
-        sk[cur_j][4] = (double)sy;
-        sk[cur_j][5] = (double)cnt;
-      }
+    if (lane < 3 && fold_j >= 0) sk[fold_j][lane] = acc;
+    if (lane == 0 && cur_j >= 0) {
+      sk[cur_j][3] = (double)sx;
+      sk[cur_j][4] = (double)sy;
+      sk[cur_j][5] = (double)cnt;
     }
     __syncwarp();
     if (lane == 0) {
@@ -702,7 +728,7 @@ int launch_reduce_cells(const Part* part, const float* img, const int32_t* label
   SPX_CUDA(cudaMemsetAsync(worklist_n, 0, sizeof(int32_t), st));
   k_reduce_cells<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_reduce_cells");
-  k_exact_clusters<<<(unsigned)num_sms() * 8, 128, 0, st>>>(p);
+  k_exact_clusters<<<(unsigned)num_sms() * 16, kExWarps * 32, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_exact_clusters");
   return SPX_OK;
 }
