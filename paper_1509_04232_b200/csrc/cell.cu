@@ -544,11 +544,16 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
           const bool m = lv[rr][cb] == fk;
           const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
           if (m) {
+            // asynchronous global -> shared copies: all of the block's value
+            // loads are in flight together (one DRAM round trip per block)
             const int pos = base + __popc(bm & lt);
-            const long long q = (long long)y * p.w + wx0 + col;
-            cv[warp][0][pos] = fabsf(__ldg(im + q));
-            cv[warp][1][pos] = __ldg(im + hw + q);
-            cv[warp][2][pos] = __ldg(im + 2 * hw + q);
+            const float* g = im + (long long)y * p.w + wx0 + col;
+            const unsigned d0 = (unsigned)__cvta_generic_to_shared(&cv[warp][0][pos]);
+            const unsigned d1 = (unsigned)__cvta_generic_to_shared(&cv[warp][1][pos]);
+            const unsigned d2 = (unsigned)__cvta_generic_to_shared(&cv[warp][2][pos]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d0), "l"(g));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d1), "l"(g + hw));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d2), "l"(g + 2 * hw));
           }
           rx += (int)__reduce_add_sync(0xFFFFFFFFu, m ? (unsigned)(wx0 + col) : 0u);
           rn += __popc(bm);
@@ -569,6 +574,7 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
         }
       }
       if (lane == 0) rstart[warp][rows] = base;
+      asm volatile("cp.async.wait_all;" ::: "memory");
       __syncwarp();
       if (lane < 3) {
         // fold this block's rows in order; strips change only at row boundaries
@@ -583,14 +589,22 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
           }
           const float* src = cv[warp][lane];
           int i = b0;
+          // channel 0 carries the certified-sum flag in its sign bit: |L|
+          const bool l0 = lane == 0;
           for (; i + 4 <= b1; i += 4) {
-            const float v0 = src[i], v1 = src[i + 1], v2 = src[i + 2], v3 = src[i + 3];
+            float v0 = src[i], v1 = src[i + 1], v2 = src[i + 2], v3 = src[i + 3];
+            if (l0) {
+              v0 = fabsf(v0);
+              v1 = fabsf(v1);
+              v2 = fabsf(v2);
+              v3 = fabsf(v3);
+            }
             acc = dadd(acc, (double)v0);
             acc = dadd(acc, (double)v1);
             acc = dadd(acc, (double)v2);
             acc = dadd(acc, (double)v3);
           }
-          for (; i < b1; ++i) acc = dadd(acc, (double)src[i]);
+          for (; i < b1; ++i) acc = dadd(acc, (double)(l0 ? fabsf(src[i]) : src[i]));
         }
       }
       __syncwarp();
