@@ -69,7 +69,7 @@ struct CellParams {
   const double* clab;      // [F][K][3]
   const CRec* rec;         // [F][K]     fp32 records of the current centres
   int32_t* labels;         // [F][H][W]
-  Part* part;              // [F][K][9]  (ACC only)
+  ClusterAcc* acc;         // [F][K]     (ACC only) atomically accumulated sums
   const int32_t* done;     // per frame, skip == 1 (may be null)
   int h, w, s, ns_r, ns_c, frames;
   int lanes_per_cell;      // 32 or 16
@@ -131,7 +131,6 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   // grid: x = cell groups of one frame, y = frame (no 64-bit divisions)
   const int f = blockIdx.y;
   const int cell = (blockIdx.x * kWarps + warp) * cpw + ci;
-  const long long gcell = (long long)f * K + cell;
   unsigned char* wbase = smem + (size_t)warp * (ACC ? kWarpSmemAcc : kWarpSmemNoAcc);
   CandPairs* cand = reinterpret_cast<CandPairs*>(wbase) + ci * 9;
   int* cand_k = reinterpret_cast<int*>(wbase + sizeof(CandPairs) * 18) + ci * 9;
@@ -319,9 +318,14 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   __syncwarp();
   // ---- per-cell column reduction: 9 slots x (3 colour + 1 packed int) -------
   // column c < 27: colour (slot c/3, channel c%3); 27 <= c < 36: ints of slot
-  // c-27.  Each column holds lpc lane entries, read as 16-byte vectors.
+  // c-27.  Each column holds lpc lane entries, read as 16-byte vectors.  The
+  // cell's per-slot sums go straight into the owning cluster's accumulator
+  // with global atomics: under the certified-sum condition every partial sum
+  // is exact, so the result does not depend on the order of the atomics
+  // (flagged clusters are recomputed exactly by k_exact_clusters).
   const int lane0 = ci * lpc;
   if (active) {
+    ClusterAcc* fa = p.acc + (long long)f * K;
     for (int col = ll; col < 36; col += lpc) {
       if (col < 27) {
         const double2* src = reinterpret_cast<const double2*>(accd + col * 32 + lane0);
@@ -330,7 +334,8 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
           const double2 v = src[q];
           sacc = dadd(dadd(sacc, v.x), v.y);
         }
-        p.part[gcell * 9 + col / 3].s[col % 3] = sacc;
+        // an empty (or out-of-grid) slot sums to +0.0: nothing to add
+        if (sacc != 0.0) atomicAdd(&fa[cand_k[col / 3]].s[col % 3], sacc);
       } else {
         const ulonglong2* src = reinterpret_cast<const ulonglong2*>(acci + (col - 27) * 32 + lane0);
         unsigned long long tot = 0;
@@ -338,11 +343,14 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
           const ulonglong2 v = src[q];
           tot += v.x + v.y;  // fields cannot overflow (see packing above)
         }
-        Part* o = p.part + gcell * 9 + (col - 27);
-        o->cnt = (int)(tot & 2047ull);
-        o->flag = (int)((tot >> 11) & 2047ull);
-        o->sx = (int)((tot >> 22) & 0x1FFFFFull);
-        o->sy = (int)(tot >> 43);
+        const unsigned long long cnt = tot & 2047ull;
+        if (cnt) {
+          ClusterAcc* o = fa + cand_k[col - 27];
+          const unsigned long long flg = (tot >> 11) & 2047ull;
+          atomicAdd(&o->sx, ((tot >> 22) & 0x1FFFFFull) + cnt * (unsigned long long)x_cell);
+          atomicAdd(&o->sy, (tot >> 43) + cnt * (unsigned long long)y_cell);
+          atomicAdd(&o->cf, cnt | (flg << 32));
+        }
       }
     }
   }
@@ -373,7 +381,7 @@ __global__ void k_records(const double* __restrict__ cxy, const double* __restri
 }
 
 struct ReduceParams {
-  const Part* part;
+  ClusterAcc* acc;
   const float* img;
   const int32_t* labels;
   const double* prev_xy;
@@ -440,29 +448,17 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
     todo = !(p.done && p.done[f]);
   }
   if (todo) {
-    const Part* pf = p.part + (long long)f * K * 9;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    long long sx = 0, sy = 0, cnt = 0;
-    int fl = 0;
-    // cell (kr - dr, kc - dc) sees this cluster at offset (dr, dc)
-    for (int dr = -1; dr <= 1; ++dr)
-      for (int dc = -1; dc <= 1; ++dc) {
-        const int r2 = kr - dr, c2 = kc - dc;
-        if (r2 < 0 || r2 >= p.ns_r || c2 < 0 || c2 >= p.ns_c) continue;
-        const int idx = (dr + 1) * 3 + (dc + 1);
-        const int t = idx < 4 ? idx + 1 : (idx == 4 ? 0 : idx);
-        const Part q = pf[(long long)(r2 * p.ns_c + c2) * 9 + t];
-        s0 = dadd(s0, q.s[0]);
-        s1 = dadd(s1, q.s[1]);
-        s2 = dadd(s2, q.s[2]);
-        sx += (long long)q.sx + (long long)q.cnt * c2 * p.s;
-        sy += (long long)q.sy + (long long)q.cnt * r2 * p.s;
-        cnt += q.cnt;
-        fl |= q.flag;
-      }
+    ClusterAcc* a = p.acc + gk;
+    const double4 s012 = *reinterpret_cast<const double4*>(a);  // s[0..2], sx
+    const ulonglong2 syc = *reinterpret_cast<const ulonglong2*>(&a->sy);
+    // consume and clear for the next pass
+    *reinterpret_cast<double4*>(a) = make_double4(0.0, 0.0, 0.0, 0.0);
+    *reinterpret_cast<ulonglong2*>(&a->sy) = make_ulonglong2(0ull, 0ull);
+    const unsigned long long sx = __double_as_longlong(s012.w);
+    const unsigned long long cnt = syc.y & 0xFFFFFFFFull, fl = syc.y >> 32;
     flagged = fl != 0;
     if (!flagged)
-      write_centre(p, gk, kr, kc, (double)cnt, s0, s1, s2, (double)sx, (double)sy);
+      write_centre(p, gk, kr, kc, (double)cnt, s012.x, s012.y, s012.z, (double)sx, (double)syc.x);
   }
   if (flagged) p.worklist[atomicAdd(p.worklist_n, 1)] = (int32_t)gk;
 }
@@ -658,8 +654,8 @@ void assoc_bound_coefficients(double xy_weight, float& w32, float& k_mp, float& 
                               float& k_const, float& k_rel);
 
 int launch_cell(const float* img, const double* cxy, const double* clab, const CRec* rec,
-                int32_t* labels, Part* part, const int32_t* done, int64_t h, int64_t w, int64_t s,
-                int64_t ns_r, int64_t ns_c, double xy_weight, int frames, bool acc,
+                int32_t* labels, ClusterAcc* sums, const int32_t* done, int64_t h, int64_t w,
+                int64_t s, int64_t ns_r, int64_t ns_c, double xy_weight, int frames, bool acc,
                 cudaStream_t st) {
   CellParams p;
   p.img = img;
@@ -667,7 +663,7 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.clab = clab;
   p.rec = rec;
   p.labels = labels;
-  p.part = part;
+  p.acc = sums;
   p.done = done;
   p.h = (int)h;
   p.w = (int)w;
@@ -713,14 +709,14 @@ int launch_records(const double* cxy, const double* clab, CRec* rec, int64_t ns_
   return SPX_OK;
 }
 
-int launch_reduce_cells(const Part* part, const float* img, const int32_t* labels,
+int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels,
                         const double* prev_xy, const double* prev_lab, double* out_xy,
                         double* out_lab, int64_t* counts, CRec* rec, const int32_t* done,
                         int32_t* worklist, int32_t* worklist_n, int64_t h, int64_t w, int64_t s,
                         int64_t ns_r, int64_t ns_c, int64_t tile_len, int frames,
                         cudaStream_t st) {
   ReduceParams p;
-  p.part = part;
+  p.acc = acc;
   p.img = img;
   p.labels = labels;
   p.prev_xy = prev_xy;
@@ -752,7 +748,7 @@ int launch_reduce_cells(const Part* part, const float* img, const int32_t* label
                                     (int)xs));
       xcfg = xs;
     }
-    k_exact_clusters<<<(unsigned)num_sms() * 8, kExThreads, xs, st>>>(p);
+    k_exact_clusters<<<(unsigned)num_sms() * 24, kExThreads, xs, st>>>(p);
   }
   SPX_LAUNCH_CHECK("k_exact_clusters");
   return SPX_OK;

@@ -30,12 +30,12 @@ int launch_weak2(const int32_t*, int32_t*, int64_t, int64_t, int, cudaStream_t);
 int launch_strict(const int32_t*, int32_t*, int64_t, int64_t, int, int64_t, int64_t, int32_t*,
                   int32_t*, int32_t*, int32_t*, cudaStream_t);
 bool cell_path_ok(int64_t, int64_t, int64_t, int64_t);
-int launch_cell(const float*, const double*, const double*, const CRec*, int32_t*, Part*,
+int launch_cell(const float*, const double*, const double*, const CRec*, int32_t*, ClusterAcc*,
                 const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, double, int, bool,
                 cudaStream_t);
 int launch_records(const double*, const double*, CRec*, int64_t, int64_t, int64_t, int,
                    cudaStream_t);
-int launch_reduce_cells(const Part*, const float*, const int32_t*, const double*, const double*,
+int launch_reduce_cells(ClusterAcc*, const float*, const int32_t*, const double*, const double*,
                         double*, double*, int64_t*, CRec*, const int32_t*, int32_t*, int32_t*,
                         int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t);
 int launch_fill_i32(int32_t*, int, int, cudaStream_t);
@@ -78,7 +78,7 @@ struct Engine {
   int32_t* passes = nullptr;
   int32_t *cc_parent = nullptr, *cc_size = nullptr, *cc_nxt = nullptr, *cc_first = nullptr;
   CRec* rec = nullptr;   // fp32 filter records of the current centres (cell path)
-  Part* part = nullptr;  // per (cell, slot) partial sums (cell path)
+  ClusterAcc* acc = nullptr;  // per-cluster update accumulators (cell path)
   int32_t* worklist = nullptr;  // flagged clusters for the exact fallback (cell path)
   bool use_cell = false;
   cudaEvent_t ev[EV_FIXED] = {};
@@ -91,7 +91,7 @@ struct Engine {
     for (void* p : {(void*)lab, (void*)labels, (void*)scratch, (void*)cxy[0], (void*)cxy[1],
                     (void*)clab[0], (void*)clab[1], (void*)slab, (void*)done, (void*)passes,
                     (void*)cc_parent, (void*)cc_size, (void*)cc_nxt, (void*)cc_first,
-                    (void*)rec, (void*)part, (void*)worklist})
+                    (void*)rec, (void*)acc, (void*)worklist})
       if (p) cudaFree(p);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -128,7 +128,7 @@ struct Engine {
     use_cell = cell_path_ok(st.height, st.width, st.s, st.tile_len) && K < (1ll << 31);
     if (use_cell) {
       SPX_CUDA(cudaMalloc(&rec, B * K * sizeof(CRec)));
-      SPX_CUDA(cudaMalloc(&part, B * K * 9 * sizeof(Part)));
+      SPX_CUDA(cudaMalloc(&acc, B * K * sizeof(ClusterAcc)));
       SPX_CUDA(cudaMalloc(&worklist, (B * K + 1) * sizeof(int32_t)));
     } else {
       SPX_CUDA(cudaMalloc(&slab, B * K * n_bl * 6 * sizeof(double)));
@@ -154,10 +154,11 @@ struct Engine {
     return v[i];
   }
 
-  int associate(int cur, int frames, const int32_t* dn, bool acc, cudaStream_t s) {
+  int associate(int cur, int frames, const int32_t* dn, bool with_update, cudaStream_t s) {
     cudaEventRecord(pass_event(ev_assoc, 2 * n_assoc), s);
-    int rc = use_cell ? launch_cell(lab, cxy[cur], clab[cur], rec, labels, part, dn, st.height,
-                                    st.width, st.s, st.ns_r, st.ns_c, xy_weight, frames, acc, s)
+    int rc = use_cell ? launch_cell(lab, cxy[cur], clab[cur], rec, labels, acc, dn, st.height,
+                                    st.width, st.s, st.ns_r, st.ns_c, xy_weight, frames,
+                                    with_update, s)
                       : launch_assoc(lab, cxy[cur], clab[cur], labels, dn, st.height, st.width,
                                      st.s, st.ns_r, st.ns_c, xy_weight, 0, st.height, frames, K, s);
     cudaEventRecord(pass_event(ev_assoc, 2 * n_assoc + 1), s);
@@ -198,6 +199,7 @@ struct Engine {
     if (use_cell) {
       if ((rc = launch_records(cxy[0], clab[0], rec, st.ns_r, st.ns_c, st.s, B, s))) return rc;
       ++launches;
+      SPX_CUDA(cudaMemsetAsync(acc, 0, (size_t)B * K * sizeof(ClusterAcc), s));
     }
     cudaEventRecord(ev[EV_PERTURB], s);
     if (early) {
@@ -209,7 +211,7 @@ struct Engine {
     for (int it = 0; it < st.no_iters; ++it) {
       cudaEventRecord(pass_event(ev_update, 2 * n_update), s);
       if (use_cell) {
-        if ((rc = launch_reduce_cells(part, lab, labels, cxy[cur], clab[cur], cxy[nxt], clab[nxt],
+        if ((rc = launch_reduce_cells(acc, lab, labels, cxy[cur], clab[cur], cxy[nxt], clab[nxt],
                                       out_counts, rec, dn, worklist, worklist + max_batch * K,
                                       st.height, st.width, st.s, st.ns_r, st.ns_c, st.tile_len, B,
                                       s)))
@@ -307,7 +309,7 @@ struct Engine {
 
   int ensure_staging() {
     if (s_comp) return SPX_OK;
-    chunk = std::max<int64_t>(1, std::min<int64_t>(max_batch, 32));
+    chunk = std::max<int64_t>(1, std::min<int64_t>(max_batch, 64));
     for (int i = 0; i < 2; ++i) {
       SPX_CUDA(cudaMalloc(&h_rgb[i], chunk * hw * 3));
       SPX_CUDA(cudaMalloc(&h_lab[i], chunk * hw * sizeof(int32_t)));
