@@ -463,36 +463,33 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
   if (flagged) p.worklist[atomicAdd(p.worklist_n, 1)] = (int32_t)gk;
 }
 
-// Exact recomputation of flagged clusters (certificate failed): one CTA per
+// Exact recomputation of flagged clusters (certificate failed): one warp per
 // cluster, latency-oriented (a handful of clusters per frame are flagged, so
-// this kernel's duration is about one cluster's latency).
-//   1. the cluster's whole 3Sx3S label window is staged into shared memory
-//      with 16-byte cp.async (one DRAM round trip);
-//   2. each warp takes rows, ballots the members and reduces x / y / count per
-//      row with REDUX; a row-offset scan compacts the members in row-major
-//      order, and their planar Lab values are fetched with cp.async (a second
-//      round trip, in chunks of kExVals);
-//   3. lanes 0..2 of warp 0 fold the three colour channels in exactly the
-//      reference's order (_core.pyx:233-243), each strip from 0.0, and apply
-//      the pairwise strip tree (_core.pyx:300-311).
-// Pipeline labels never spill, so the window holds every member.
-constexpr int kExThreads = 128;
-constexpr int kExVals = 1024;  // compacted members staged per chunk
+// this kernel's duration is one cluster's latency).  The 3Sx3S window is
+// walked in blocks of kRows rows with the next block's label loads in flight
+// while the current one is folded.  Per row, lanes own columns; matches are
+// compacted in row-major order into shared memory (ballot + popc), x / y /
+// count are reduced per row with REDUX.  Lanes 0..2 then fold the three
+// colour channels in exactly the reference's order (_core.pyx:233-243), each
+// strip from 0.0, and lane 0 applies the pairwise strip tree
+// (_core.pyx:300-311).  Pipeline labels never spill, so the window holds
+// every member.
+constexpr int kRows = 8;
+constexpr int kCols = 96;  // window width 3S <= 96 (S <= 32)
+constexpr int kExWarps = 2;
 
-__global__ void __launch_bounds__(kExThreads) k_exact_clusters(ReduceParams p) {
-  extern __shared__ __align__(16) unsigned char xsm[];
-  __shared__ double sk[32][6];
-  __shared__ float cv[3][kExVals];
-  __shared__ int rcount[3 * 32 + 1];      // members per window row (<= 96 rows)
-  __shared__ int roff[3 * 32 + 1];        // exclusive prefix
-  __shared__ long long rsx[3 * 32];       // per-row x sums
-  int32_t* wlab = reinterpret_cast<int32_t*>(xsm);  // window labels [rows][ww]
+__global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p) {
+  __shared__ double strips[kExWarps][32][6];
+  __shared__ float cv[kExWarps][3][kRows * kCols];  // compacted l / a / b
+  __shared__ int rstart[kExWarps][kRows + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.ns_r * p.ns_c;
   const int n = *p.worklist_n;
+  const int nwarps = gridDim.x * kExWarps;
+  double (*sk)[6] = strips[warp];
   const long long hw = (long long)p.h * p.w;
   const unsigned lt = (1u << lane) - 1u;
-  for (int item = blockIdx.x; item < n; item += gridDim.x) {
+  for (int item = blockIdx.x * kExWarps + warp; item < n; item += nwarps) {
     const int gk = p.worklist[item];
     const int ff = gk / K, fk = gk - ff * K;
     const float* im = p.img + (long long)ff * 3 * hw;  // planar [3][H][W]
@@ -501,90 +498,98 @@ __global__ void __launch_bounds__(kExThreads) k_exact_clusters(ReduceParams p) {
     const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
     const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
     const int ya = max(ry0, 0);
-    const int ww = wx1 - wx0, nrows = ry1 - ya;  // ww % 4 == 0 on the cell path
-    const int q4 = ww >> 2;
-    // 1. window labels -> smem
-    for (int i = threadIdx.x; i < nrows * q4; i += kExThreads) {
-      const int rr = i / q4, qq = i - rr * q4;
-      const unsigned d = (unsigned)__cvta_generic_to_shared(wlab + rr * ww + qq * 4);
-      const int32_t* g = lb + (long long)(ya + rr) * p.w + wx0 + qq * 4;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(g));
-    }
-    if (threadIdx.x < p.n_bl)
-      for (int comp = 0; comp < 6; ++comp) sk[threadIdx.x][comp] = 0.0;
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    // 2a. per-row member counts and x sums
-    for (int rr = warp; rr < nrows; rr += kExThreads / 32) {
-      int cntr = 0;
-      unsigned sxr = 0;
-      for (int cb = 0; cb < ww; cb += 32) {
-        const int col = cb + lane;
-        const bool m = col < ww && wlab[rr * ww + col] == fk;
-        cntr += __popc(__ballot_sync(0xFFFFFFFFu, m));
-        sxr += __reduce_add_sync(0xFFFFFFFFu, m ? (unsigned)(wx0 + col) : 0u);
-      }
-      if (lane == 0) {
-        rcount[rr] = cntr;
-        rsx[rr] = sxr;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int acc_n = 0;
-      for (int rr = 0; rr < nrows; ++rr) {
-        roff[rr] = acc_n;
-        acc_n += rcount[rr];
-      }
-      roff[nrows] = acc_n;
-    }
-    __syncthreads();
-    const int total = roff[nrows];
-    // strip bookkeeping for lanes 0..2 of warp 0 (colour folds)
-    int fold_j = -1;
+    const int ww = wx1 - wx0;
+    const int ncb = (ww + 31) >> 5;  // column blocks of 32 (<= 3)
+    if (lane < p.n_bl)
+      for (int comp = 0; comp < 6; ++comp) sk[lane][comp] = 0.0;
+    int cur_j = -1, fold_j = -1;
     double acc = 0.0;
-    for (int c0 = 0; c0 < total; c0 += kExVals) {
-      const int c1 = min(c0 + kExVals, total);
-      // 2b. compact members with index in [c0, c1) and fetch their values
-      for (int rr = warp; rr < nrows; rr += kExThreads / 32) {
-        if (roff[rr + 1] <= c0 || roff[rr] >= c1) continue;
-        int pos = roff[rr];
-        for (int cb = 0; cb < ww; cb += 32) {
-          const int col = cb + lane;
-          const bool m = col < ww && wlab[rr * ww + col] == fk;
+    long long sx = 0, sy = 0, cnt = 0;  // lane 0: running strip totals
+    int32_t nxt[kRows][3];
+    auto load_block = [&](int yb, int32_t (&lv)[kRows][3]) {
+#pragma unroll
+      for (int rr = 0; rr < kRows; ++rr)
+#pragma unroll
+        for (int cb = 0; cb < 3; ++cb) {
+          const int col = cb * 32 + lane;
+          lv[rr][cb] = (yb + rr < ry1 && col < ww)
+                           ? __ldg(lb + (long long)(yb + rr) * p.w + wx0 + col)
+                           : -1;
+        }
+    };
+    load_block(ya, nxt);
+    for (int yb = ya; yb < ry1; yb += kRows) {
+      int32_t lv[kRows][3];
+#pragma unroll
+      for (int rr = 0; rr < kRows; ++rr)
+#pragma unroll
+        for (int cb = 0; cb < 3; ++cb) lv[rr][cb] = nxt[rr][cb];
+      if (yb + kRows < ry1) load_block(yb + kRows, nxt);  // prefetch the next block
+      const int rows = min(kRows, ry1 - yb);
+      int base = 0;
+#pragma unroll
+      for (int rr = 0; rr < kRows; ++rr) {
+        if (rr >= rows) break;
+        const int y = yb + rr;
+        if (lane == 0) rstart[warp][rr] = base;
+        int rx = 0, rn = 0;
+#pragma unroll
+        for (int cb = 0; cb < 3; ++cb) {
+          if (cb >= ncb) break;
+          const int col = cb * 32 + lane;
+          const bool m = lv[rr][cb] == fk;
           const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
-          const int my = pos + __popc(bm & lt);
-          if (m && my >= c0 && my < c1) {
-            const float* g = im + (long long)(ya + rr) * p.w + wx0 + col;
-            const int o = my - c0;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                             (unsigned)__cvta_generic_to_shared(&cv[0][o])), "l"(g));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                             (unsigned)__cvta_generic_to_shared(&cv[1][o])), "l"(g + hw));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                             (unsigned)__cvta_generic_to_shared(&cv[2][o])), "l"(g + 2 * hw));
+          if (m) {
+            // asynchronous global -> shared copies: all of the block's value
+            // loads are in flight together (one DRAM round trip per block)
+            const int pos = base + __popc(bm & lt);
+            const float* g = im + (long long)y * p.w + wx0 + col;
+            const unsigned d0 = (unsigned)__cvta_generic_to_shared(&cv[warp][0][pos]);
+            const unsigned d1 = (unsigned)__cvta_generic_to_shared(&cv[warp][1][pos]);
+            const unsigned d2 = (unsigned)__cvta_generic_to_shared(&cv[warp][2][pos]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d0), "l"(g));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d1), "l"(g + hw));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d2), "l"(g + 2 * hw));
           }
-          pos += __popc(bm);
+          rx += (int)__reduce_add_sync(0xFFFFFFFFu, m ? (unsigned)(wx0 + col) : 0u);
+          rn += __popc(bm);
+          base += __popc(bm);
+        }
+        if (lane == 0 && rn) {
+          const int j = (y - ry0) / p.tile_len;
+          if (j != cur_j && cur_j >= 0) {
+            sk[cur_j][3] = (double)sx;
+            sk[cur_j][4] = (double)sy;
+            sk[cur_j][5] = (double)cnt;
+            sx = sy = cnt = 0;
+          }
+          if (j != cur_j) cur_j = j;  // lanes 1, 2 track cur_j below
+          sx += rx;
+          sy += (long long)y * rn;
+          cnt += rn;
         }
       }
+      if (lane == 0) rstart[warp][rows] = base;
       asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncthreads();
-      // 3. ordered folds (rows in order; strips change only at row boundaries)
-      if (warp == 0 && lane < 3) {
-        const float* src = cv[lane];
-        for (int rr = 0; rr < nrows; ++rr) {
-          const int b0 = max(roff[rr], c0), b1 = min(roff[rr + 1], c1);
-          if (b0 >= b1) continue;
-          const int j = (ya + rr - ry0) / p.tile_len;
+      __syncwarp();
+      if (lane < 3) {
+        // fold this block's rows in order; strips change only at row boundaries
+        for (int rr = 0; rr < rows; ++rr) {
+          const int b0 = rstart[warp][rr], b1 = rstart[warp][rr + 1];
+          if (b0 == b1) continue;
+          const int j = (yb + rr - ry0) / p.tile_len;
           if (j != fold_j) {
             if (fold_j >= 0) sk[fold_j][lane] = acc;
             fold_j = j;
             acc = 0.0;
           }
+          const float* src = cv[warp][lane];
           int i = b0;
+          // channel 0 carries the certified-sum flag in its sign bit: |L|
+          const bool l0 = lane == 0;
           for (; i + 4 <= b1; i += 4) {
-            float v0 = src[i - c0], v1 = src[i + 1 - c0], v2 = src[i + 2 - c0], v3 = src[i + 3 - c0];
-            if (lane == 0) {  // channel 0 carries the certified-sum flag in its sign bit
+            float v0 = src[i], v1 = src[i + 1], v2 = src[i + 2], v3 = src[i + 3];
+            if (l0) {
               v0 = fabsf(v0);
               v1 = fabsf(v1);
               v2 = fabsf(v2);
@@ -595,38 +600,31 @@ __global__ void __launch_bounds__(kExThreads) k_exact_clusters(ReduceParams p) {
             acc = dadd(acc, (double)v2);
             acc = dadd(acc, (double)v3);
           }
-          for (; i < b1; ++i) {
-            const float v = src[i - c0];
-            acc = dadd(acc, (double)(lane == 0 ? fabsf(v) : v));
-          }
+          for (; i < b1; ++i) acc = dadd(acc, (double)(l0 ? fabsf(src[i]) : src[i]));
         }
       }
-      __syncthreads();
+      __syncwarp();
     }
-    if (warp == 0) {
-      if (lane < 3 && fold_j >= 0) sk[fold_j][lane] = acc;
-      if (lane == 0) {
-        // integer sums per strip (order-free)
-        for (int rr = 0; rr < nrows; ++rr) {
-          if (!rcount[rr]) continue;
-          const int j = (ya + rr - ry0) / p.tile_len;
-          sk[j][3] += (double)rsx[rr];
-          sk[j][4] += (double)((long long)(ya + rr) * rcount[rr]);
-          sk[j][5] += (double)rcount[rr];
-        }
-        int m = p.n_bl;
-        while (m > 1) {  // pairwise strip tree, _core.pyx:300-311
-          int half = m >> 1;
-          for (int i = 0; i < half; ++i)
-            for (int comp = 0; comp < 6; ++comp) sk[i][comp] = dadd(sk[2 * i][comp], sk[2 * i + 1][comp]);
-          if (m & 1)
-            for (int comp = 0; comp < 6; ++comp) sk[half][comp] = sk[m - 1][comp];
-          m = half + (m & 1);
-        }
-        write_centre(p, gk, r, c, sk[0][5], sk[0][0], sk[0][1], sk[0][2], sk[0][3], sk[0][4]);
+    if (lane < 3 && fold_j >= 0) sk[fold_j][lane] = acc;
+    if (lane == 0 && cur_j >= 0) {
+      sk[cur_j][3] = (double)sx;
+      sk[cur_j][4] = (double)sy;
+      sk[cur_j][5] = (double)cnt;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      int m = p.n_bl;
+      while (m > 1) {  // pairwise strip tree, _core.pyx:300-311
+        int half = m >> 1;
+        for (int i = 0; i < half; ++i)
+          for (int comp = 0; comp < 6; ++comp) sk[i][comp] = dadd(sk[2 * i][comp], sk[2 * i + 1][comp]);
+        if (m & 1)
+          for (int comp = 0; comp < 6; ++comp) sk[half][comp] = sk[m - 1][comp];
+        m = half + (m & 1);
       }
+      write_centre(p, gk, r, c, sk[0][5], sk[0][0], sk[0][1], sk[0][2], sk[0][3], sk[0][4]);
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
@@ -740,16 +738,7 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   SPX_CUDA(cudaMemsetAsync(worklist_n, 0, sizeof(int32_t), st));
   k_reduce_cells<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_reduce_cells");
-  {
-    const size_t xs = (size_t)9 * s * s * sizeof(int32_t);  // label window
-    static size_t xcfg = 0;
-    if (xs > 48 * 1024 - 20000 && xs > xcfg) {
-      SPX_CUDA(cudaFuncSetAttribute(k_exact_clusters, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)xs));
-      xcfg = xs;
-    }
-    k_exact_clusters<<<(unsigned)num_sms() * 24, kExThreads, xs, st>>>(p);
-  }
+  k_exact_clusters<<<(unsigned)num_sms() * 16, kExWarps * 32, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_exact_clusters");
   return SPX_OK;
 }
