@@ -29,7 +29,8 @@ def launches(path, out):
     ki, mi, vi, ui = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
     tot = collections.defaultdict(float)
     cnt = collections.Counter()
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3,
+             "second": 1e6}
     for r in data:
         if len(r) > mi and r[mi] == "gpu__time_duration.sum":
             name = r[ki].split("(")[0].replace("void ", "")
@@ -66,11 +67,24 @@ def report(rep, out, traffic_json=None, pixels=None):
     for r in det[1:]:
         if r[mi] in WANT:
             per.setdefault((r[ii], r[ki].split("(")[0]), {})[r[mi]] = f"{r[vi]} {r[ui]}".strip()
-    rh = raw[0]
+    rh, ru = raw[0], raw[1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3,
+             "usecond": 1.0, "msecond": 1e3}
     rawvals = {}
     for r in raw[2:]:
         key = r[rh.index("ID")]
-        rawvals[key] = {m: r[rh.index(m)] for m in RAW if m in rh}
+        vals = {}
+        for m in RAW:
+            if m in rh:
+                i = rh.index(m)
+                unit = ru[i]
+                try:
+                    v = float(r[i].replace(",", "")) * scale.get(unit, 1.0)
+                    unit = "byte" if unit.endswith("byte") else ("us" if unit.endswith("second") else unit)
+                    vals[m] = f"{v:.6g} {unit}"
+                except ValueError:
+                    vals[m] = r[i]
+        rawvals[key] = vals
     lines = []
     traffic = {}
     for (i, name), m in per.items():
@@ -82,8 +96,8 @@ def report(rep, out, traffic_json=None, pixels=None):
         for k, v in rv.items():
             lines.append(f"- {k}: {v}")
         try:
-            b = float(rv["dram__bytes_read.sum"].replace(",", "")) + float(
-                rv["dram__bytes_write.sum"].replace(",", ""))
+            b = float(rv["dram__bytes_read.sum"].split()[0]) + float(
+                rv["dram__bytes_write.sum"].split()[0])
             traffic.setdefault(name, []).append(b)
         except (KeyError, ValueError):
             pass
@@ -91,10 +105,12 @@ def report(rep, out, traffic_json=None, pixels=None):
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if traffic_json and pixels:
-        assoc = [v for k, vs in traffic.items() if "k_cell" in k for v in vs]
+        assoc = [v for k, vs in traffic.items() if "k_cell<1>" in k or "k_cell<true>" in k for v in vs]
         if assoc:
-            json.dump({"kernel": "k_cell", "dram_bytes_per_pixel": sum(assoc) / len(assoc) / float(pixels),
-                       "source": rep, "launches": len(assoc)}, open(traffic_json, "w"), indent=1)
+            json.dump({"kernel": "k_cell<ACC> (association + centre-update pass)",
+                       "dram_bytes_per_pixel": sum(assoc) / len(assoc) / float(pixels),
+                       "pixels_per_launch": int(pixels), "source": rep, "launches": len(assoc)},
+                      open(traffic_json, "w"), indent=1)
 
 
 if __name__ == "__main__":
