@@ -57,11 +57,6 @@ SPX_API int32_t spx_debug_tables(double *lut, double *mat, double *white);
 /* Test hook: max relative error of the association filter's fp32 sqrt over
  * all floats in [1,4) (the error bound assumes <= 2^-21).  Synchronous. */
 SPX_API int32_t spx_debug_sqrt_error(double *out_host);
-/* Test hook: the engine's table-driven convert (planar [3][npx] output, the
- * certified-sum flag of grid interval s in channel 0's sign bit) of npx
- * device pixels (npx % 4 == 0).  Synchronous. */
-SPX_API int32_t spx_debug_convert_engine(const uint8_t *rgb, float *out, int64_t npx,
-                                         int32_t space, int64_t s);
 
 /* ---- kernel protocol: replaces pkg/src/superpix/kernels/_core.pyx ---------- */
 

@@ -12,8 +12,6 @@
 // arithmetic (three glibc-cbrt evaluations with a division each, three
 // divisions by the white point) makes this kernel FP64-pipe bound on B200;
 // see DESIGN.md.
-#include <algorithm>
-
 #include "spx_internal.cuh"
 
 namespace spx {
@@ -206,107 +204,6 @@ __global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb
 
 // planar_hw > 0: the engine's planar layout with the certified-sum flag of
 // grid interval `s` in channel 0's sign bit.
-// ---- exact colour table (engine path) -----------------------------------------
-// The convert output depends only on the 24-bit RGB triple, so the engine
-// gathers it from a 2^24-entry float4 table (268 MB of HBM per colour space)
-// built once per process by the exact kernel above: bit-identical by
-// construction, and the per-pixel cost drops from ~150 binary64 operations
-// (three glibc cbrt, six divisions) to one 16-byte gather.
-template <int SPACE>
-__global__ void __launch_bounds__(256) k_build_lut(float4* __restrict__ lut) {
-  __shared__ double tab[256];
-  if (SPACE != 0) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = g_lut[i];
-    __syncthreads();
-  }
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < (1u << 24);
-       c += gridDim.x * blockDim.x) {
-    float o0, o1, o2;
-    convert_px<SPACE>(tab, (c >> 16) & 255u, (c >> 8) & 255u, c & 255u, o0, o1, o2);
-    lut[c] = make_float4(o0, o1, o2, 0.f);
-  }
-}
-
-// Planar engine convert through the table; frames contiguous, hw % 4 == 0.
-__global__ void __launch_bounds__(256) k_convert_lut(const uint8_t* __restrict__ rgb,
-                                                     const float4* __restrict__ lut,
-                                                     float* __restrict__ out, int64_t groups,
-                                                     int64_t hw, float tau) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
-    const int64_t q = g << 2;
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(rgb + q * 3);
-    const uint32_t w0 = __ldg(src), w1 = __ldg(src + 1), w2 = __ldg(src + 2);
-    // 4 pixels = bytes r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3 (little endian)
-    const uint32_t i0 = ((w0 & 0xFFu) << 16) | (w0 & 0xFF00u) | ((w0 >> 16) & 0xFFu);
-    const uint32_t i1 = ((w0 >> 24) << 16) | ((w1 & 0xFFu) << 8) | ((w1 >> 8) & 0xFFu);
-    const uint32_t i2 = (((w1 >> 16) & 0xFFu) << 16) | ((w1 >> 24) << 8) | (w2 & 0xFFu);
-    const uint32_t i3 = (((w2 >> 8) & 0xFFu) << 16) | (((w2 >> 16) & 0xFFu) << 8) | (w2 >> 24);
-    const float4 v0 = __ldg(lut + i0), v1 = __ldg(lut + i1), v2 = __ldg(lut + i2),
-                 v3 = __ldg(lut + i3);
-    const int64_t f = q / hw, r = q - f * hw;
-    float* base = out + f * 3 * hw + r;
-    *reinterpret_cast<float4*>(base) =
-        make_float4(with_flag(v0.x, v0.y, v0.z, tau), with_flag(v1.x, v1.y, v1.z, tau),
-                    with_flag(v2.x, v2.y, v2.z, tau), with_flag(v3.x, v3.y, v3.z, tau));
-    *reinterpret_cast<float4*>(base + hw) = make_float4(v0.y, v1.y, v2.y, v3.y);
-    *reinterpret_cast<float4*>(base + 2 * hw) = make_float4(v0.z, v1.z, v2.z, v3.z);
-  }
-}
-
-constexpr int kMaxDevices = 64;
-static float4* g_colour_lut[3][kMaxDevices] = {};
-
-// Process-wide table for `space` on the current device, built on first use
-// and kept for the life of the process (268 MB per colour space per device).
-int colour_lut(int space, cudaStream_t st, const float4** out) {
-  int dev = 0;
-  SPX_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= kMaxDevices) {
-    set_error("device index %d out of range", dev);
-    return SPX_ERR_VALUE;
-  }
-  if (g_colour_lut[space][dev]) {
-    *out = g_colour_lut[space][dev];
-    return SPX_OK;
-  }
-  int rc = upload_tables();
-  if (rc) return rc;
-  float4* lut = nullptr;
-  SPX_CUDA(cudaMalloc(&lut, sizeof(float4) << 24));
-  const unsigned blocks = (unsigned)num_sms() * 8;
-  switch (space) {
-    case 0: k_build_lut<0><<<blocks, 256, 0, st>>>(lut); break;
-    case 1: k_build_lut<1><<<blocks, 256, 0, st>>>(lut); break;
-    default: k_build_lut<2><<<blocks, 256, 0, st>>>(lut); break;
-  }
-  SPX_LAUNCH_CHECK("k_build_lut");
-  g_colour_lut[space][dev] = lut;
-  *out = lut;
-  return SPX_OK;
-}
-
-int launch_convert_lut(const uint8_t* rgb, float* out, int64_t npx, int space, int64_t hw,
-                       int64_t s, cudaStream_t st) {
-  if (npx <= 0) return SPX_OK;
-  if (space < 0 || space > 2) {
-    set_error("unknown colour space %d", space);
-    return SPX_ERR_VALUE;
-  }
-  if (hw % 4 != 0 || (uintptr_t)rgb % 4 != 0 || (uintptr_t)out % 16 != 0) {
-    set_error("table convert needs h*w %% 4 == 0 and aligned buffers");
-    return SPX_ERR_VALUE;
-  }
-  const float4* lut = nullptr;
-  int rc = colour_lut(space, st, &lut);
-  if (rc) return rc;
-  const int64_t groups = npx >> 2;
-  int64_t blocks = std::min<int64_t>(ceil_div(groups, 256), (int64_t)num_sms() * 16);
-  k_convert_lut<<<(unsigned)blocks, 256, 0, st>>>(rgb, lut, out, groups, hw, certified_tau(s));
-  SPX_LAUNCH_CHECK("k_convert_lut");
-  return SPX_OK;
-}
-
 int launch_convert(const uint8_t* rgb, float* out, int64_t p0, int64_t p1, int space,
                    cudaStream_t st, int64_t planar_hw, int64_t s) {
   const float tau = planar_hw > 0 ? certified_tau(s) : 0.f;
@@ -341,16 +238,6 @@ int launch_convert(const uint8_t* rgb, float* out, int64_t p0, int64_t p1, int s
 }
 
 }  // namespace spx
-
-// Test hook: the engine's table convert (planar output with the certified-sum
-// flag in channel 0's sign bit) of `npx` pixels (npx % 4 == 0), synchronous.
-extern "C" int32_t spx_debug_convert_engine(const uint8_t* rgb, float* out, int64_t npx,
-                                            int32_t space, int64_t s) {
-  int rc = spx::launch_convert_lut(rgb, out, npx, space, npx, s, 0);
-  if (rc) return rc;
-  SPX_CUDA(cudaDeviceSynchronize());
-  return SPX_OK;
-}
 
 extern "C" int32_t spx_convert_band(const uint8_t* rgb, float* out, int64_t h, int64_t w,
                                     int32_t space, int64_t y0, int64_t y1, void* stream) {

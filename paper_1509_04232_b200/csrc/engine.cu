@@ -13,7 +13,6 @@
 
 namespace spx {
 int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
-int launch_convert_lut(const uint8_t*, float*, int64_t, int, int64_t, int64_t, cudaStream_t);
 int launch_init(const float*, int64_t, int64_t, int64_t, int64_t, double*, double*, int64_t,
                 int64_t, int64_t, int, int, int, cudaStream_t, int);
 int launch_assoc(const float*, const double*, const double*, int32_t*, const int32_t*, int64_t,
@@ -182,8 +181,7 @@ struct Engine {
     launches = 0;
     const int32_t* dn = early ? done : nullptr;
     cudaEventRecord(ev[EV_START], s);
-    if ((rc = use_cell ? launch_convert_lut(rgb, lab, (int64_t)B * hw, st.color_space, hw, st.s, s)
-                       : launch_convert(rgb, lab, 0, (int64_t)B * hw, st.color_space, s, 0, st.s)))
+    if ((rc = launch_convert(rgb, lab, 0, (int64_t)B * hw, st.color_space, s, use_cell ? hw : 0, st.s)))
       return rc;
     ++launches;
     cudaEventRecord(ev[EV_CONVERT], s);
