@@ -164,6 +164,41 @@ SPX_API int32_t spx_engine_segment_host(spx_engine *eng, const uint8_t *rgb_host
 /* Stage timings of the last spx_engine_segment* call (synchronises). */
 SPX_API int32_t spx_engine_timing(spx_engine *eng, spx_timing *out);
 
+/* ---- row strips: one large image across ranks --------
+ * A strip owns grid cell rows [row_lo, row_hi) of the global settings `st`.
+ * Its input is the RGB window rows [y0, y0 + hl) reported by
+ * spx_strip_geometry (own rows plus one halo cell row on each side that
+ * exists).  Per iteration the host moves three kinds of buffers between
+ * vertical neighbours (NCCL send/recv between ranks, or device copies):
+ *   centres  ns_c * 5 doubles   (pack after begin/update, unpack before associate)
+ *   sums     ns_c * 48 bytes    (pack after associate-with-update, unpack before update)
+ *   labels   S * W int32        (pack after associate, unpack before update/finish)
+ * Sequence: begin, xchg centres, { associate(1), xchg sums+labels, update,
+ * xchg centres } x no_iters, associate(0), xchg labels, finish.
+ * Results equal the single-GPU engine bit for bit.  Weak or no connectivity,
+ * no early stop, fused-cell geometry only. */
+typedef struct spx_strip spx_strip;
+SPX_API int32_t spx_strip_create(const spx_settings *st, int64_t row_lo, int64_t row_hi,
+                                 int32_t device, spx_strip **out);
+SPX_API int32_t spx_strip_destroy(spx_strip *s);
+/* out6 = {y0, hl, own_y0, own_y1, row_lo, row_hi} (global pixel / cell rows). */
+SPX_API int32_t spx_strip_geometry(spx_strip *s, int64_t *out6);
+SPX_API int32_t spx_strip_begin(spx_strip *s, const uint8_t *rgb_window, void *stream);
+SPX_API int32_t spx_strip_associate(spx_strip *s, int32_t with_update, void *stream);
+SPX_API int32_t spx_strip_update(spx_strip *s, void *stream);
+SPX_API int32_t spx_strip_pack_centres(spx_strip *s, double *up, double *down, void *stream);
+SPX_API int32_t spx_strip_unpack_centres(spx_strip *s, const double *from_up,
+                                         const double *from_down, void *stream);
+SPX_API int32_t spx_strip_pack_sums(spx_strip *s, void *up, void *down, void *stream);
+SPX_API int32_t spx_strip_unpack_sums(spx_strip *s, const void *from_up, const void *from_down,
+                                      void *stream);
+SPX_API int32_t spx_strip_pack_labels(spx_strip *s, int32_t *up, int32_t *down, void *stream);
+SPX_API int32_t spx_strip_unpack_labels(spx_strip *s, const int32_t *from_up,
+                                        const int32_t *from_down, void *stream);
+/* Own rows' labels (global ids) and own clusters' centres / counts. */
+SPX_API int32_t spx_strip_finish(spx_strip *s, int32_t *labels, double *cxy, double *clab,
+                                 int64_t *counts, void *stream);
+
 /* Number of kernel launches the last segment call enqueued. */
 SPX_API int64_t spx_engine_last_launches(spx_engine *eng);
 

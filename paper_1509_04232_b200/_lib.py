@@ -64,6 +64,19 @@ SIGNATURES = {
     "spx_engine_segment_host": (I32, [P, P, I64, P, P, P, P, P]),
     "spx_engine_timing": (I32, [P, ctypes.POINTER(SpxTiming)]),
     "spx_engine_last_launches": (I64, [P]),
+    "spx_strip_create": (I32, [ctypes.POINTER(SpxSettings), I64, I64, I32, ctypes.POINTER(P)]),
+    "spx_strip_destroy": (I32, [P]),
+    "spx_strip_geometry": (I32, [P, P]),
+    "spx_strip_begin": (I32, [P, P, P]),
+    "spx_strip_associate": (I32, [P, I32, P]),
+    "spx_strip_update": (I32, [P, P]),
+    "spx_strip_pack_centres": (I32, [P, P, P, P]),
+    "spx_strip_unpack_centres": (I32, [P, P, P, P]),
+    "spx_strip_pack_sums": (I32, [P, P, P, P]),
+    "spx_strip_unpack_sums": (I32, [P, P, P, P]),
+    "spx_strip_pack_labels": (I32, [P, P, P, P]),
+    "spx_strip_unpack_labels": (I32, [P, P, P, P]),
+    "spx_strip_finish": (I32, [P, P, P, P, P, P]),
 }
 
 _lib = None

@@ -72,6 +72,8 @@ struct CellParams {
   ClusterAcc* acc;         // [F][K]     (ACC only) atomically accumulated sums
   const int32_t* done;     // per frame, skip == 1 (may be null)
   int h, w, s, ns_r, ns_c, frames;
+  int cr0, cr1;            // cell rows processed (local grid)
+  int row_off;             // global cell row of local row 0 (strips; 0 otherwise)
   int lanes_per_cell;      // 32 or 16
   int runs_per_row;        // S / 4
   int runs;                // S * S / 4
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   const int K = p.ns_r * p.ns_c;
   // grid: x = cell groups of one frame, y = frame (no 64-bit divisions)
   const int f = blockIdx.y;
-  const int cell = (blockIdx.x * kWarps + warp) * cpw + ci;
+  const int cell = p.cr0 * p.ns_c + (blockIdx.x * kWarps + warp) * cpw + ci;
   unsigned char* wbase = smem + (size_t)warp * (ACC ? kWarpSmemAcc : kWarpSmemNoAcc);
   CandPairs* cand = reinterpret_cast<CandPairs*>(wbase) + ci * 9;
   int* cand_k = reinterpret_cast<int*>(wbase + sizeof(CandPairs) * 18) + ci * 9;
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   unsigned long long* acci =
       reinterpret_cast<unsigned long long*>(wbase + kCandBytes + 9 * 3 * 32 * sizeof(double));
 
-  bool active = cell < K && !(p.done && p.done[f] == 1);
+  bool active = cell < p.cr1 * p.ns_c && !(p.done && p.done[f] == 1);
   int cr = 0, cc = 0;
   if (active) {
     cr = cell / p.ns_c;
@@ -198,7 +200,8 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
   // Cell constant of 2A: k_mc*Mc + k_xy*(3*Mxy + 2S) + k_const
   float two_a_cell = __fmaf_rn(mc, p.k_mc, __fmaf_rn(__fmaf_rn(3.f, mxy, 2.f * S), p.k_xy, p.k_const));
   if (okf == 0.f) two_a_cell = INFINITY;
-  const int x_cell = cc * S, y_cell = cr * S;
+  const int x_cell = cc * S, y_cell = cr * S;          // local pixel origin
+  const int y_glob0 = (cr + p.row_off) * S;           // global y of the cell's row 0
   const long long img_base = (long long)f * p.h * p.w;
 
   if (active) {
@@ -295,11 +298,11 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
         int k = cand_k[t];
         if (!(gap > thr) || !(mp < 1e15f)) {
           k = exact_argmin(p.cxy + (long long)f * K * 2, p.clab + (long long)f * K * 3, L[i], A[i],
-                           B[i], x + i, y, cr, cc, p.ns_r, p.ns_c, p.xy_weight);
+                           B[i], x + i, y_glob0 + row, cr, cc, p.ns_r, p.ns_c, p.xy_weight);
           const int idx = (k / p.ns_c - cr + 1) * 3 + (k % p.ns_c - cc + 1);
           t = idx < 4 ? idx + 1 : (idx == 4 ? 0 : idx);  // (dr,dc) -> scan slot
         }
-        lab4[i] = k;
+        lab4[i] = k + p.row_off * p.ns_c;  // labels carry GLOBAL cluster ids
         if (ACC) {
           const unsigned fl = (fl4 >> i) & 1u;
           double* d = accd + t * 96 + lane;
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
           ClusterAcc* o = fa + cand_k[col - 27];
           const unsigned long long flg = (tot >> 11) & 2047ull;
           atomicAdd(&o->sx, ((tot >> 22) & 0x1FFFFFull) + cnt * (unsigned long long)x_cell);
-          atomicAdd(&o->sy, (tot >> 43) + cnt * (unsigned long long)y_cell);
+          atomicAdd(&o->sy, (tot >> 43) + cnt * (unsigned long long)y_glob0);
           atomicAdd(&o->cf, cnt | (flg << 32));
         }
       }
@@ -360,11 +363,15 @@ namespace {
 
 // fp32 filter records of the current centres (after init / perturb).
 __global__ void k_records(const double* __restrict__ cxy, const double* __restrict__ clab,
-                          CRec* __restrict__ rec, int ns_c, int s, int k_per_frame, long long n) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int k = (int)(i % k_per_frame);
-  int kr = k / ns_c, kc = k % ns_c;
+                          CRec* __restrict__ rec, int ns_c, int s, int k_per_frame, long long n,
+                          int k0, int k1, int row_off) {
+  long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int nk = k1 - k0;
+  const long long f = j / nk;
+  int k = k0 + (int)(j % nk);
+  const long long i = f * k_per_frame + k;
+  int kr = k / ns_c + row_off, kc = k % ns_c;
   double x = cxy[2 * i], y = cxy[2 * i + 1];
   double l = clab[3 * i], a = clab[3 * i + 1], b = clab[3 * i + 2];
   CRec r;
@@ -394,6 +401,8 @@ struct ReduceParams {
   int32_t* worklist;       // flagged clusters (global index f*K + k)
   int32_t* worklist_n;
   int h, w, s, ns_r, ns_c, frames, n_bl, tile_len;
+  int kr0, kr1;            // cluster rows reduced (local grid)
+  int row_off;             // global cell row of local row 0
 };
 
 __device__ __forceinline__ void write_centre(const ReduceParams& p, long long gk, int kr, int kc,
@@ -424,7 +433,7 @@ __device__ __forceinline__ void write_centre(const ReduceParams& p, long long gk
   r.a = __double2float_rn(a);
   r.b = __double2float_rn(b);
   r.xr = __double2float_rn(dsub(x, (double)kc * p.s));
-  r.yr = __double2float_rn(dsub(y, (double)kr * p.s));
+  r.yr = __double2float_rn(dsub(y, (double)(kr + p.row_off) * p.s));
   r.mag_lab = fmaxf(fabsf(r.l), fmaxf(fabsf(r.a), fabsf(r.b)));
   r.mag_xy = fmaxf(fabsf(r.xr), fabsf(r.yr));
   r.ok = (fin_small(x) && fin_small(y) && fin_small(l) && fin_small(a) && fin_small(b)) ? 1.f : 0.f;
@@ -436,13 +445,16 @@ __device__ __forceinline__ void write_centre(const ReduceParams& p, long long gk
 // warp with the reference strip folds + pairwise strip tree (_core.pyx:300-311).
 __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
   const int K = p.ns_r * p.ns_c;
-  const long long gk = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool in = gk < (long long)K * p.frames;
+  const int nk = (p.kr1 - p.kr0) * p.ns_c;
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = j < (long long)nk * p.frames;
   int f = 0, k = 0, kr = 0, kc = 0;
+  long long gk = 0;
   bool todo = false, flagged = false;
   if (in) {
-    f = (int)(gk / K);
-    k = (int)(gk % K);
+    f = (int)(j / nk);
+    k = p.kr0 * p.ns_c + (int)(j % nk);
+    gk = (long long)f * K + k;
     kr = k / p.ns_c;
     kc = k % p.ns_c;
     todo = !(p.done && p.done[f]);
@@ -454,7 +466,7 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
     // consume and clear for the next pass
     *reinterpret_cast<double4*>(a) = make_double4(0.0, 0.0, 0.0, 0.0);
     *reinterpret_cast<ulonglong2*>(&a->sy) = make_ulonglong2(0ull, 0ull);
-    const unsigned long long sx = __double_as_longlong(s012.w);
+    const unsigned long long sx = (unsigned long long)__double_as_longlong(s012.w);
     const unsigned long long cnt = syc.y & 0xFFFFFFFFull, fl = syc.y >> 32;
     flagged = fl != 0;
     if (!flagged)
@@ -537,7 +549,7 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
         for (int cb = 0; cb < 3; ++cb) {
           if (cb >= ncb) break;
           const int col = cb * 32 + lane;
-          const bool m = lv[rr][cb] == fk;
+          const bool m = lv[rr][cb] == fk + p.row_off * p.ns_c;  // global ids
           const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
           if (m) {
             // asynchronous global -> shared copies: all of the block's value
@@ -565,7 +577,7 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
           }
           if (j != cur_j) cur_j = j;  // lanes 1, 2 track cur_j below
           sx += rx;
-          sy += (long long)y * rn;
+          sy += (long long)(y + p.row_off * p.s) * rn;
           cnt += rn;
         }
       }
@@ -654,7 +666,7 @@ void assoc_bound_coefficients(double xy_weight, float& w32, float& k_mp, float& 
 int launch_cell(const float* img, const double* cxy, const double* clab, const CRec* rec,
                 int32_t* labels, ClusterAcc* sums, const int32_t* done, int64_t h, int64_t w,
                 int64_t s, int64_t ns_r, int64_t ns_c, double xy_weight, int frames, bool acc,
-                cudaStream_t st) {
+                cudaStream_t st, int64_t cr0, int64_t cr1, int64_t row_off) {
   CellParams p;
   p.img = img;
   p.cxy = cxy;
@@ -669,6 +681,10 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.ns_r = (int)ns_r;
   p.ns_c = (int)ns_c;
   p.frames = frames;
+  if (cr1 < 0) cr1 = ns_r;
+  p.cr0 = (int)cr0;
+  p.cr1 = (int)cr1;
+  p.row_off = (int)row_off;
   p.runs = (int)(s * s / 4);
   p.runs_per_row = (int)(s / 4);
   p.row_magic = (unsigned)((65536 + p.runs_per_row - 1) / p.runs_per_row);
@@ -676,7 +692,8 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.xy_weight = xy_weight;
   assoc_bound_coefficients(xy_weight, p.w32, p.k_mp, p.k_mc, p.k_xy, p.k_const, p.k_rel);
   const int cpw = 32 / p.lanes_per_cell;
-  const long long warps = ceil_div(ns_r * ns_c, cpw);
+  if (cr1 <= cr0) return SPX_OK;
+  const long long warps = ceil_div((cr1 - cr0) * ns_c, cpw);
   const dim3 blocks((unsigned)ceil_div(warps, kWarps), (unsigned)frames);
   if (frames > 65535) {
     set_error("k_cell: at most 65535 frames per launch");
@@ -699,10 +716,14 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
 }
 
 int launch_records(const double* cxy, const double* clab, CRec* rec, int64_t ns_r, int64_t ns_c,
-                   int64_t s, int frames, cudaStream_t st) {
-  long long n = ns_r * ns_c * (long long)frames;
+                   int64_t s, int frames, cudaStream_t st, int64_t k0, int64_t k1,
+                   int64_t row_off) {
+  if (k1 < 0) k1 = ns_r * ns_c;
+  if (k1 <= k0) return SPX_OK;
+  long long n = (k1 - k0) * (long long)frames;
   k_records<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(cxy, clab, rec, (int)ns_c, (int)s,
-                                                        (int)(ns_r * ns_c), n);
+                                                        (int)(ns_r * ns_c), n, (int)k0, (int)k1,
+                                                        (int)row_off);
   SPX_LAUNCH_CHECK("k_records");
   return SPX_OK;
 }
@@ -712,7 +733,7 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
                         double* out_lab, int64_t* counts, CRec* rec, const int32_t* done,
                         int32_t* worklist, int32_t* worklist_n, int64_t h, int64_t w, int64_t s,
                         int64_t ns_r, int64_t ns_c, int64_t tile_len, int frames,
-                        cudaStream_t st) {
+                        cudaStream_t st, int64_t kr0, int64_t kr1, int64_t row_off) {
   ReduceParams p;
   p.acc = acc;
   p.img = img;
@@ -734,8 +755,13 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   p.frames = frames;
   p.n_bl = (int)ceil_div(3 * s, tile_len);
   p.tile_len = (int)tile_len;
-  long long n = ns_r * ns_c * (long long)frames;
+  if (kr1 < 0) kr1 = ns_r;
+  p.kr0 = (int)kr0;
+  p.kr1 = (int)kr1;
+  p.row_off = (int)row_off;
+  long long n = (kr1 - kr0) * ns_c * (long long)frames;
   SPX_CUDA(cudaMemsetAsync(worklist_n, 0, sizeof(int32_t), st));
+  if (n <= 0) return SPX_OK;
   k_reduce_cells<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_reduce_cells");
   k_exact_clusters<<<(unsigned)num_sms() * 16, kExWarps * 32, 0, st>>>(p);

@@ -47,20 +47,24 @@ __device__ __forceinline__ void perturb_one(const LabView& im, int64_t h, int64_
 
 // _core.pyx:86-107 (+ optional perturb).  Clusters [k0,k1) of each of
 // `frames` frames; `planar` selects the engine's [3][H][W] Lab layout.
+// Row strips: the buffer holds local rows (hl of them, starting at global
+// cell row row_off); h is the GLOBAL image height and all coordinates are
+// global.  Whole frames: hl == h, row_off == 0.
 __global__ void k_init(const float* __restrict__ img, int64_t h, int64_t w, int64_t s,
                        int64_t ns_c, double* __restrict__ cxy, double* __restrict__ clab,
                        int64_t k0, int64_t k1, int64_t k_stride, int frames, int perturb,
-                       int do_init, int planar) {
+                       int do_init, int planar, int64_t hl, int64_t row_off) {
   int64_t nk = k1 - k0;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nk * frames) return;
   int64_t f = i / nk;
   int64_t k = k0 + i % nk;
-  const LabView im{img + f * h * w * 3, w, h * w, planar != 0};
+  LabView im{img + f * hl * w * 3, w, hl * w, planar != 0};
+  im.yoff = row_off * s;
   double* xy = cxy + (f * k_stride + k) * 2;
   double* lab = clab + (f * k_stride + k) * 3;
   if (do_init) {
-    int64_t r = k / ns_c, c = k % ns_c;
+    int64_t r = k / ns_c + row_off, c = k % ns_c;
     int64_t ix = c * s + s / 2;
     if (ix > w - 1) ix = w - 1;
     int64_t iy = r * s + s / 2;
@@ -76,11 +80,13 @@ __global__ void k_init(const float* __restrict__ img, int64_t h, int64_t w, int6
 
 int launch_init(const float* img, int64_t h, int64_t w, int64_t s, int64_t ns_c, double* cxy,
                 double* clab, int64_t k0, int64_t k1, int64_t k_stride, int frames, int perturb,
-                int do_init, cudaStream_t st, int planar) {
+                int do_init, cudaStream_t st, int planar, int64_t hl, int64_t row_off) {
   int64_t n = (k1 - k0) * frames;
   if (n <= 0) return SPX_OK;
+  if (hl < 0) hl = h;
   k_init<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(img, h, w, s, ns_c, cxy, clab, k0, k1,
-                                                     k_stride, frames, perturb, do_init, planar);
+                                                     k_stride, frames, perturb, do_init, planar,
+                                                     hl, row_off);
   SPX_LAUNCH_CHECK("k_init");
   return SPX_OK;
 }
@@ -236,7 +242,7 @@ extern "C" int32_t spx_init_centers_range(const float* img, int64_t h, int64_t w
     set_error("init_centers_range: bad grid (s=%lld ns_c=%lld)", (long long)s, (long long)ns_c);
     return SPX_ERR_VALUE;
   }
-  return launch_init(img, h, w, s, ns_c, cxy, clab, k0, k1, 0, 1, 0, 1, as_stream(stream), 0);
+  return launch_init(img, h, w, s, ns_c, cxy, clab, k0, k1, 0, 1, 0, 1, as_stream(stream), 0, -1, 0);
 }
 
 extern "C" int32_t spx_perturb_range(const float* img, int64_t h, int64_t w, double* cxy,
@@ -245,7 +251,7 @@ extern "C" int32_t spx_perturb_range(const float* img, int64_t h, int64_t w, dou
     set_error("perturb_range: negative cluster index");
     return SPX_ERR_VALUE;
   }
-  return launch_init(img, h, w, 1, 1, cxy, clab, k0, k1, 0, 1, 1, 0, as_stream(stream), 0);
+  return launch_init(img, h, w, 1, 1, cxy, clab, k0, k1, 0, 1, 1, 0, as_stream(stream), 0, -1, 0);
 }
 
 extern "C" int32_t spx_reduce_range(double* slab, int64_t n_bl, const double* prev_xy,

@@ -82,8 +82,12 @@ __device__ __forceinline__ int32_t weak_rule_g(const int32_t* t, int pitch, int 
   return hl ? left : (hu ? up : v);
 }
 
+// Output rows [y0, y1) of a buffer of h rows (row strips pass their halo
+// rows in the buffer and only their own rows as the output range; image
+// edges coincide with buffer edges, interior strip edges have >= 2 halo rows).
 __global__ void __launch_bounds__(256) k_weak2(const int32_t* __restrict__ src,
-                                               int32_t* __restrict__ dst, int h, int w) {
+                                               int32_t* __restrict__ dst, int h, int w, int y0,
+                                               int y1) {
   constexpr int P0 = WT2W + 8, R0 = WT2H + 4;  // source tile: 4-col / 2-row halo
   constexpr int P1 = WT2W + 2, R1 = WT2H + 2;  // pass-1 tile: 1-px halo
   __shared__ __align__(16) int32_t t0[R0 * P0];
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(256) k_weak2(const int32_t* __restrict__ src,
   const long long fo = (long long)blockIdx.z * h * w;
   const int32_t* s = src + fo;
   int32_t* d = dst + fo;
-  const int tx0 = blockIdx.x * WT2W, ty0 = blockIdx.y * WT2H;
+  const int tx0 = blockIdx.x * WT2W, ty0 = y0 + blockIdx.y * WT2H;
   const int tid = threadIdx.x;
   const bool vec = (w & 3) == 0;
   // load: tile columns [tx0-4, tx0+WT2W+4), rows [ty0-2, ty0+WT2H+2)
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__(256) k_weak2(const int32_t* __restrict__ src,
   for (int i = tid; i < WT2H * (WT2W / 4); i += 256) {
     const int ly = i / (WT2W / 4), lq = i % (WT2W / 4);
     const int y = ty0 + ly, x = tx0 + lq * 4;
-    if (y >= h) continue;
+    if (y >= y1) continue;
     int o[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -252,14 +256,15 @@ int launch_weak1(const int32_t* src, int32_t* dst, int64_t h, int64_t w, int64_t
 }
 
 int launch_weak2(const int32_t* src, int32_t* dst, int64_t h, int64_t w, int frames,
-                 cudaStream_t st) {
-  if (h <= 0 || w <= 0 || frames <= 0) return SPX_OK;
+                 cudaStream_t st, int64_t y0, int64_t y1) {
+  if (y1 < 0) y1 = h;
+  if (y1 <= y0 || w <= 0 || frames <= 0) return SPX_OK;
   if (h * w >= (int64_t)1 << 31 || frames > 65535) {
     set_error("weak: frame too large for the fused kernel");
     return SPX_ERR_VALUE;
   }
-  dim3 grid((unsigned)ceil_div(w, WT2W), (unsigned)ceil_div(h, WT2H), (unsigned)frames);
-  k_weak2<<<grid, 256, 0, st>>>(src, dst, (int)h, (int)w);
+  dim3 grid((unsigned)ceil_div(w, WT2W), (unsigned)ceil_div(y1 - y0, WT2H), (unsigned)frames);
+  k_weak2<<<grid, 256, 0, st>>>(src, dst, (int)h, (int)w, (int)y0, (int)y1);
   SPX_LAUNCH_CHECK("k_weak2");
   return SPX_OK;
 }

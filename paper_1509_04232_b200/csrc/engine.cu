@@ -14,7 +14,7 @@
 namespace spx {
 int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
 int launch_init(const float*, int64_t, int64_t, int64_t, int64_t, double*, double*, int64_t,
-                int64_t, int64_t, int, int, int, cudaStream_t, int);
+                int64_t, int64_t, int, int, int, cudaStream_t, int, int64_t, int64_t);
 int launch_assoc(const float*, const double*, const double*, int32_t*, const int32_t*, int64_t,
                  int64_t, int64_t, int64_t, int64_t, double, int64_t, int64_t, int, int64_t,
                  cudaStream_t);
@@ -26,18 +26,19 @@ int launch_reduce(double*, int64_t, const double*, const double*, double*, doubl
 int launch_shift(const double*, const double*, int64_t, int, double*, int32_t*, int32_t*, double,
                  cudaStream_t);
 int launch_commit_done(int32_t*, int, cudaStream_t);
-int launch_weak2(const int32_t*, int32_t*, int64_t, int64_t, int, cudaStream_t);
+int launch_weak2(const int32_t*, int32_t*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
 int launch_strict(const int32_t*, int32_t*, int64_t, int64_t, int, int64_t, int64_t, int32_t*,
                   int32_t*, int32_t*, int32_t*, cudaStream_t);
 bool cell_path_ok(int64_t, int64_t, int64_t, int64_t);
 int launch_cell(const float*, const double*, const double*, const CRec*, int32_t*, ClusterAcc*,
                 const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, double, int, bool,
-                cudaStream_t);
+                cudaStream_t, int64_t, int64_t, int64_t);
 int launch_records(const double*, const double*, CRec*, int64_t, int64_t, int64_t, int,
-                   cudaStream_t);
+                   cudaStream_t, int64_t, int64_t, int64_t);
 int launch_reduce_cells(ClusterAcc*, const float*, const int32_t*, const double*, const double*,
                         double*, double*, int64_t*, CRec*, const int32_t*, int32_t*, int32_t*,
-                        int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t);
+                        int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t,
+                        int64_t, int64_t, int64_t);
 int launch_fill_i32(int32_t*, int, int, cudaStream_t);
 
 namespace {
@@ -158,7 +159,7 @@ struct Engine {
     cudaEventRecord(pass_event(ev_assoc, 2 * n_assoc), s);
     int rc = use_cell ? launch_cell(lab, cxy[cur], clab[cur], rec, labels, acc, dn, st.height,
                                     st.width, st.s, st.ns_r, st.ns_c, xy_weight, frames,
-                                    with_update, s)
+                                    with_update, s, 0, -1, 0)
                       : launch_assoc(lab, cxy[cur], clab[cur], labels, dn, st.height, st.width,
                                      st.s, st.ns_r, st.ns_c, xy_weight, 0, st.height, frames, K, s);
     cudaEventRecord(pass_event(ev_assoc, 2 * n_assoc + 1), s);
@@ -186,18 +187,19 @@ struct Engine {
     ++launches;
     cudaEventRecord(ev[EV_CONVERT], s);
     if ((rc = launch_init(lab, st.height, st.width, st.s, st.ns_c, cxy[0], clab[0], 0, K, K, B, 0,
-                          1, s, use_cell)))
+                          1, s, use_cell, -1, 0)))
       return rc;
     ++launches;
     cudaEventRecord(ev[EV_INIT], s);
     if (st.perturb) {
       if ((rc = launch_init(lab, st.height, st.width, st.s, st.ns_c, cxy[0], clab[0], 0, K, K, B,
-                            1, 0, s, use_cell)))
+                            1, 0, s, use_cell, -1, 0)))
         return rc;
       ++launches;
     }
     if (use_cell) {
-      if ((rc = launch_records(cxy[0], clab[0], rec, st.ns_r, st.ns_c, st.s, B, s))) return rc;
+      if ((rc = launch_records(cxy[0], clab[0], rec, st.ns_r, st.ns_c, st.s, B, s, 0, -1, 0)))
+        return rc;
       ++launches;
       SPX_CUDA(cudaMemsetAsync(acc, 0, (size_t)B * K * sizeof(ClusterAcc), s));
     }
@@ -214,7 +216,7 @@ struct Engine {
         if ((rc = launch_reduce_cells(acc, lab, labels, cxy[cur], clab[cur], cxy[nxt], clab[nxt],
                                       out_counts, rec, dn, worklist, worklist + max_batch * K,
                                       st.height, st.width, st.s, st.ns_r, st.ns_c, st.tile_len, B,
-                                      s)))
+                                      s, 0, -1, 0)))
           return rc;
         launches += 2;
       } else {
@@ -244,7 +246,7 @@ struct Engine {
     }
     cudaEventRecord(ev[EV_CONN0], s);
     if (st.connectivity == 1) {
-      if ((rc = launch_weak2(labels, out_labels, st.height, st.width, B, s))) return rc;
+      if ((rc = launch_weak2(labels, out_labels, st.height, st.width, B, s, 0, -1))) return rc;
       ++launches;
     } else if (st.connectivity == 2) {
       if ((rc = launch_strict(labels, out_labels, st.height, st.width, B, K, st.min_size,

@@ -69,3 +69,38 @@ def test_strip_plan_exact_cover(h, s, world):
     for st in plan:
         assert st.halo_lo == max(st.cell_row_lo - 1, 0)
         assert st.halo_hi == min(st.cell_row_hi + 1, ns_r)
+
+
+def _strip_worker(rank, world, port, q):
+    """DistComm moves [[send_up, recv_up], [send_down, recv_down]] between
+    vertical neighbours (gloo, CPU tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1509_04232_b200.strips import DistComm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bufs = [[torch.full((5,), 100.0 * rank + 1), torch.zeros(5)],
+            [torch.full((5,), 100.0 * rank + 2), torch.zeros(5)]]
+    DistComm(rank, world).exchange_buffers(bufs)
+    q.put((rank, float(bufs[0][1][0]), float(bufs[1][1][0])))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_strip_neighbour_exchange(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_strip_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    for rank, from_up, from_down in res:
+        # from_up = the upper rank's "send down" (100*(r-1)+2); from_down = lower's "send up"
+        assert from_up == (100.0 * (rank - 1) + 2 if rank > 0 else 0.0)
+        assert from_down == (100.0 * (rank + 1) + 1 if rank < world - 1 else 0.0)

@@ -217,3 +217,24 @@ def test_cell_path_batch_gray_heavy_frames():
         assert r.spixel_map.centers_lab.tobytes() == clab.tobytes()
         assert r.spixel_map.centers_xy.tobytes() == cxy.tobytes()
         assert np.array_equal(r.spixel_map.num_pixels, counts)
+
+
+@pytest.mark.parametrize("h,w,kw,n", [
+    (480, 640, dict(num_superpixels=1200), 3),
+    (200, 160, dict(spixel_size=16), 2),
+    (200, 160, dict(spixel_size=16), 5),
+    (250, 96, dict(spixel_size=8, tile_len=5, enable_perturbation=True), 4),
+    (130, 64, dict(spixel_size=12, do_enforce_connectivity=False, no_iters=3), 3),
+])
+def test_row_strips_equal_whole_image(h, w, kw, n):
+    """C5 decomposition: strips with halo centres / partial-sum / label exchange
+    give exactly the single-GPU (and reference) result."""
+    from paper_1509_04232_b200.strips import segment_strips_local
+    st = spx.Settings(img_width=w, img_height=h, **kw)
+    for name, rgb in _images(h, w, 7 * n + h).items():
+        labels, cxy, clab, counts = segment_strips_local(st, rgb, n)
+        wl, wx, wlab, wc, _ = _oracle_pipeline(rgb, st)
+        assert np.array_equal(labels, wl), name
+        assert cxy.tobytes() == wx.tobytes(), name
+        assert clab.tobytes() == wlab.tobytes(), name
+        assert np.array_equal(counts, wc), name
