@@ -161,6 +161,19 @@ SPX_API int32_t spx_engine_segment_host(spx_engine *eng, const uint8_t *rgb_host
                                 int32_t *labels_host, double *cxy_host, double *clab_host,
                                 int64_t *counts_host, int32_t *passes_host);
 
+/* Asynchronous form of spx_engine_segment_host for streams of batches: enqueues
+ * the batch's H2D / compute / D2H chunks and returns.  Consecutive submits
+ * continue one pipeline, so the copies of batch i overlap the compute of
+ * batch i+1.  Host buffers must stay valid (and the outputs unread) until
+ * spx_engine_wait returns.  Input buffers should be pinned. */
+SPX_API int32_t spx_engine_submit_host(spx_engine *eng, const uint8_t *rgb_host, int64_t batch,
+                               int32_t *labels_host, double *cxy_host, double *clab_host,
+                               int64_t *counts_host, int32_t *passes_host);
+SPX_API int32_t spx_engine_wait(spx_engine *eng);
+/* Frames per host-pipeline chunk (default 64, capped at max_batch); waits for
+ * submitted work and re-allocates the staging buffers. */
+SPX_API int32_t spx_engine_set_host_chunk(spx_engine *eng, int64_t frames);
+
 /* Stage timings of the last spx_engine_segment* call (synchronises). */
 SPX_API int32_t spx_engine_timing(spx_engine *eng, spx_timing *out);
 

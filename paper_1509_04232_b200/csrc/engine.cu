@@ -299,7 +299,7 @@ struct Engine {
   // (copy engines run both directions concurrently with the SMs).  Host
   // buffers must be pinned for the copies to be asynchronous; pageable
   // buffers still give correct results, serialised.
-  int64_t chunk = 0;
+  int64_t chunk = 0, chunk_req = 64;
   uint8_t* h_rgb[2] = {nullptr, nullptr};
   int32_t* h_lab[2] = {nullptr, nullptr};
   double* h_xy[2] = {nullptr, nullptr};
@@ -311,7 +311,7 @@ struct Engine {
 
   int ensure_staging() {
     if (s_comp) return SPX_OK;
-    chunk = std::max<int64_t>(1, std::min<int64_t>(max_batch, 64));
+    chunk = std::max<int64_t>(1, std::min<int64_t>(max_batch, chunk_req));
     for (int i = 0; i < 2; ++i) {
       SPX_CUDA(cudaMalloc(&h_rgb[i], chunk * hw * 3));
       SPX_CUDA(cudaMalloc(&h_lab[i], chunk * hw * sizeof(int32_t)));
@@ -336,13 +336,40 @@ struct Engine {
         if (q) cudaFree(q);
       for (cudaEvent_t e : {ev_h2d[i], ev_comp[i], ev_d2h[i]})
         if (e) cudaEventDestroy(e);
+      h_rgb[i] = nullptr, h_lab[i] = nullptr, h_xy[i] = nullptr, h_cl[i] = nullptr;
+      h_cnt[i] = nullptr, h_pass[i] = nullptr;
+      ev_h2d[i] = ev_comp[i] = ev_d2h[i] = nullptr;
     }
     for (cudaStream_t q : {s_h2d, s_comp, s_d2h})
       if (q) cudaStreamDestroy(q);
+    s_h2d = s_comp = s_d2h = nullptr;
   }
 
-  int segment_host(const uint8_t* rgb, int64_t batch, int32_t* out_labels, double* out_xy,
-                   double* out_lab, int64_t* out_counts, int32_t* out_passes) {
+  // Frames per pipeline chunk.  Small chunks expose less fill/drain in a single
+  // call; chunk = batch is best for a stream of batches (bench: 256).
+  int set_host_chunk(int64_t n) {
+    if (n < 1) {
+      set_error("host chunk must be >= 1");
+      return SPX_ERR_VALUE;
+    }
+    int rc = wait_host();
+    if (rc) return rc;
+    free_staging();
+    chunk_req = n;
+    seq = 0;
+    return SPX_OK;
+  }
+
+  // Host-buffer pipeline: chunks of `chunk` frames alternate between two
+  // device staging slots; H2D, compute and D2H run on three streams ordered
+  // by events.  The slot sequence continues across calls, so back-to-back
+  // submit_host calls (a stream of batches) keep all three engines busy and
+  // only the very first H2D and the last D2H are exposed.
+  int64_t seq = 0;
+  std::vector<cudaEvent_t> tl;  // SPX_DEBUG_TIMELINE=1 per-chunk timeline
+
+  int submit_host(const uint8_t* rgb, int64_t batch, int32_t* out_labels, double* out_xy,
+                  double* out_lab, int64_t* out_counts, int32_t* out_passes) {
     SPX_CUDA(cudaSetDevice(device));
     int rc = ensure_staging();
     if (rc) return rc;
@@ -351,9 +378,7 @@ struct Engine {
       return SPX_ERR_VALUE;
     }
     const int64_t nchunks = ceil_div(batch, chunk);
-    // optional per-chunk timeline (diagnostics): SPX_DEBUG_TIMELINE=1
     static const bool dbg = getenv("SPX_DEBUG_TIMELINE") != nullptr;
-    std::vector<cudaEvent_t> tl;
     auto mark = [&](cudaStream_t q) {
       if (!dbg) return;
       cudaEvent_t e;
@@ -361,17 +386,17 @@ struct Engine {
       cudaEventRecord(e, q);
       tl.push_back(e);
     };
-    for (int64_t c = 0; c < nchunks; ++c) {
-      const int sl = (int)(c & 1);
+    for (int64_t c = 0; c < nchunks; ++c, ++seq) {
+      const int sl = (int)(seq & 1);
       const int64_t f0 = c * chunk, nb = std::min(chunk, batch - f0);
-      if (c >= 2) SPX_CUDA(cudaStreamWaitEvent(s_h2d, ev_comp[sl], 0));
+      if (seq >= 2) SPX_CUDA(cudaStreamWaitEvent(s_h2d, ev_comp[sl], 0));
       mark(s_h2d);
       SPX_CUDA(cudaMemcpyAsync(h_rgb[sl], rgb + f0 * hw * 3, nb * hw * 3, cudaMemcpyHostToDevice,
                                s_h2d));
       mark(s_h2d);
       SPX_CUDA(cudaEventRecord(ev_h2d[sl], s_h2d));
       SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_h2d[sl], 0));
-      if (c >= 2) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
+      if (seq >= 2) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
       mark(s_comp);
       if ((rc = segment(h_rgb[sl], nb, h_lab[sl], h_xy[sl], h_cl[sl], h_cnt[sl], h_pass[sl],
                         s_comp)))
@@ -398,10 +423,15 @@ struct Engine {
       mark(s_d2h);
       SPX_CUDA(cudaEventRecord(ev_d2h[sl], s_d2h));
     }
+    return SPX_OK;
+  }
+
+  int wait_host() {
+    SPX_CUDA(cudaSetDevice(device));
+    if (!s_d2h) return SPX_OK;
     SPX_CUDA(cudaStreamSynchronize(s_d2h));
-    if (dbg && !tl.empty()) {
-      cudaDeviceSynchronize();
-      for (size_t i = 0; i < tl.size(); i += 6) {
+    if (!tl.empty()) {
+      for (size_t i = 0; i + 5 < tl.size(); i += 6) {
         float a0, a1, b0, b1, c0, c1;
         cudaEventElapsedTime(&a0, tl[0], tl[i]);
         cudaEventElapsedTime(&a1, tl[0], tl[i + 1]);
@@ -413,8 +443,16 @@ struct Engine {
                 b0, b1, c0, c1);
       }
       for (auto e : tl) cudaEventDestroy(e);
+      tl.clear();
     }
     return SPX_OK;
+  }
+
+  int segment_host(const uint8_t* rgb, int64_t batch, int32_t* out_labels, double* out_xy,
+                   double* out_lab, int64_t* out_counts, int32_t* out_passes) {
+    int rc = submit_host(rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes);
+    int rw = wait_host();
+    return rc ? rc : rw;
   }
 };
 
@@ -475,6 +513,19 @@ int32_t spx_engine_segment_host(spx_engine* eng, const uint8_t* rgb_host, int64_
                                 int64_t* counts_host, int32_t* passes_host) {
   return eng->e.segment_host(rgb_host, batch, labels_host, cxy_host, clab_host, counts_host,
                              passes_host);
+}
+
+int32_t spx_engine_submit_host(spx_engine* eng, const uint8_t* rgb_host, int64_t batch,
+                               int32_t* labels_host, double* cxy_host, double* clab_host,
+                               int64_t* counts_host, int32_t* passes_host) {
+  return eng->e.submit_host(rgb_host, batch, labels_host, cxy_host, clab_host, counts_host,
+                            passes_host);
+}
+
+int32_t spx_engine_wait(spx_engine* eng) { return eng->e.wait_host(); }
+
+int32_t spx_engine_set_host_chunk(spx_engine* eng, int64_t frames) {
+  return eng->e.set_host_chunk(frames);
 }
 
 int32_t spx_engine_timing(spx_engine* eng, spx_timing* out) { return eng->e.timing(out); }

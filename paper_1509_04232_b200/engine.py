@@ -95,6 +95,7 @@ class SegEngine:
             device = torch.cuda.current_device() if torch.cuda.is_available() else 0
         self.device = int(device)
         self.max_batch = int(max_batch)
+        self._pending = []  # host arrays of submitted batches, kept alive until wait()
         lib = _lib.load()
         self._st = _native_settings(settings, self.grid)
         handle = ctypes.c_void_p()
@@ -190,6 +191,38 @@ class SegEngine:
         _lib.check(self._lib.spx_engine_segment_host(self._h, p(rgb), b, p(labels), p(cxy),
                                                      p(clab), p(counts), p(passes)), "segment")
         return labels, cxy, clab, counts, passes
+
+    def submit_host(self, rgb, labels, cxy, clab, counts, passes):
+        """Enqueue one batch of host frames without waiting (stream of batches).
+
+        All arrays must be caller-owned numpy arrays (pinned for overlap) that
+        stay alive and unread until `wait()`.  Consecutive submits share one
+        H2D / compute / D2H pipeline.
+        """
+        st = self.settings
+        if rgb.ndim != 4 or rgb.shape[1:] != (st.img_height, st.img_width, 3) or \
+                rgb.dtype != np.uint8 or not rgb.flags.c_contiguous:
+            raise DimensionMismatchError("submit_host needs contiguous uint8 (B, H, W, 3) frames")
+        b = rgb.shape[0]
+        k = self.grid.num_clusters
+        for a, shape, dt in ((labels, (b, st.img_height, st.img_width), np.int32),
+                             (cxy, (b, k, 2), np.float64), (clab, (b, k, 3), np.float64),
+                             (counts, (b, k), np.int64), (passes, (b,), np.int32)):
+            if a.shape != shape or a.dtype != dt or not a.flags.c_contiguous:
+                raise ValueError(f"output {a.shape}/{a.dtype} does not match {shape}/{np.dtype(dt)}")
+        self._pending.append((rgb, labels, cxy, clab, counts, passes))
+        p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        _lib.check(self._lib.spx_engine_submit_host(self._h, p(rgb), b, p(labels), p(cxy),
+                                                    p(clab), p(counts), p(passes)), "submit")
+
+    def set_host_chunk(self, frames):
+        """Frames per H2D/compute/D2H pipeline chunk of the host-buffer path."""
+        _lib.check(self._lib.spx_engine_set_host_chunk(self._h, int(frames)), "set_host_chunk")
+
+    def wait(self):
+        """Wait for every submitted batch; their outputs are then valid."""
+        _lib.check(self._lib.spx_engine_wait(self._h), "wait")
+        self._pending.clear()
 
     def last_timing(self):
         """Per-stage device times (seconds) of the last call, batch-wide."""

@@ -238,3 +238,35 @@ def test_row_strips_equal_whole_image(h, w, kw, n):
         assert cxy.tobytes() == wx.tobytes(), name
         assert clab.tobytes() == wlab.tobytes(), name
         assert np.array_equal(counts, wc), name
+
+
+def test_submit_host_pipeline_across_batches():
+    """Back-to-back submit_host calls (chunks cross batch boundaries and reuse
+    staging slots) give the same results as one synchronous call per batch."""
+    import torch
+    h, w = 48, 64
+    st = spx.Settings(img_width=w, img_height=h, spixel_size=8)
+    eng = spx.SegEngine(st, max_batch=70)
+    eng.set_host_chunk(32)
+    k = eng.grid.num_clusters
+    rng = np.random.default_rng(21)
+    batches = [rng.integers(0, 256, (n, h, w, 3), dtype=np.uint8) for n in (70, 5, 66, 1)]
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory().numpy()  # noqa: E731
+    outs = []
+    for b in batches:
+        n = b.shape[0]
+        o = (pin((n, h, w), torch.int32), pin((n, k, 2), torch.float64),
+             pin((n, k, 3), torch.float64), pin((n, k), torch.int64), pin((n,), torch.int32))
+        eng.submit_host(torch.from_numpy(b).pin_memory().numpy(), *o)
+        outs.append(o)
+    eng.wait()
+    for b, o in zip(batches, outs):
+        want = eng.segment_host(b)
+        for got, ref in zip(o, want):
+            assert got.tobytes() == ref.tobytes()
+    eng.set_host_chunk(70)
+    for b, o in zip(batches, outs):
+        for got, ref in zip(o, eng.segment_host(b)):
+            assert got.tobytes() == ref.tobytes()
+    with pytest.raises(ValueError):
+        eng.submit_host(batches[1], *outs[0])
