@@ -10,6 +10,8 @@ import os
 from .errors import DimensionMismatchError, InvalidSettingsError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspx.so")
+# Development only: A/B kernel variants built by tools/build_variants.py.
+LIB_PATH = os.environ.get("SPX_LIB_VARIANT", LIB_PATH)
 
 SPX_OK = 0
 SPX_ERR_INVALID_SETTINGS = 1

@@ -23,6 +23,7 @@
 // exact sum.  Pixels outside that range set a flag bit; the reduce kernel
 // recomputes flagged clusters with the reference's exact strip fold.
 #include <cmath>
+#include <cstdlib>
 
 #include "spx_internal.cuh"
 
@@ -74,7 +75,7 @@ struct CellParams {
   int h, w, s, ns_r, ns_c, frames;
   int cr0, cr1;            // cell rows processed (local grid)
   int row_off;             // global cell row of local row 0 (strips; 0 otherwise)
-  int lanes_per_cell;      // 32 or 16
+  int pairs_per_warp;      // consecutive cell pairs walked by one warp
   int runs_per_row;        // S / 4
   int runs;                // S * S / 4
   unsigned row_magic;      // ceil(2^16 / runs_per_row)
@@ -104,144 +105,192 @@ __device__ __noinline__ int exact_argmin(const double* __restrict__ cxy, const d
 }
 
 // Shared-memory layout per warp.
-//   cand[cpw][9]: duplicated fp32 pairs (l,l) (a,a) (b,b) (x,x) for FFMA2
-//   cy[cpw][9]:   candidate y (cell relative)
+//   cand[2][9]:   fp32 candidate l, a, b, x (cell relative); the packed
+//                 FADD2/FFMA2 ops take them as broadcast scalar operands
+//   cy[2][9]:     candidate y (cell relative)
+//   cand_k[2][9]: cluster id of each candidate slot
 //   acc (ACC):    lane-private per-slot accumulators, lane-interleaved so
 //                 any per-lane slot choice is bank-conflict free:
-//                 accd[9][3][32] double, acci[9][32] uint64 (packed
+//                 accd[9][3][kCS] double, acci[9][kCS] uint64 (packed
 //                 count | flags<<11 | sum_x<<22 | sum_y<<43).
-//   cand_k[cpw][9]: cluster id of each candidate slot
-struct alignas(16) CandPairs {
-  unsigned long long l, a, b, x, y, pad;
-};
+// The whole per-warp block stays <= 10496 B so 16 warps fit the 164 KB
+// shared-memory carve-out and leave 92 KB of L1 for the Lab stream.
 constexpr int kWarps = 4;
-constexpr size_t kCandBytes = 944;  // 18 CandPairs + 18 floats (cpw <= 2), 16-aligned
-static_assert(sizeof(CandPairs) * 18 + sizeof(float) * 18 <= kCandBytes, "cand smem");
-constexpr size_t kAccBytes = 9 * 3 * 32 * sizeof(double) + 9 * 32 * sizeof(uint64_t);
+constexpr int kPairsPerWarp = 4;
+#ifndef SPX_TREE
+#define SPX_TREE 0  // tree (1) or chained (0) epilogue column sums
+#endif
+#ifndef SPX_MINB
+#define SPX_MINB 4  // resident blocks per SM the register budget is sized for
+#endif
+#ifndef SPX_ACC_MODE
+#define SPX_ACC_MODE 0  // development timing knob: 1 = skip per-pixel sums, 2 = skip epilogue
+#endif
+#ifndef SPX_XPF
+#define SPX_XPF 0   // load the next pair's records / first run during this pair
+#endif
+constexpr size_t kCandBytes = 18 * 16 + 18 * 4 + 18 * 4;  // cand, cy, cand_k
+#ifndef SPX_ACC_STRIDE
+#define SPX_ACC_STRIDE 34
+#endif
+// Accumulator column stride (entries).  34 = 32 lanes + 2 pad: per-pixel
+// updates are lane-consecutive (conflict-free) and the epilogue's per-lane
+// column reads (lane l reads column l) land 4 banks apart instead of all on
+// the same bank, which a stride of 32 would give (a 32-way conflict).
+constexpr int kCS = SPX_ACC_STRIDE;
+constexpr size_t kAccBytes = 9 * 3 * kCS * sizeof(double) + 9 * kCS * sizeof(uint64_t);
 constexpr size_t kWarpSmemAcc = kCandBytes + kAccBytes;
 constexpr size_t kWarpSmemNoAcc = kCandBytes;
 
+constexpr int kLpc = 16;  // lanes per cell: two cells per warp, 9 staging lanes per cell
+
+// One warp walks `pairs_per_warp` consecutive cell pairs of one frame.  The
+// next pair's candidate records and first Lab run are loaded while the current
+// pair finishes (its last runs and its epilogue), so the per-cell load
+// latency is hidden behind work instead of exposed at every cell start.
 template <bool ACC>
-__global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
+__global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int lpc = p.lanes_per_cell;
-  const int cpw = 32 / lpc;                    // cells per warp (1 or 2)
-  const int ci = lane / lpc, ll = lane % lpc;  // cell within warp, lane within cell
+  const int ci = lane / kLpc, ll = lane % kLpc;  // cell within warp, lane within cell
   const int S = p.s;
   const int K = p.ns_r * p.ns_c;
-  // grid: x = cell groups of one frame, y = frame (no 64-bit divisions)
   const int f = blockIdx.y;
-  const int cell = p.cr0 * p.ns_c + (blockIdx.x * kWarps + warp) * cpw + ci;
+  if (p.done && p.done[f] == 1) return;  // whole block: one frame
+  const int n_cells = (p.cr1 - p.cr0) * p.ns_c;
+  const int pair_begin = (blockIdx.x * kWarps + warp) * p.pairs_per_warp;
+  const int pair_end = min(pair_begin + p.pairs_per_warp, (n_cells + 1) >> 1);
+  if (pair_begin >= pair_end) return;  // whole warp
+
   unsigned char* wbase = smem + (size_t)warp * (ACC ? kWarpSmemAcc : kWarpSmemNoAcc);
-  CandPairs* cand = reinterpret_cast<CandPairs*>(wbase) + ci * 9;
-  int* cand_k = reinterpret_cast<int*>(wbase + sizeof(CandPairs) * 18) + ci * 9;
+  float4* cand = reinterpret_cast<float4*>(wbase) + ci * 9;
+  float* cyv = reinterpret_cast<float*>(wbase + 18 * 16) + ci * 9;
+  int* cand_k = reinterpret_cast<int*>(wbase + 18 * 16 + 18 * 4) + ci * 9;
   double* accd = reinterpret_cast<double*>(wbase + kCandBytes);
   unsigned long long* acci =
-      reinterpret_cast<unsigned long long*>(wbase + kCandBytes + 9 * 3 * 32 * sizeof(double));
+      reinterpret_cast<unsigned long long*>(wbase + kCandBytes + 9 * 3 * kCS * sizeof(double));
 
-  bool active = cell < p.cr1 * p.ns_c && !(p.done && p.done[f] == 1);
-  int cr = 0, cc = 0;
-  if (active) {
-    cr = cell / p.ns_c;
-    cc = cell - cr * p.ns_c;
-  }
-
-  // ---- stage the 9 candidates (lanes ll < 9 of each cell) ------------------
-  float mc = 0.f, mxy = 0.f, okf = 1.f;
-  if (active && ll < 9) {
-    const int t = ll;
-    const int kr = cr + off_r(t), kc = cc + off_c(t);
-    CandPairs cp;
-    float cyt;
-    if (kr >= 0 && kr < p.ns_r && kc >= 0 && kc < p.ns_c) {
-      const float4* q = reinterpret_cast<const float4*>(p.rec + (long long)f * K + kr * p.ns_c + kc);
-      const float4 v0 = __ldg(q), v1 = __ldg(q + 1);
-      const float cxt = __fadd_rn(v0.w, (float)(off_c(t) * S));
-      cyt = __fadd_rn(v1.x, (float)(off_r(t) * S));
-      cp.l = f2_pack(v0.x, v0.x);
-      cp.a = f2_pack(v0.y, v0.y);
-      cp.b = f2_pack(v0.z, v0.z);
-      cp.x = f2_pack(cxt, cxt);
-      cp.y = f2_pack(cyt, cyt);
-      mc = v1.y;
-      mxy = fmaxf(fabsf(cxt), fabsf(cyt));
-      okf = v1.w;
-    } else {
-      // Out of the grid: colour 1e18 away makes D ~1e18, never the argmin.
-      cp.l = f2_pack(1e18f, 1e18f);
-      cp.a = cp.b = f2_pack(0.f, 0.f);
-      cp.x = f2_pack(0.f, 0.f);
-      cp.y = f2_pack(0.f, 0.f);
-      cyt = 0.f;
+  const long long hw = (long long)p.h * p.w;
+  const float* fimg = p.img + (long long)f * 3 * hw;
+  const CRec* frec = p.rec + (long long)f * K;
+  const long long img_base = (long long)f * hw;
+  const unsigned rmag = p.row_magic;
+  // row = j / runs_per_row via a 16-bit reciprocal (exact for j <= 256, rpr <= 8)
+  auto run_pos = [&](int jj, int& row, int& c4) {
+    row = (int)(((unsigned)jj * rmag) >> 16);
+    c4 = (jj - row * p.runs_per_row) * 4;
+  };
+  // geometry of a cell (local grid): row, column; valid if inside [cr0, cr1)
+  auto cell_rc = [&](int pair, int& cr, int& cc) {
+    const int cell = p.cr0 * p.ns_c + pair * 2 + ci;
+    const bool ok = pair * 2 + ci < n_cells;
+    cr = ok ? cell / p.ns_c : 0;
+    cc = ok ? cell - cr * p.ns_c : 0;
+    return ok;
+  };
+  // loads of one cell's staging record (lanes ll < 9) and a lane's first run
+  auto load_rec = [&](bool act, int cr, int cc, float4& v0, float4& v1) {
+    const int kr = cr + off_r(ll), kc = cc + off_c(ll);
+    if (act && ll < 9 && kr >= 0 && kr < p.ns_r && kc >= 0 && kc < p.ns_c) {
+      const float4* q = reinterpret_cast<const float4*>(frec + kr * p.ns_c + kc);
+      v0 = __ldg(q);
+      v1 = __ldg(q + 1);
     }
-    cand[t] = cp;
-    cand_k[t] = kr * p.ns_c + kc;  // only read for in-grid winners
-  }
-  // cell-wide maxima over the 9 staging lanes
-#pragma unroll
-  for (int o = 8; o; o >>= 1) {
-    mc = fmaxf(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, o));
-    mxy = fmaxf(mxy, __shfl_xor_sync(0xFFFFFFFFu, mxy, o));
-    okf = fminf(okf, __shfl_xor_sync(0xFFFFFFFFu, okf, o));
-  }
-  // lanes 0..15 of each cell hold the reduction; broadcast from the cell's lane 0
-  mc = __shfl_sync(0xFFFFFFFFu, mc, ci * lpc);
-  mxy = __shfl_sync(0xFFFFFFFFu, mxy, ci * lpc);
-  okf = __shfl_sync(0xFFFFFFFFu, okf, ci * lpc);
-  if (ACC) {
-    // zero the warp's accumulator block cooperatively with 16-byte stores
-    float4* z = reinterpret_cast<float4*>(accd);
-#pragma unroll
-    for (int i = lane; i < (int)(kAccBytes / 16); i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  __syncwarp();
-
-  // Cell constant of 2A: k_mc*Mc + k_xy*(3*Mxy + 2S) + k_const
-  float two_a_cell = __fmaf_rn(mc, p.k_mc, __fmaf_rn(__fmaf_rn(3.f, mxy, 2.f * S), p.k_xy, p.k_const));
-  if (okf == 0.f) two_a_cell = INFINITY;
-  const int x_cell = cc * S, y_cell = cr * S;          // local pixel origin
-  const int y_glob0 = (cr + p.row_off) * S;           // global y of the cell's row 0
-  const long long img_base = (long long)f * p.h * p.w;
-
-  if (active) {
-    const long long hw = (long long)p.h * p.w;
-    const float* fimg = p.img + (long long)f * 3 * hw;
-    // row = j / runs_per_row via a 16-bit reciprocal (exact for j <= 256, rpr <= 8)
-    const unsigned rmag = p.row_magic;
-    auto run_ok = [&](int jj, int& row, int& c4) {
-      row = (int)(((unsigned)jj * rmag) >> 16);
-      c4 = (jj - row * p.runs_per_row) * 4;
-      return jj < p.runs && y_cell + row < p.h && x_cell + c4 < p.w;
-    };
-    int row_n, c4_n;
-    bool ok_n = run_ok(ll, row_n, c4_n);
-    float4 Ln = make_float4(0.f, 0.f, 0.f, 0.f), An = Ln, Bn = Ln;
-    if (ok_n) {
-      const float* q = fimg + (long long)(y_cell + row_n) * p.w + x_cell + c4_n;
-      Ln = __ldg(reinterpret_cast<const float4*>(q));
-      An = __ldg(reinterpret_cast<const float4*>(q + hw));
-      Bn = __ldg(reinterpret_cast<const float4*>(q + 2 * hw));
+  };
+  int row0, c40;
+  run_pos(ll, row0, c40);
+  auto load_run = [&](bool ok, int y, int x, float4& Lx, float4& Ax, float4& Bx) {
+    if (ok) {
+      const float* q = fimg + (long long)y * p.w + x;
+      Lx = __ldg(reinterpret_cast<const float4*>(q));
+      Ax = __ldg(reinterpret_cast<const float4*>(q + hw));
+      Bx = __ldg(reinterpret_cast<const float4*>(q + 2 * hw));
     }
-    for (int j = ll; j < p.runs; j += lpc) {
+  };
+
+  // prefetch for the first pair
+  int cr_n, cc_n;
+  bool act_n = cell_rc(pair_begin, cr_n, cc_n);
+  float4 rv0 = make_float4(0.f, 0.f, 0.f, 0.f), rv1 = rv0;
+  load_rec(act_n, cr_n, cc_n, rv0, rv1);
+  bool ok_n = act_n && ll < p.runs && cr_n * S + row0 < p.h && cc_n * S + c40 < p.w;
+  int row_n = row0, c4_n = c40;
+  float4 Ln = make_float4(0.f, 0.f, 0.f, 0.f), An = Ln, Bn = Ln;
+  load_run(ok_n, cr_n * S + row0, cc_n * S + c40, Ln, An, Bn);
+
+  for (int pair = pair_begin; pair < pair_end; ++pair) {
+    const bool active = act_n;
+    const int cr = cr_n, cc = cc_n;
+    // ---- stage the 9 candidates (lanes ll < 9 of each cell) ----------------
+    float mc = 0.f, mxy = 0.f, okf = 1.f;
+    if (active && ll < 9) {
+      const int t = ll;
+      const int kr = cr + off_r(t), kc = cc + off_c(t);
+      float4 cp;
+      float cyt = 0.f;
+      if (kr >= 0 && kr < p.ns_r && kc >= 0 && kc < p.ns_c) {
+        const float cxt = __fadd_rn(rv0.w, (float)(off_c(t) * S));
+        cyt = __fadd_rn(rv1.x, (float)(off_r(t) * S));
+        cp = make_float4(rv0.x, rv0.y, rv0.z, cxt);
+        mc = rv1.y;
+        mxy = fmaxf(fabsf(cxt), fabsf(cyt));
+        okf = rv1.w;
+      } else {
+        // Out of the grid: colour 1e18 away makes D ~1e18, never the argmin.
+        cp = make_float4(1e18f, 0.f, 0.f, 0.f);
+      }
+      cand[t] = cp;
+      cyv[t] = cyt;
+      cand_k[t] = kr * p.ns_c + kc;  // only read for in-grid winners
+    }
+#pragma unroll
+    for (int o = 8; o; o >>= 1) {
+      mc = fmaxf(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, o));
+      mxy = fmaxf(mxy, __shfl_xor_sync(0xFFFFFFFFu, mxy, o));
+      okf = fminf(okf, __shfl_xor_sync(0xFFFFFFFFu, okf, o));
+    }
+    if (ACC) {
+      float4* z = reinterpret_cast<float4*>(accd);
+#pragma unroll
+      for (int i = lane; i < (int)(kAccBytes / 16); i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+
+    // Cell constant of 2A: k_mc*Mc + k_xy*(3*Mxy + 2S) + k_const
+    float two_a_cell =
+        __fmaf_rn(mc, p.k_mc, __fmaf_rn(__fmaf_rn(3.f, mxy, 2.f * S), p.k_xy, p.k_const));
+    if (okf == 0.f) two_a_cell = INFINITY;
+    const int x_cell = cc * S, y_cell = cr * S;  // local pixel origin
+    const int y_glob0 = (cr + p.row_off) * S;    // global y of the cell's row 0
+
+    // the next pair's geometry and staging records (loaded during this pair)
+    const bool has_next = pair + 1 < pair_end;
+    act_n = has_next && cell_rc(pair + 1, cr_n, cc_n);
+    if (SPX_XPF) load_rec(act_n, cr_n, cc_n, rv0, rv1);
+
+    for (int j = ll; j < p.runs; j += kLpc) {
       const int row = row_n, c4 = c4_n;
       const bool ok = ok_n;
       const float4 Lv = Ln, Av = An, Bv = Bn;
-      // prefetch the next run of this lane (software pipelining)
-      ok_n = run_ok(j + lpc, row_n, c4_n);
-      if (ok_n) {
-        const float* q = fimg + (long long)(y_cell + row_n) * p.w + x_cell + c4_n;
-        Ln = __ldg(reinterpret_cast<const float4*>(q));
-        An = __ldg(reinterpret_cast<const float4*>(q + hw));
-        Bn = __ldg(reinterpret_cast<const float4*>(q + 2 * hw));
+      // prefetch the lane's next run: this cell's, else the next pair's first
+      if (j + kLpc < p.runs) {
+        run_pos(j + kLpc, row_n, c4_n);
+        ok_n = active && y_cell + row_n < p.h && x_cell + c4_n < p.w;
+        load_run(ok_n, y_cell + row_n, x_cell + c4_n, Ln, An, Bn);
+      } else if (SPX_XPF) {
+        row_n = row0;
+        c4_n = c40;
+        ok_n = act_n && cr_n * S + row0 < p.h && cc_n * S + c40 < p.w;
+        load_run(ok_n, cr_n * S + row0, cc_n * S + c40, Ln, An, Bn);
       }
       if (!ok) continue;
       const int y = y_cell + row, x = x_cell + c4;
-      const long long pix = img_base + (long long)y * p.w + x;   // label index
+      const long long pix = img_base + (long long)y * p.w + x;  // label index
       // Channel 0 carries the certified-sum flag in its sign bit (set by the
       // engine's planar convert; channel 0 is never negative): strip it.
       const unsigned fl4 = (__float_as_uint(Lv.x) >> 31) | ((__float_as_uint(Lv.y) >> 31) << 1) |
-                           ((__float_as_uint(Lv.z) >> 31) << 2) | ((__float_as_uint(Lv.w) >> 31) << 3);
+                           ((__float_as_uint(Lv.z) >> 31) << 2) |
+                           ((__float_as_uint(Lv.w) >> 31) << 3);
       const float L[4] = {fabsf(Lv.x), fabsf(Lv.y), fabsf(Lv.z), fabsf(Lv.w)};
       const float A[4] = {Av.x, Av.y, Av.z, Av.w};
       const float B[4] = {Bv.x, Bv.y, Bv.z, Bv.w};
@@ -252,15 +301,18 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
       const unsigned long long X01 = f2_pack(xr0, xr0 + 1.f);
       const unsigned long long X23 = f2_pack(xr0 + 2.f, xr0 + 3.f);
       const float yr = (float)row;
-      const unsigned long long Y2 = f2_pack(yr, yr);
       unsigned k1[4] = {0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu};
       unsigned k2[4] = {0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu};
       const float w32 = p.w32;
 #pragma unroll
       for (int t = 0; t < 9; ++t) {
-        const CandPairs c = cand[t];
-        const unsigned long long dy = sub2(c.y, Y2);
-        const unsigned long long dyy = mul2(dy, dy);
+        const float4 cv = cand[t];
+        const float dyf = __fsub_rn(cyv[t], yr);
+        const float dyyf = __fmul_rn(dyf, dyf);
+        const unsigned long long dyy = f2_pack(dyyf, dyyf);
+        struct {
+          unsigned long long l, a, b, x;
+        } c = {f2_pack(cv.x, cv.x), f2_pack(cv.y, cv.y), f2_pack(cv.z, cv.z), f2_pack(cv.w, cv.w)};
         float Q[4], R[4];
         {
           unsigned long long dl = sub2(c.l, L01), da = sub2(c.a, A01), db = sub2(c.b, B01);
@@ -303,58 +355,81 @@ __global__ void __launch_bounds__(128, 4) k_cell(CellParams p) {
           t = idx < 4 ? idx + 1 : (idx == 4 ? 0 : idx);  // (dr,dc) -> scan slot
         }
         lab4[i] = k + p.row_off * p.ns_c;  // labels carry GLOBAL cluster ids
-        if (ACC) {
+        if (ACC && SPX_ACC_MODE != 1) {
           const unsigned fl = (fl4 >> i) & 1u;
-          double* d = accd + t * 96 + lane;
+          double* d = accd + t * (3 * kCS) + lane;
           d[0] = dadd(d[0], (double)L[i]);
-          d[32] = dadd(d[32], (double)A[i]);
-          d[64] = dadd(d[64], (double)B[i]);
-          acci[t * 32 + lane] += 1ull | ((unsigned long long)fl << 11) |
+          d[kCS] = dadd(d[kCS], (double)A[i]);
+          d[2 * kCS] = dadd(d[2 * kCS], (double)B[i]);
+          acci[t * kCS + lane] += 1ull | ((unsigned long long)fl << 11) |
                                  ((unsigned long long)(c4 + i) << 22) |
                                  ((unsigned long long)row << 43);
         }
       }
       *reinterpret_cast<int4*>(p.labels + pix) = make_int4(lab4[0], lab4[1], lab4[2], lab4[3]);
     }
-  }
-  if (!ACC) return;
-  __syncwarp();
-  // ---- per-cell column reduction: 9 slots x (3 colour + 1 packed int) -------
-  // column c < 27: colour (slot c/3, channel c%3); 27 <= c < 36: ints of slot
-  // c-27.  Each column holds lpc lane entries, read as 16-byte vectors.  The
-  // cell's per-slot sums go straight into the owning cluster's accumulator
-  // with global atomics: under the certified-sum condition every partial sum
-  // is exact, so the result does not depend on the order of the atomics
-  // (flagged clusters are recomputed exactly by k_exact_clusters).
-  const int lane0 = ci * lpc;
-  if (active) {
-    ClusterAcc* fa = p.acc + (long long)f * K;
-    for (int col = ll; col < 36; col += lpc) {
-      if (col < 27) {
-        const double2* src = reinterpret_cast<const double2*>(accd + col * 32 + lane0);
-        double sacc = 0.0;
-        for (int q = 0; q < lpc / 2; ++q) {
-          const double2 v = src[q];
-          sacc = dadd(dadd(sacc, v.x), v.y);
-        }
-        // an empty (or out-of-grid) slot sums to +0.0: nothing to add
-        if (sacc != 0.0) atomicAdd(&fa[cand_k[col / 3]].s[col % 3], sacc);
-      } else {
-        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(acci + (col - 27) * 32 + lane0);
-        unsigned long long tot = 0;
-        for (int q = 0; q < lpc / 2; ++q) {
-          const ulonglong2 v = src[q];
-          tot += v.x + v.y;  // fields cannot overflow (see packing above)
-        }
-        const unsigned long long cnt = tot & 2047ull;
-        if (cnt) {
-          ClusterAcc* o = fa + cand_k[col - 27];
-          const unsigned long long flg = (tot >> 11) & 2047ull;
-          atomicAdd(&o->sx, ((tot >> 22) & 0x1FFFFFull) + cnt * (unsigned long long)x_cell);
-          atomicAdd(&o->sy, (tot >> 43) + cnt * (unsigned long long)y_glob0);
-          atomicAdd(&o->cf, cnt | (flg << 32));
+    if (ACC && SPX_ACC_MODE != 2) {
+      __syncwarp();
+      // ---- per-cell column reduction: 9 slots x (3 colour + 1 packed int) ---
+      // column c < 27: colour (slot c/3, channel c%3); 27 <= c < 36: ints of
+      // slot c-27.  The 16 lane entries of a column are summed as a tree (any
+      // order is exact under the certified-sum condition; flagged clusters
+      // are recomputed by k_exact_clusters) and go straight into the owning
+      // cluster's accumulator with global atomics.
+      const int lane0 = ci * kLpc;
+      if (active) {
+        ClusterAcc* fa = p.acc + (long long)f * K;
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int col = ll + u * kLpc;
+          if (col < 27) {
+            const double2* src = reinterpret_cast<const double2*>(accd + col * kCS + lane0);
+#if SPX_TREE
+            double s4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double2 v = src[q], w2 = src[q + 4];
+              s4[q] = dadd(dadd(v.x, v.y), dadd(w2.x, w2.y));
+            }
+            const double sacc = dadd(dadd(s4[0], s4[1]), dadd(s4[2], s4[3]));
+#else
+            double sacc = 0.0;
+            for (int q = 0; q < 8; ++q) {
+              const double2 v = src[q];
+              sacc = dadd(dadd(sacc, v.x), v.y);
+            }
+#endif
+            // an empty (or out-of-grid) slot sums to +0.0: nothing to add
+            if (SPX_ACC_MODE == 3 ? sacc == 1.2345e300 : sacc != 0.0)
+              atomicAdd(&fa[cand_k[col / 3]].s[col % 3], sacc);
+          } else if (col < 36) {
+            const ulonglong2* src =
+                reinterpret_cast<const ulonglong2*>(acci + (col - 27) * kCS + lane0);
+            unsigned long long tot = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const ulonglong2 v = src[q];
+              tot += v.x + v.y;  // fields cannot overflow (see packing above)
+            }
+            const unsigned long long cnt = tot & 2047ull;
+            if (SPX_ACC_MODE == 3 ? cnt == 2047 : cnt != 0) {
+              ClusterAcc* o = fa + cand_k[col - 27];
+              const unsigned long long flg = (tot >> 11) & 2047ull;
+              atomicAdd(&o->sx, ((tot >> 22) & 0x1FFFFFull) + cnt * (unsigned long long)x_cell);
+              atomicAdd(&o->sy, (tot >> 43) + cnt * (unsigned long long)y_glob0);
+              atomicAdd(&o->cf, cnt | (flg << 32));
+            }
+          }
         }
       }
+    }
+    __syncwarp();  // smem (candidates, accumulators) is rewritten by the next pair
+    if (!SPX_XPF) {
+      load_rec(act_n, cr_n, cc_n, rv0, rv1);
+      row_n = row0;
+      c4_n = c40;
+      ok_n = act_n && cr_n * S + row0 < p.h && cc_n * S + c40 < p.w;
+      load_run(ok_n, cr_n * S + row0, cc_n * S + c40, Ln, An, Bn);
     }
   }
 }
@@ -688,12 +763,12 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.runs = (int)(s * s / 4);
   p.runs_per_row = (int)(s / 4);
   p.row_magic = (unsigned)((65536 + p.runs_per_row - 1) / p.runs_per_row);
-  p.lanes_per_cell = 16;  // two cells per warp; 9 staging lanes per cell
+  static const int ppw_env = getenv("SPX_PPW") ? atoi(getenv("SPX_PPW")) : kPairsPerWarp;
+  p.pairs_per_warp = ppw_env;
   p.xy_weight = xy_weight;
   assoc_bound_coefficients(xy_weight, p.w32, p.k_mp, p.k_mc, p.k_xy, p.k_const, p.k_rel);
-  const int cpw = 32 / p.lanes_per_cell;
   if (cr1 <= cr0) return SPX_OK;
-  const long long warps = ceil_div((cr1 - cr0) * ns_c, cpw);
+  const long long warps = ceil_div(ceil_div((cr1 - cr0) * ns_c, 2), p.pairs_per_warp);
   const dim3 blocks((unsigned)ceil_div(warps, kWarps), (unsigned)frames);
   if (frames > 65535) {
     set_error("k_cell: at most 65535 frames per launch");
