@@ -126,17 +126,21 @@ constexpr int kPairsPerWarp = 4;
 #ifndef SPX_ACC_MODE
 #define SPX_ACC_MODE 0  // development timing knob: 1 = skip per-pixel sums, 2 = skip epilogue
 #endif
+#ifndef SPX_LEAD
+#define SPX_LEAD 0  // combine same-slot pixels of a run before the smem update
+#endif
 #ifndef SPX_XPF
 #define SPX_XPF 0   // load the next pair's records / first run during this pair
 #endif
 constexpr size_t kCandBytes = 18 * 16 + 18 * 4 + 18 * 4;  // cand, cy, cand_k
 #ifndef SPX_ACC_STRIDE
-#define SPX_ACC_STRIDE 34
+#define SPX_ACC_STRIDE 32
 #endif
-// Accumulator column stride (entries).  34 = 32 lanes + 2 pad: per-pixel
-// updates are lane-consecutive (conflict-free) and the epilogue's per-lane
-// column reads (lane l reads column l) land 4 banks apart instead of all on
-// the same bank, which a stride of 32 would give (a 32-way conflict).
+// Accumulator column stride (entries).  With 32, every column starts on
+// bank 0, so the per-pixel updates (lane l touches entry l of the column of
+// its slot) are conflict-free whatever slots the lanes pick; the epilogue,
+// where lane l sums column l, starts each lane at a different 16-byte
+// offset ((q + l) & 7) so its reads do not all hit the same banks.
 constexpr int kCS = SPX_ACC_STRIDE;
 constexpr size_t kAccBytes = 9 * 3 * kCS * sizeof(double) + 9 * kCS * sizeof(uint64_t);
 constexpr size_t kWarpSmemAcc = kCandBytes + kAccBytes;
@@ -339,31 +343,105 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
           k1[i] = min(k1[i], key);
         }
       }
-      int lab4[4];
+      // certificate for the 4 pixels; uncertain ones (rare) take the exact path
+      int t[4];
+      bool unsure = false;
+      unsigned need = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float mp = fabsf(L[i]) + fabsf(A[i]) + fabsf(B[i]);
         const float f2v = __uint_as_float(k2[i]);
         const float thr = __fmaf_rn(f2v, p.k_rel, __fmaf_rn(mp, p.k_mp, two_a_cell));
         const float gap = __fsub_rn(f2v, __uint_as_float(k1[i]));
-        int t = (int)(k1[i] & 15u);
-        int k = cand_k[t];
-        if (!(gap > thr) || !(mp < 1e15f)) {
-          k = exact_argmin(p.cxy + (long long)f * K * 2, p.clab + (long long)f * K * 3, L[i], A[i],
-                           B[i], x + i, y_glob0 + row, cr, cc, p.ns_r, p.ns_c, p.xy_weight);
-          const int idx = (k / p.ns_c - cr + 1) * 3 + (k % p.ns_c - cc + 1);
-          t = idx < 4 ? idx + 1 : (idx == 4 ? 0 : idx);  // (dr,dc) -> scan slot
+        t[i] = (int)(k1[i] & 15u);
+        const bool u = !(gap > thr) || !(mp < 1e15f);
+        need |= (unsigned)u << i;
+        unsure |= u;
+      }
+      if (unsure) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (need >> i & 1u) {
+            const int k = exact_argmin(p.cxy + (long long)f * K * 2, p.clab + (long long)f * K * 3,
+                                       L[i], A[i], B[i], x + i, y_glob0 + row, cr, cc, p.ns_r,
+                                       p.ns_c, p.xy_weight);
+            const int idx = (k / p.ns_c - cr + 1) * 3 + (k % p.ns_c - cc + 1);
+            t[i] = idx < 4 ? idx + 1 : (idx == 4 ? 0 : idx);  // (dr,dc) -> scan slot
+          }
         }
-        lab4[i] = k + p.row_off * p.ns_c;  // labels carry GLOBAL cluster ids
-        if (ACC && SPX_ACC_MODE != 1) {
-          const unsigned fl = (fl4 >> i) & 1u;
-          double* d = accd + t * (3 * kCS) + lane;
+      }
+      int lab4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) lab4[i] = cand_k[t[i]] + p.row_off * p.ns_c;  // GLOBAL ids
+      if (ACC && SPX_ACC_MODE != 1 && !SPX_LEAD) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double* d = accd + t[i] * (3 * kCS) + lane;
           d[0] = dadd(d[0], (double)L[i]);
           d[kCS] = dadd(d[kCS], (double)A[i]);
           d[2 * kCS] = dadd(d[2 * kCS], (double)B[i]);
-          acci[t * kCS + lane] += 1ull | ((unsigned long long)fl << 11) |
-                                 ((unsigned long long)(c4 + i) << 22) |
-                                 ((unsigned long long)row << 43);
+          acci[t[i] * kCS + lane] += 1ull | ((unsigned long long)((fl4 >> i) & 1u) << 11) |
+                                     ((unsigned long long)(c4 + i) << 22) |
+                                     ((unsigned long long)row << 43);
+        }
+      }
+      if (ACC && SPX_ACC_MODE != 1 && SPX_LEAD) {
+        // Pixels of the run that share a slot are summed in registers first
+        // and only the first of them (the leader) updates the slot's
+        // accumulator, so the four read-modify-writes touch distinct entries
+        // and overlap instead of chaining through shared memory.  (Any
+        // summation order is exact under the certified-sum condition.)
+        const bool e01 = t[1] == t[0], e02 = t[2] == t[0], e03 = t[3] == t[0];
+        const bool e12 = t[2] == t[1], e13 = t[3] == t[1], e23 = t[3] == t[2];
+        const bool lead[4] = {true, !e01, !e02 && !e12, !e03 && !e13 && !e23};
+        unsigned long long pk[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          pk[i] = 1ull | ((unsigned long long)((fl4 >> i) & 1u) << 11) |
+                  ((unsigned long long)(c4 + i) << 22) | ((unsigned long long)row << 43);
+        double g[4][3];
+        unsigned long long gi[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          g[i][0] = (double)L[i];
+          g[i][1] = (double)A[i];
+          g[i][2] = (double)B[i];
+          gi[i] = pk[i];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (e01) g[0][c] = dadd(g[0][c], g[1][c]);
+          if (e02) g[0][c] = dadd(g[0][c], g[2][c]);
+          if (e03) g[0][c] = dadd(g[0][c], g[3][c]);
+          if (e12) g[1][c] = dadd(g[1][c], g[2][c]);
+          if (e13) g[1][c] = dadd(g[1][c], g[3][c]);
+          if (e23) g[2][c] = dadd(g[2][c], g[3][c]);
+        }
+        if (e01) gi[0] += pk[1];
+        if (e02) gi[0] += pk[2];
+        if (e03) gi[0] += pk[3];
+        if (e12) gi[1] += pk[2];
+        if (e13) gi[1] += pk[3];
+        if (e23) gi[2] += pk[3];
+        double old[4][3];
+        unsigned long long oldi[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double* d = accd + t[i] * (3 * kCS) + lane;
+          old[i][0] = d[0];
+          old[i][1] = d[kCS];
+          old[i][2] = d[2 * kCS];
+          oldi[i] = acci[t[i] * kCS + lane];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (lead[i]) {
+            double* d = accd + t[i] * (3 * kCS) + lane;
+            d[0] = dadd(old[i][0], g[i][0]);
+            d[kCS] = dadd(old[i][1], g[i][1]);
+            d[2 * kCS] = dadd(old[i][2], g[i][2]);
+            acci[t[i] * kCS + lane] = oldi[i] + gi[i];
+          }
         }
       }
       *reinterpret_cast<int4*>(p.labels + pix) = make_int4(lab4[0], lab4[1], lab4[2], lab4[3]);
@@ -388,14 +466,14 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
             double s4[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const double2 v = src[q], w2 = src[q + 4];
+              const double2 v = src[(q + ll) & 7], w2 = src[(q + 4 + ll) & 7];
               s4[q] = dadd(dadd(v.x, v.y), dadd(w2.x, w2.y));
             }
             const double sacc = dadd(dadd(s4[0], s4[1]), dadd(s4[2], s4[3]));
 #else
             double sacc = 0.0;
             for (int q = 0; q < 8; ++q) {
-              const double2 v = src[q];
+              const double2 v = src[(q + ll) & 7];
               sacc = dadd(dadd(sacc, v.x), v.y);
             }
 #endif
@@ -408,7 +486,7 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
             unsigned long long tot = 0;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const ulonglong2 v = src[q];
+              const ulonglong2 v = src[(q + ll) & 7];
               tot += v.x + v.y;  // fields cannot overflow (see packing above)
             }
             const unsigned long long cnt = tot & 2047ull;
