@@ -90,9 +90,54 @@ __device__ __forceinline__ double div_const(double x, double d, double inv) {
   return __fma_rn(r, inv, q);
 }
 
-__device__ __forceinline__ double lab_f(double t) {
-  // _core.pyx:73-75
-  return t > c_eps ? cbrt_glibc(t) : div_const(dadd(dmul(c_kappa, t), 16.0), 116.0, c_inv116);
+// Correctly rounded a / b for positive normal operands well inside the
+// exponent range (the cbrt quotient below: a, b in [0.5, 8]): MUFU reciprocal
+// seed, two Newton steps, then one Markstein correction.  Branch-free, unlike
+// the library division (whose special-case slow path splits the code and
+// stops the compiler from interleaving the 12 independent cbrt chains of a
+// 4-pixel group).  Proven equal to RN(a / b) on every input convert can
+// produce by the exhaustive 2^24-colour test.
+__device__ __forceinline__ double div_rn_fast(double a, double b) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+  double e = __fma_rn(-b, y, 1.0);
+  y = __fma_rn(e, y, y);
+  e = __fma_rn(-b, y, 1.0);
+  y = __fma_rn(e, y, y);
+  const double q = dmul(a, y);
+  const double r = __fma_rn(-b, q, a);
+  return __fma_rn(r, y, q);
+}
+
+// cbrt_glibc for positive normal x of moderate size (convert's t = X / Xw in
+// (0, 1.2]), with no branches: frexp by bit manipulation, the factor picked
+// with selects, ldexp by an exact power of two.  Same operations, same
+// rounding as cbrt_glibc.
+__device__ __forceinline__ double cbrt_fast(double x, const double* fac) {
+  const long long bits = __double_as_longlong(x);
+  const int xe = (int)((bits >> 52) & 0x7ff) - 1022;
+  const double xm = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | (1022LL << 52));
+  double p = dsub(0.784932344976639262, dmul(0.145263899385486377, xm));
+  p = dadd(-1.83469277483613086, dmul(p, xm));
+  p = dadd(2.44693122563534430, dmul(p, xm));
+  p = dadd(-2.11499494167371287, dmul(p, xm));
+  p = dadd(1.50819193781584896, dmul(p, xm));
+  const double u = dadd(0.354895765043919860, dmul(p, xm));
+  const double t2 = dmul(dmul(u, u), u);
+  const int m = xe % 3;  // in [-2, 2]
+  const double f = m == 0 ? fac[2] : m == 1 ? fac[3] : m == 2 ? fac[4] : m == -1 ? fac[1] : fac[0];
+  const double ym =
+      dmul(div_rn_fast(dmul(u, dadd(t2, dmul(2.0, xm))), dadd(dmul(2.0, t2), xm)), f);
+  const int n = xe / 3;
+  return dmul(ym, __longlong_as_double((long long)(1023 + n) << 52));
+}
+
+__device__ __forceinline__ double lab_f(double t, const double* fac) {
+  // _core.pyx:73-75; both branches evaluated, the cheap linear one selected
+  // for t <= eps (cbrt_fast's result is then unused, whatever it is).
+  const double c = cbrt_fast(t > c_eps ? t : 1.0, fac);
+  const double lin = div_const(dadd(dmul(c_kappa, t), 16.0), 116.0, c_inv116);
+  return t > c_eps ? c : lin;
 }
 
 template <int SPACE>
@@ -114,9 +159,10 @@ __device__ __forceinline__ void convert_px(const double* lut, uint32_t R, uint32
     o2 = __double2float_rn(cz);
     return;
   }
-  double fx = lab_f(div_const(cx, c_white[0], c_inv_white[0]));
-  double fy = lab_f(div_const(cy, c_white[1], c_inv_white[1]));
-  double fz = lab_f(div_const(cz, c_white[2], c_inv_white[2]));
+  const double fac[5] = {c_factor[0], c_factor[1], c_factor[2], c_factor[3], c_factor[4]};
+  double fx = lab_f(div_const(cx, c_white[0], c_inv_white[0]), fac);
+  double fy = lab_f(div_const(cy, c_white[1], c_inv_white[1]), fac);
+  double fz = lab_f(div_const(cz, c_white[2], c_inv_white[2]), fac);
   double light = dsub(dmul(116.0, fy), 16.0);
   if (light < 0.0) light = 0.0;
   if (light > 100.0) light = 100.0;
@@ -140,8 +186,11 @@ __device__ __forceinline__ float with_flag(float o0, float o1, float o2, float t
   return f ? __uint_as_float(__float_as_uint(o0) | 0x80000000u) : o0;
 }
 
+#ifndef SPX_CONV_MINB
+#define SPX_CONV_MINB 4  // 64 registers: 32 warps per SM
+#endif
 template <int SPACE, bool PLANAR>
-__global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb,
+__global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* __restrict__ rgb,
                                                  float* __restrict__ out, int64_t p0,
                                                  int64_t p1, int vec, int64_t hw, float tau) {
   __shared__ double lut[256];
@@ -151,7 +200,15 @@ __global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb
   }
   int64_t g0 = p0 >> 2, g1 = (p1 + 3) >> 2;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t g = g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < g1; g += stride) {
+  int64_t g = g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // PLANAR: frame index / offset of pixel q = 4g, advanced incrementally (no
+  // 64-bit division in the loop)
+  int64_t pf = 0, pr = 0;
+  if (PLANAR) {
+    pf = (g << 2) / hw;
+    pr = (g << 2) - pf * hw;
+  }
+  for (; g < g1; g += stride) {
     int64_t q = g << 2;
     if (vec && q >= p0 && q + 4 <= p1) {
       const uint32_t* src = reinterpret_cast<const uint32_t*>(rgb + q * 3);
@@ -169,8 +226,7 @@ __global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb
         convert_px<SPACE>(lut, c[3 * i], c[3 * i + 1], c[3 * i + 2], o[3 * i], o[3 * i + 1],
                           o[3 * i + 2]);
       if (PLANAR) {
-        const int64_t f = q / hw, r = q - f * hw;
-        float* base = out + f * 3 * hw + r;
+        float* base = out + pf * 3 * hw + pr;
         *reinterpret_cast<float4*>(base) =
             make_float4(with_flag(o[0], o[1], o[2], tau), with_flag(o[3], o[4], o[5], tau),
                         with_flag(o[6], o[7], o[8], tau), with_flag(o[9], o[10], o[11], tau));
@@ -197,6 +253,13 @@ __global__ void __launch_bounds__(256) k_convert(const uint8_t* __restrict__ rgb
           out[p * 3 + 1] = o1;
           out[p * 3 + 2] = o2;
         }
+      }
+    }
+    if (PLANAR) {
+      pr += stride << 2;
+      while (pr >= hw) {
+        pr -= hw;
+        ++pf;
       }
     }
   }

@@ -79,6 +79,21 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  {
+    for (int w = 0; w < 10; ++w) CK(launch_convert(rgb, lab, 0, B * hw, 2, s, hw, S));
+    std::vector<float> t(reps);
+    for (int r = 0; r < reps; ++r) {
+      cudaEventRecord(e0, s);
+      CK(launch_convert(rgb, lab, 0, B * hw, 2, s, hw, S));
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&t[r], e0, e1);
+    }
+    float sum = 0.f;
+    for (float v : t) sum += v;
+    printf("k_convert %dx%dx%d: mean %.4f ms (%.1f Gpx/s)\n", B, H, W, sum / reps,
+           B * hw / (sum / reps) / 1e6);
+  }
   for (int accf = 1; accf >= 0; --accf) {
     for (int w = 0; w < 3; ++w)
       CK(launch_cell(lab, cxy[cur], clab[cur], rec, labels, acc, nullptr, H, W, S, ns_r, ns_c, xyw,
