@@ -90,29 +90,39 @@ __device__ __forceinline__ double div_const(double x, double d, double inv) {
   return __fma_rn(r, inv, q);
 }
 
+#ifndef SPX_DIV_NEWTON
+#define SPX_DIV_NEWTON 1
+#endif
 // Correctly rounded a / b for positive normal operands well inside the
 // exponent range (the cbrt quotient below: a, b in [0.5, 8]): MUFU reciprocal
-// seed, two Newton steps, then one Markstein correction.  Branch-free, unlike
-// the library division (whose special-case slow path splits the code and
-// stops the compiler from interleaving the 12 independent cbrt chains of a
-// 4-pixel group).  Proven equal to RN(a / b) on every input convert can
-// produce by the exhaustive 2^24-colour test.
+// seed, SPX_DIV_NEWTON Newton steps, then one Markstein correction.
+// Branch-free, unlike the library division (whose special-case slow path
+// splits the code and stops the compiler from interleaving the 12
+// independent cbrt chains of a 4-pixel group).  Proven equal to RN(a / b) on
+// every input convert can produce by the exhaustive 2^24-colour test.
 __device__ __forceinline__ double div_rn_fast(double a, double b) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
-  double e = __fma_rn(-b, y, 1.0);
-  y = __fma_rn(e, y, y);
-  e = __fma_rn(-b, y, 1.0);
-  y = __fma_rn(e, y, y);
+#pragma unroll
+  for (int i = 0; i < SPX_DIV_NEWTON; ++i) {
+    const double e = __fma_rn(-b, y, 1.0);
+    y = __fma_rn(e, y, y);
+  }
   const double q = dmul(a, y);
   const double r = __fma_rn(-b, q, a);
   return __fma_rn(r, y, q);
 }
 
+// Exact scaling of a positive normal double by 2^n (result normal): an
+// integer add on the exponent field instead of a binary64 multiply.
+__device__ __forceinline__ double scale2(double x, int n) {
+  return __hiloint2double(__double2hiint(x) + (n << 20), __double2loint(x));
+}
+
 // cbrt_glibc for positive normal x of moderate size (convert's t = X / Xw in
 // (0, 1.2]), with no branches: frexp by bit manipulation, the factor picked
-// with selects, ldexp by an exact power of two.  Same operations, same
-// rounding as cbrt_glibc.
+// with selects, the exact doublings and the final ldexp as exponent adds.
+// Same rounded operations as cbrt_glibc, so the same result.
 __device__ __forceinline__ double cbrt_fast(double x, const double* fac) {
   const long long bits = __double_as_longlong(x);
   const int xe = (int)((bits >> 52) & 0x7ff) - 1022;
@@ -125,24 +135,29 @@ __device__ __forceinline__ double cbrt_fast(double x, const double* fac) {
   const double u = dadd(0.354895765043919860, dmul(p, xm));
   const double t2 = dmul(dmul(u, u), u);
   const int m = xe % 3;  // in [-2, 2]
-  const double f = m == 0 ? fac[2] : m == 1 ? fac[3] : m == 2 ? fac[4] : m == -1 ? fac[1] : fac[0];
+  double f = fac[2];  // selects on register values (no branches)
+  f = m == 1 ? fac[3] : f;
+  f = m == 2 ? fac[4] : f;
+  f = m == -1 ? fac[1] : f;
+  f = m == -2 ? fac[0] : f;
+  // 2*xm and 2*t2 are exact doublings (xm in [0.5, 1), t2 > 0.04)
   const double ym =
-      dmul(div_rn_fast(dmul(u, dadd(t2, dmul(2.0, xm))), dadd(dmul(2.0, t2), xm)), f);
-  const int n = xe / 3;
-  return dmul(ym, __longlong_as_double((long long)(1023 + n) << 52));
+      dmul(div_rn_fast(dmul(u, dadd(t2, scale2(xm, 1))), dadd(scale2(t2, 1), xm)), f);
+  return scale2(ym, xe / 3);
 }
 
-__device__ __forceinline__ double lab_f(double t, const double* fac) {
-  // _core.pyx:73-75; both branches evaluated, the cheap linear one selected
-  // for t <= eps (cbrt_fast's result is then unused, whatever it is).
-  const double c = cbrt_fast(t > c_eps ? t : 1.0, fac);
-  const double lin = div_const(dadd(dmul(c_kappa, t), 16.0), 116.0, c_inv116);
-  return t > c_eps ? c : lin;
+__device__ __forceinline__ double lab_lin(double t) {
+  return div_const(dadd(dmul(c_kappa, t), 16.0), 116.0, c_inv116);
 }
+
+struct Factors {
+  double f[5];
+};
 
 template <int SPACE>
-__device__ __forceinline__ void convert_px(const double* lut, uint32_t R, uint32_t G, uint32_t B,
-                                           float& o0, float& o1, float& o2) {
+__device__ __forceinline__ void convert_px(const double* lut, const Factors& fc, uint32_t R,
+                                           uint32_t G, uint32_t B, float& o0, float& o1,
+                                           float& o2) {
   if (SPACE == 0) {
     o0 = __double2float_rn(ddiv((double)R, 255.0));
     o1 = __double2float_rn(ddiv((double)G, 255.0));
@@ -159,10 +174,20 @@ __device__ __forceinline__ void convert_px(const double* lut, uint32_t R, uint32
     o2 = __double2float_rn(cz);
     return;
   }
-  const double fac[5] = {c_factor[0], c_factor[1], c_factor[2], c_factor[3], c_factor[4]};
-  double fx = lab_f(div_const(cx, c_white[0], c_inv_white[0]), fac);
-  double fy = lab_f(div_const(cy, c_white[1], c_inv_white[1]), fac);
-  double fz = lab_f(div_const(cz, c_white[2], c_inv_white[2]), fac);
+  const double* fac = fc.f;
+  // _core.pyx:73-75: f(t) = cbrt(t) if t > eps else (kappa t + 16) / 116.  The
+  // cbrt chains run unconditionally (on 1.0 where t <= eps) so the compiler
+  // can interleave them; the rare linear branch is patched in afterwards.
+  const double tx = div_const(cx, c_white[0], c_inv_white[0]);
+  const double ty = div_const(cy, c_white[1], c_inv_white[1]);
+  const double tz = div_const(cz, c_white[2], c_inv_white[2]);
+  const double eps = c_eps;
+  double fx = cbrt_fast(tx > eps ? tx : 1.0, fac);
+  double fy = cbrt_fast(ty > eps ? ty : 1.0, fac);
+  double fz = cbrt_fast(tz > eps ? tz : 1.0, fac);
+  if (!(tx > eps)) fx = lab_lin(tx);
+  if (!(ty > eps)) fy = lab_lin(ty);
+  if (!(tz > eps)) fz = lab_lin(tz);
   double light = dsub(dmul(116.0, fy), 16.0);
   if (light < 0.0) light = 0.0;
   if (light > 100.0) light = 100.0;
@@ -194,6 +219,9 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
                                                  float* __restrict__ out, int64_t p0,
                                                  int64_t p1, int vec, int64_t hw, float tau) {
   __shared__ double lut[256];
+  Factors fc;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) fc.f[i] = c_factor[i];
   if (SPACE != 0) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = g_lut[i];
     __syncthreads();
@@ -223,7 +251,7 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
       float o[12];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        convert_px<SPACE>(lut, c[3 * i], c[3 * i + 1], c[3 * i + 2], o[3 * i], o[3 * i + 1],
+        convert_px<SPACE>(lut, fc, c[3 * i], c[3 * i + 1], c[3 * i + 2], o[3 * i], o[3 * i + 1],
                           o[3 * i + 2]);
       if (PLANAR) {
         float* base = out + pf * 3 * hw + pr;
@@ -242,7 +270,7 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
       for (int64_t p = q; p < q + 4; ++p) {
         if (p < p0 || p >= p1) continue;
         float o0, o1, o2;
-        convert_px<SPACE>(lut, rgb[p * 3], rgb[p * 3 + 1], rgb[p * 3 + 2], o0, o1, o2);
+        convert_px<SPACE>(lut, fc, rgb[p * 3], rgb[p * 3 + 1], rgb[p * 3 + 2], o0, o1, o2);
         if (PLANAR) {
           const int64_t f = p / hw, r = p - f * hw;
           out[f * 3 * hw + r] = with_flag(o0, o1, o2, tau);
