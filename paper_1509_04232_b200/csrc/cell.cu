@@ -599,14 +599,14 @@ __device__ __forceinline__ void write_centre(const ReduceParams& p, long long gk
 __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
   const int K = p.ns_r * p.ns_c;
   const int nk = (p.kr1 - p.kr0) * p.ns_c;
-  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool in = j < (long long)nk * p.frames;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;  // cluster of frame blockIdx.y
+  const bool in = j < nk;
   int f = 0, k = 0, kr = 0, kc = 0;
   long long gk = 0;
   bool todo = false, flagged = false;
   if (in) {
-    f = (int)(j / nk);
-    k = p.kr0 * p.ns_c + (int)(j % nk);
+    f = blockIdx.y;
+    k = p.kr0 * p.ns_c + j;
     gk = (long long)f * K + k;
     kr = k / p.ns_c;
     kc = k % p.ns_c;
@@ -628,130 +628,121 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
   if (flagged) p.worklist[atomicAdd(p.worklist_n, 1)] = (int32_t)gk;
 }
 
-// Exact recomputation of flagged clusters (certificate failed): one warp per
-// cluster, latency-oriented (a handful of clusters per frame are flagged, so
-// this kernel's duration is one cluster's latency).  The 3Sx3S window is
-// walked in blocks of kRows rows with the next block's label loads in flight
-// while the current one is folded.  Per row, lanes own columns; matches are
-// compacted in row-major order into shared memory (ballot + popc), x / y /
-// count are reduced per row with REDUX.  Lanes 0..2 then fold the three
-// colour channels in exactly the reference's order (_core.pyx:233-243), each
-// strip from 0.0, and lane 0 applies the pairwise strip tree
-// (_core.pyx:300-311).  Pipeline labels never spill, so the window holds
-// every member.
+// Exact recomputation of flagged clusters (certificate failed).  One block
+// per cluster; its warps take the cluster's row strips (strip j = rows
+// [ry0 + j*tile_len, ...) of the 3S x 3S window), each strip being an
+// independent reference fold that starts from 0.0 (_core.pyx:233-243), so a
+// cluster's latency is one strip's, not the whole window's.  A strip is
+// walked in blocks of kRows rows with the next block's label loads in flight;
+// per row, lanes own columns, matches are compacted in row-major order into
+// shared memory (ballot + popc) with cp.async value copies, x / y / count are
+// reduced per row with REDUX, and lanes 0..2 fold the three colour channels
+// in order.  Thread 0 applies the pairwise strip tree (_core.pyx:300-311).
+// Pipeline labels never spill, so the window holds every member.
 constexpr int kRows = 8;
 constexpr int kCols = 96;  // window width 3S <= 96 (S <= 32)
-constexpr int kExWarps = 2;
+#ifndef SPX_EXW
+#define SPX_EXW 3
+#endif
+#ifndef SPX_EXG
+#define SPX_EXG 16
+#endif
+constexpr int kExWarps = SPX_EXW;  // 3 = n_bl for the default tile_len 16 (3S / 16 strips when S = 16)
 
 __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p) {
-  __shared__ double strips[kExWarps][32][6];
+  __shared__ double strips[32][6];
   __shared__ float cv[kExWarps][3][kRows * kCols];  // compacted l / a / b
   __shared__ int rstart[kExWarps][kRows + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.ns_r * p.ns_c;
   const int n = *p.worklist_n;
-  const int nwarps = gridDim.x * kExWarps;
-  double (*sk)[6] = strips[warp];
   const long long hw = (long long)p.h * p.w;
   const unsigned lt = (1u << lane) - 1u;
-  for (int item = blockIdx.x * kExWarps + warp; item < n; item += nwarps) {
+  for (int item = blockIdx.x; item < n; item += gridDim.x) {
     const int gk = p.worklist[item];
     const int ff = gk / K, fk = gk - ff * K;
     const float* im = p.img + (long long)ff * 3 * hw;  // planar [3][H][W]
     const int32_t* lb = p.labels + (long long)ff * hw;
     const int r = fk / p.ns_c, c = fk - r * p.ns_c;
+    const int gid = fk + p.row_off * p.ns_c;  // labels carry global ids
     const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
     const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
-    const int ya = max(ry0, 0);
     const int ww = wx1 - wx0;
     const int ncb = (ww + 31) >> 5;  // column blocks of 32 (<= 3)
-    if (lane < p.n_bl)
-      for (int comp = 0; comp < 6; ++comp) sk[lane][comp] = 0.0;
-    int cur_j = -1, fold_j = -1;
-    double acc = 0.0;
-    long long sx = 0, sy = 0, cnt = 0;  // lane 0: running strip totals
-    int32_t nxt[kRows][3];
-    auto load_block = [&](int yb, int32_t (&lv)[kRows][3]) {
+    for (int i = threadIdx.x; i < p.n_bl * 6; i += blockDim.x) (&strips[0][0])[i] = 0.0;
+    __syncthreads();
+    for (int j = warp; j < p.n_bl; j += kExWarps) {
+      const int ya = max(ry0 + j * p.tile_len, 0);
+      const int yz = min(ry0 + (j + 1) * p.tile_len, ry1);
+      if (ya >= yz) continue;  // warp-uniform
+      double acc = 0.0;
+      long long sx = 0, sy = 0, cnt = 0;  // lane 0
+      int32_t nxt[kRows][3];
+      auto load_block = [&](int yb, int32_t (&lv)[kRows][3]) {
 #pragma unroll
-      for (int rr = 0; rr < kRows; ++rr)
+        for (int rr = 0; rr < kRows; ++rr)
 #pragma unroll
-        for (int cb = 0; cb < 3; ++cb) {
-          const int col = cb * 32 + lane;
-          lv[rr][cb] = (yb + rr < ry1 && col < ww)
-                           ? __ldg(lb + (long long)(yb + rr) * p.w + wx0 + col)
-                           : -1;
-        }
-    };
-    load_block(ya, nxt);
-    for (int yb = ya; yb < ry1; yb += kRows) {
-      int32_t lv[kRows][3];
-#pragma unroll
-      for (int rr = 0; rr < kRows; ++rr)
-#pragma unroll
-        for (int cb = 0; cb < 3; ++cb) lv[rr][cb] = nxt[rr][cb];
-      if (yb + kRows < ry1) load_block(yb + kRows, nxt);  // prefetch the next block
-      const int rows = min(kRows, ry1 - yb);
-      int base = 0;
-#pragma unroll
-      for (int rr = 0; rr < kRows; ++rr) {
-        if (rr >= rows) break;
-        const int y = yb + rr;
-        if (lane == 0) rstart[warp][rr] = base;
-        int rx = 0, rn = 0;
-#pragma unroll
-        for (int cb = 0; cb < 3; ++cb) {
-          if (cb >= ncb) break;
-          const int col = cb * 32 + lane;
-          const bool m = lv[rr][cb] == fk + p.row_off * p.ns_c;  // global ids
-          const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
-          if (m) {
-            // asynchronous global -> shared copies: all of the block's value
-            // loads are in flight together (one DRAM round trip per block)
-            const int pos = base + __popc(bm & lt);
-            const float* g = im + (long long)y * p.w + wx0 + col;
-            const unsigned d0 = (unsigned)__cvta_generic_to_shared(&cv[warp][0][pos]);
-            const unsigned d1 = (unsigned)__cvta_generic_to_shared(&cv[warp][1][pos]);
-            const unsigned d2 = (unsigned)__cvta_generic_to_shared(&cv[warp][2][pos]);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d0), "l"(g));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d1), "l"(g + hw));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d2), "l"(g + 2 * hw));
+          for (int cb = 0; cb < 3; ++cb) {
+            const int col = cb * 32 + lane;
+            lv[rr][cb] = (yb + rr < yz && col < ww)
+                             ? __ldg(lb + (long long)(yb + rr) * p.w + wx0 + col)
+                             : -1;
           }
-          rx += (int)__reduce_add_sync(0xFFFFFFFFu, m ? (unsigned)(wx0 + col) : 0u);
-          rn += __popc(bm);
-          base += __popc(bm);
-        }
-        if (lane == 0 && rn) {
-          const int j = (y - ry0) / p.tile_len;
-          if (j != cur_j && cur_j >= 0) {
-            sk[cur_j][3] = (double)sx;
-            sk[cur_j][4] = (double)sy;
-            sk[cur_j][5] = (double)cnt;
-            sx = sy = cnt = 0;
+      };
+      load_block(ya, nxt);
+      for (int yb = ya; yb < yz; yb += kRows) {
+        int32_t lv[kRows][3];
+#pragma unroll
+        for (int rr = 0; rr < kRows; ++rr)
+#pragma unroll
+          for (int cb = 0; cb < 3; ++cb) lv[rr][cb] = nxt[rr][cb];
+        if (yb + kRows < yz) load_block(yb + kRows, nxt);  // prefetch the next block
+        const int rows = min(kRows, yz - yb);
+        int base = 0;
+#pragma unroll
+        for (int rr = 0; rr < kRows; ++rr) {
+          if (rr >= rows) break;
+          const int y = yb + rr;
+          if (lane == 0) rstart[warp][rr] = base;
+          int rx = 0, rn = 0;
+#pragma unroll
+          for (int cb = 0; cb < 3; ++cb) {
+            if (cb >= ncb) break;
+            const int col = cb * 32 + lane;
+            const bool m = lv[rr][cb] == gid;
+            const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
+            if (m) {
+              // asynchronous global -> shared copies: the block's value loads
+              // are all in flight together (one round trip per block)
+              const int pos = base + __popc(bm & lt);
+              const float* g = im + (long long)y * p.w + wx0 + col;
+              const unsigned d0 = (unsigned)__cvta_generic_to_shared(&cv[warp][0][pos]);
+              const unsigned d1 = (unsigned)__cvta_generic_to_shared(&cv[warp][1][pos]);
+              const unsigned d2 = (unsigned)__cvta_generic_to_shared(&cv[warp][2][pos]);
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d0), "l"(g));
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d1), "l"(g + hw));
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d2), "l"(g + 2 * hw));
+            }
+            rx += (int)__reduce_add_sync(0xFFFFFFFFu, m ? (unsigned)(wx0 + col) : 0u);
+            rn += __popc(bm);
+            base += __popc(bm);
           }
-          if (j != cur_j) cur_j = j;  // lanes 1, 2 track cur_j below
-          sx += rx;
-          sy += (long long)(y + p.row_off * p.s) * rn;
-          cnt += rn;
-        }
-      }
-      if (lane == 0) rstart[warp][rows] = base;
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncwarp();
-      if (lane < 3) {
-        // fold this block's rows in order; strips change only at row boundaries
-        for (int rr = 0; rr < rows; ++rr) {
-          const int b0 = rstart[warp][rr], b1 = rstart[warp][rr + 1];
-          if (b0 == b1) continue;
-          const int j = (yb + rr - ry0) / p.tile_len;
-          if (j != fold_j) {
-            if (fold_j >= 0) sk[fold_j][lane] = acc;
-            fold_j = j;
-            acc = 0.0;
+          if (lane == 0) {
+            sx += rx;
+            sy += (long long)(y + p.row_off * p.s) * rn;
+            cnt += rn;
           }
+        }
+        if (lane == 0) rstart[warp][rows] = base;
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        if (lane < 3) {
+          // row-major order within the strip; channel 0 carries the
+          // certified-sum flag in its sign bit: |L|
           const float* src = cv[warp][lane];
-          int i = b0;
-          // channel 0 carries the certified-sum flag in its sign bit: |L|
+          const int b1 = rstart[warp][rows];
           const bool l0 = lane == 0;
+          int i = 0;
           for (; i + 4 <= b1; i += 4) {
             float v0 = src[i], v1 = src[i + 1], v2 = src[i + 2], v3 = src[i + 3];
             if (l0) {
@@ -767,29 +758,31 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
           }
           for (; i < b1; ++i) acc = dadd(acc, (double)(l0 ? fabsf(src[i]) : src[i]));
         }
+        __syncwarp();
       }
-      __syncwarp();
+      if (lane < 3) strips[j][lane] = acc;
+      if (lane == 0) {
+        strips[j][3] = (double)sx;
+        strips[j][4] = (double)sy;
+        strips[j][5] = (double)cnt;
+      }
     }
-    if (lane < 3 && fold_j >= 0) sk[fold_j][lane] = acc;
-    if (lane == 0 && cur_j >= 0) {
-      sk[cur_j][3] = (double)sx;
-      sk[cur_j][4] = (double)sy;
-      sk[cur_j][5] = (double)cnt;
-    }
-    __syncwarp();
-    if (lane == 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
       int m = p.n_bl;
       while (m > 1) {  // pairwise strip tree, _core.pyx:300-311
         int half = m >> 1;
         for (int i = 0; i < half; ++i)
-          for (int comp = 0; comp < 6; ++comp) sk[i][comp] = dadd(sk[2 * i][comp], sk[2 * i + 1][comp]);
+          for (int comp = 0; comp < 6; ++comp)
+            strips[i][comp] = dadd(strips[2 * i][comp], strips[2 * i + 1][comp]);
         if (m & 1)
-          for (int comp = 0; comp < 6; ++comp) sk[half][comp] = sk[m - 1][comp];
+          for (int comp = 0; comp < 6; ++comp) strips[half][comp] = strips[m - 1][comp];
         m = half + (m & 1);
       }
-      write_centre(p, gk, r, c, sk[0][5], sk[0][0], sk[0][1], sk[0][2], sk[0][3], sk[0][4]);
+      write_centre(p, gk, r, c, strips[0][5], strips[0][0], strips[0][1], strips[0][2],
+                   strips[0][3], strips[0][4]);
     }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
@@ -912,12 +905,16 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   p.kr0 = (int)kr0;
   p.kr1 = (int)kr1;
   p.row_off = (int)row_off;
-  long long n = (kr1 - kr0) * ns_c * (long long)frames;
+  const long long nk = (kr1 - kr0) * ns_c;
   SPX_CUDA(cudaMemsetAsync(worklist_n, 0, sizeof(int32_t), st));
-  if (n <= 0) return SPX_OK;
-  k_reduce_cells<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(p);
+  if (nk <= 0 || frames <= 0) return SPX_OK;
+  if (frames > 65535) {
+    set_error("k_reduce_cells: at most 65535 frames per launch");
+    return SPX_ERR_VALUE;
+  }
+  k_reduce_cells<<<dim3((unsigned)ceil_div(nk, 128), (unsigned)frames), 128, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_reduce_cells");
-  k_exact_clusters<<<(unsigned)num_sms() * 16, kExWarps * 32, 0, st>>>(p);
+  k_exact_clusters<<<(unsigned)num_sms() * SPX_EXG, kExWarps * 32, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_exact_clusters");
   return SPX_OK;
 }

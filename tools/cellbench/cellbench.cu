@@ -74,6 +74,9 @@ int main(int argc, char** argv) {
                            counts, rec, nullptr, wl, wl + B * K, H, W, S, ns_r, ns_c, 16, B, s, 0,
                            -1, 0));
     cur ^= 1;
+    int nflag = 0;
+    CC(cudaMemcpy(&nflag, wl + B * K, 4, cudaMemcpyDeviceToHost));
+    printf("pass %d: %d of %lld clusters flagged for the exact fallback\n", it, nflag, B * K);
   }
   CC(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
