@@ -294,25 +294,29 @@ struct Engine {
     return SPX_OK;
   }
 
-  // ---- host-buffer entry point: chunked, double-buffered, three streams -------
+  // ---- host-buffer entry point: chunked, triple-buffered, three streams -------
   // H2D of chunk c+1 and D2H of chunk c-1 overlap the compute of chunk c
   // (copy engines run both directions concurrently with the SMs).  Host
   // buffers must be pinned for the copies to be asynchronous; pageable
   // buffers still give correct results, serialised.
   int64_t chunk = 0, chunk_req = 64;
-  uint8_t* h_rgb[2] = {nullptr, nullptr};
-  int32_t* h_lab[2] = {nullptr, nullptr};
-  double* h_xy[2] = {nullptr, nullptr};
-  double* h_cl[2] = {nullptr, nullptr};
-  int64_t* h_cnt[2] = {nullptr, nullptr};
-  int32_t* h_pass[2] = {nullptr, nullptr};
+  // Three staging slots: the compute of chunk c reuses chunk c-3's slot, so
+  // it never waits for the previous chunk's download (which, sharing PCIe
+  // with the next upload, is the longest of the three stages).
+  static constexpr int kSlots = 3;
+  uint8_t* h_rgb[kSlots] = {};
+  int32_t* h_lab[kSlots] = {};
+  double* h_xy[kSlots] = {};
+  double* h_cl[kSlots] = {};
+  int64_t* h_cnt[kSlots] = {};
+  int32_t* h_pass[kSlots] = {};
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
-  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+  cudaEvent_t ev_h2d[kSlots] = {}, ev_comp[kSlots] = {}, ev_d2h[kSlots] = {};
 
   int ensure_staging() {
     if (s_comp) return SPX_OK;
     chunk = std::max<int64_t>(1, std::min<int64_t>(max_batch, chunk_req));
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
       SPX_CUDA(cudaMalloc(&h_rgb[i], chunk * hw * 3));
       SPX_CUDA(cudaMalloc(&h_lab[i], chunk * hw * sizeof(int32_t)));
       SPX_CUDA(cudaMalloc(&h_xy[i], chunk * K * 2 * sizeof(double)));
@@ -330,7 +334,7 @@ struct Engine {
   }
 
   void free_staging() {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
       for (void* q : {(void*)h_rgb[i], (void*)h_lab[i], (void*)h_xy[i], (void*)h_cl[i],
                       (void*)h_cnt[i], (void*)h_pass[i]})
         if (q) cudaFree(q);
@@ -387,16 +391,16 @@ struct Engine {
       tl.push_back(e);
     };
     for (int64_t c = 0; c < nchunks; ++c, ++seq) {
-      const int sl = (int)(seq & 1);
+      const int sl = (int)(seq % kSlots);
       const int64_t f0 = c * chunk, nb = std::min(chunk, batch - f0);
-      if (seq >= 2) SPX_CUDA(cudaStreamWaitEvent(s_h2d, ev_comp[sl], 0));
+      if (seq >= kSlots) SPX_CUDA(cudaStreamWaitEvent(s_h2d, ev_comp[sl], 0));
       mark(s_h2d);
       SPX_CUDA(cudaMemcpyAsync(h_rgb[sl], rgb + f0 * hw * 3, nb * hw * 3, cudaMemcpyHostToDevice,
                                s_h2d));
       mark(s_h2d);
       SPX_CUDA(cudaEventRecord(ev_h2d[sl], s_h2d));
       SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_h2d[sl], 0));
-      if (seq >= 2) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
+      if (seq >= kSlots) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
       mark(s_comp);
       if ((rc = segment(h_rgb[sl], nb, h_lab[sl], h_xy[sl], h_cl[sl], h_cnt[sl], h_pass[sl],
                         s_comp)))
