@@ -75,7 +75,6 @@ struct CellParams {
   int h, w, s, ns_r, ns_c, frames;
   int cr0, cr1;            // cell rows processed (local grid)
   int row_off;             // global cell row of local row 0 (strips; 0 otherwise)
-  int pairs_per_warp;      // consecutive cell pairs walked by one warp
   int runs_per_row;        // S / 4
   int runs;                // S * S / 4
   unsigned row_magic;      // ceil(2^16 / runs_per_row)
@@ -104,75 +103,60 @@ __device__ __noinline__ int exact_argmin(const double* __restrict__ cxy, const d
   return best_k;
 }
 
-// Shared-memory layout per warp.
-//   cand[2][9]:   fp32 candidate l, a, b, x (cell relative); the packed
-//                 FADD2/FFMA2 ops take them as broadcast scalar operands
-//   cy[2][9]:     candidate y (cell relative)
-//   cand_k[2][9]: cluster id of each candidate slot
-//   acc (ACC):    lane-private per-slot accumulators, lane-interleaved so
-//                 any per-lane slot choice is bank-conflict free:
-//                 accd[9][3][kCS] double, acci[9][kCS] uint64 (packed
-//                 count | flags<<11 | sum_x<<22 | sum_y<<43).
-// The whole per-warp block stays <= 10496 B so 16 warps fit the 164 KB
+// Shared-memory layout per warp (CPW = 32 / LPC cells per warp).
+//   cand[CPW][9]:   fp32 candidate l, a, b, x (cell relative); the packed
+//                   FADD2/FFMA2 ops take them as broadcast scalar operands
+//   cy[CPW][9]:     candidate y (cell relative)
+//   cand_k[CPW][9]: cluster id of each candidate slot
+//   acc (ACC):      lane-private per-slot accumulators, lane-interleaved so
+//                   any per-lane slot choice is bank-conflict free:
+//                   accd[9][3][32] double, acci[9][32] uint64 (packed
+//                   count | flags<<11 | sum_x<<22 | sum_y<<43).
+// With LPC >= 8 the per-warp block is <= 10 KB, so 16 warps fit the 164 KB
 // shared-memory carve-out and leave 92 KB of L1 for the Lab stream.
 constexpr int kWarps = 4;
-constexpr int kPairsPerWarp = 4;
-#ifndef SPX_TREE
-#define SPX_TREE 0  // tree (1) or chained (0) epilogue column sums
-#endif
+constexpr int kGroupsPerWarp = 4;  // consecutive cell groups walked by one warp
 #ifndef SPX_MINB
 #define SPX_MINB 4  // resident blocks per SM the register budget is sized for
 #endif
-#ifndef SPX_ACC_MODE
-#define SPX_ACC_MODE 0  // development timing knob: 1 = skip per-pixel sums, 2 = skip epilogue
-#endif
-#ifndef SPX_LEAD
-#define SPX_LEAD 0  // combine same-slot pixels of a run before the smem update
-#endif
-#ifndef SPX_XPF
-#define SPX_XPF 0   // load the next pair's records / first run during this pair
-#endif
-constexpr size_t kCandBytes = 18 * 16 + 18 * 4 + 18 * 4;  // cand, cy, cand_k
-#ifndef SPX_ACC_STRIDE
-#define SPX_ACC_STRIDE 32
-#endif
-// Accumulator column stride (entries).  With 32, every column starts on
-// bank 0, so the per-pixel updates (lane l touches entry l of the column of
-// its slot) are conflict-free whatever slots the lanes pick; the epilogue,
-// where lane l sums column l, starts each lane at a different 16-byte
-// offset ((q + l) & 7) so its reads do not all hit the same banks.
-constexpr int kCS = SPX_ACC_STRIDE;
-constexpr size_t kAccBytes = 9 * 3 * kCS * sizeof(double) + 9 * kCS * sizeof(uint64_t);
-constexpr size_t kWarpSmemAcc = kCandBytes + kAccBytes;
-constexpr size_t kWarpSmemNoAcc = kCandBytes;
+__host__ __device__ constexpr size_t cand_bytes(int lpc) { return (size_t)(32 / lpc) * 9 * 24; }
+// Accumulator columns start on bank 0 (stride 32 entries), so the per-pixel
+// updates (lane l touches entry l of its slot's column) are conflict-free
+// whatever slots the lanes pick; in the epilogue, where a lane sums a whole
+// column of its cell, each lane starts at a rotated 16-byte offset so the
+// lanes' reads spread over the banks.
+constexpr size_t kAccBytes = 9 * 3 * 32 * sizeof(double) + 9 * 32 * sizeof(uint64_t);
+__host__ __device__ constexpr size_t warp_smem(int lpc, bool acc) {
+  return cand_bytes(lpc) + (acc ? kAccBytes : 0);
+}
 
-constexpr int kLpc = 16;  // lanes per cell: two cells per warp, 9 staging lanes per cell
-
-// One warp walks `pairs_per_warp` consecutive cell pairs of one frame.  The
-// next pair's candidate records and first Lab run are loaded while the current
-// pair finishes (its last runs and its epilogue), so the per-cell load
-// latency is hidden behind work instead of exposed at every cell start.
-template <bool ACC>
+// Work unit: a group of CPW = 32 / LPC cells of one frame; a warp walks
+// kGroupsPerWarp consecutive groups.  Each cell's LPC lanes stage its 9
+// candidates in shared memory, then stream the cell's pixels in runs of 4
+// (one 128-bit load per planar channel); LPC = 16 for S >= 16, LPC = 4 for
+// small cells (S = 8, 12) so each lane still gets several runs per cell.
+template <bool ACC, int LPC>
 __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
+  constexpr int CPW = 32 / LPC;
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ci = lane / kLpc, ll = lane % kLpc;  // cell within warp, lane within cell
+  const int ci = lane / LPC, ll = lane % LPC;  // cell within warp, lane within cell
   const int S = p.s;
   const int K = p.ns_r * p.ns_c;
   const int f = blockIdx.y;
   if (p.done && p.done[f] == 1) return;  // whole block: one frame
   const int n_cells = (p.cr1 - p.cr0) * p.ns_c;
-  const int pair_begin = (blockIdx.x * kWarps + warp) * p.pairs_per_warp;
-  const int pair_end = min(pair_begin + p.pairs_per_warp, (n_cells + 1) >> 1);
-  if (pair_begin >= pair_end) return;  // whole warp
+  const int g_begin = (blockIdx.x * kWarps + warp) * kGroupsPerWarp;
+  const int g_end = min(g_begin + kGroupsPerWarp, (n_cells + CPW - 1) / CPW);
+  if (g_begin >= g_end) return;  // whole warp
 
-  unsigned char* wbase = smem + (size_t)warp * (ACC ? kWarpSmemAcc : kWarpSmemNoAcc);
+  unsigned char* wbase = smem + (size_t)warp * warp_smem(LPC, ACC);
   float4* cand = reinterpret_cast<float4*>(wbase) + ci * 9;
-  float* cyv = reinterpret_cast<float*>(wbase + 18 * 16) + ci * 9;
-  int* cand_k = reinterpret_cast<int*>(wbase + 18 * 16 + 18 * 4) + ci * 9;
-  double* accd = reinterpret_cast<double*>(wbase + kCandBytes);
+  float* cyv = reinterpret_cast<float*>(wbase + CPW * 9 * 16) + ci * 9;
+  int* cand_k = reinterpret_cast<int*>(wbase + CPW * 9 * 20) + ci * 9;
+  double* accd = reinterpret_cast<double*>(wbase + cand_bytes(LPC));
   unsigned long long* acci =
-      reinterpret_cast<unsigned long long*>(wbase + kCandBytes + 9 * 3 * kCS * sizeof(double));
+      reinterpret_cast<unsigned long long*>(wbase + cand_bytes(LPC) + 9 * 3 * 32 * sizeof(double));
 
   const long long hw = (long long)p.h * p.w;
   const float* fimg = p.img + (long long)f * 3 * hw;
@@ -184,25 +168,6 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
     row = (int)(((unsigned)jj * rmag) >> 16);
     c4 = (jj - row * p.runs_per_row) * 4;
   };
-  // geometry of a cell (local grid): row, column; valid if inside [cr0, cr1)
-  auto cell_rc = [&](int pair, int& cr, int& cc) {
-    const int cell = p.cr0 * p.ns_c + pair * 2 + ci;
-    const bool ok = pair * 2 + ci < n_cells;
-    cr = ok ? cell / p.ns_c : 0;
-    cc = ok ? cell - cr * p.ns_c : 0;
-    return ok;
-  };
-  // loads of one cell's staging record (lanes ll < 9) and a lane's first run
-  auto load_rec = [&](bool act, int cr, int cc, float4& v0, float4& v1) {
-    const int kr = cr + off_r(ll), kc = cc + off_c(ll);
-    if (act && ll < 9 && kr >= 0 && kr < p.ns_r && kc >= 0 && kc < p.ns_c) {
-      const float4* q = reinterpret_cast<const float4*>(frec + kr * p.ns_c + kc);
-      v0 = __ldg(q);
-      v1 = __ldg(q + 1);
-    }
-  };
-  int row0, c40;
-  run_pos(ll, row0, c40);
   auto load_run = [&](bool ok, int y, int x, float4& Lx, float4& Ax, float4& Bx) {
     if (ok) {
       const float* q = fimg + (long long)y * p.w + x;
@@ -211,44 +176,53 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
       Bx = __ldg(reinterpret_cast<const float4*>(q + 2 * hw));
     }
   };
+  int row0, c40;
+  run_pos(ll, row0, c40);
 
-  // prefetch for the first pair
-  int cr_n, cc_n;
-  bool act_n = cell_rc(pair_begin, cr_n, cc_n);
-  float4 rv0 = make_float4(0.f, 0.f, 0.f, 0.f), rv1 = rv0;
-  load_rec(act_n, cr_n, cc_n, rv0, rv1);
-  bool ok_n = act_n && ll < p.runs && cr_n * S + row0 < p.h && cc_n * S + c40 < p.w;
-  int row_n = row0, c4_n = c40;
-  float4 Ln = make_float4(0.f, 0.f, 0.f, 0.f), An = Ln, Bn = Ln;
-  load_run(ok_n, cr_n * S + row0, cc_n * S + c40, Ln, An, Bn);
+  for (int grp = g_begin; grp < g_end; ++grp) {
+    // ---- geometry (local grid) -----------------------------------------------
+    const int cell = p.cr0 * p.ns_c + grp * CPW + ci;
+    const bool active = grp * CPW + ci < n_cells;
+    const int cr = active ? cell / p.ns_c : 0;
+    const int cc = active ? cell - cr * p.ns_c : 0;
+    const int x_cell = cc * S, y_cell = cr * S;  // local pixel origin
+    const int y_glob0 = (cr + p.row_off) * S;    // global y of the cell's row 0
+    // first run of this lane (its latency overlaps the staging below)
+    bool ok_n = active && ll < p.runs && y_cell + row0 < p.h && x_cell + c40 < p.w;
+    int row_n = row0, c4_n = c40;
+    float4 Ln = make_float4(0.f, 0.f, 0.f, 0.f), An = Ln, Bn = Ln;
+    load_run(ok_n, y_cell + row0, x_cell + c40, Ln, An, Bn);
 
-  for (int pair = pair_begin; pair < pair_end; ++pair) {
-    const bool active = act_n;
-    const int cr = cr_n, cc = cc_n;
-    // ---- stage the 9 candidates (lanes ll < 9 of each cell) ----------------
+    // ---- stage the 9 candidates (the cell's lanes, 9 / LPC each) --------------
     float mc = 0.f, mxy = 0.f, okf = 1.f;
-    if (active && ll < 9) {
-      const int t = ll;
-      const int kr = cr + off_r(t), kc = cc + off_c(t);
-      float4 cp;
-      float cyt = 0.f;
-      if (kr >= 0 && kr < p.ns_r && kc >= 0 && kc < p.ns_c) {
-        const float cxt = __fadd_rn(rv0.w, (float)(off_c(t) * S));
-        cyt = __fadd_rn(rv1.x, (float)(off_r(t) * S));
-        cp = make_float4(rv0.x, rv0.y, rv0.z, cxt);
-        mc = rv1.y;
-        mxy = fmaxf(fabsf(cxt), fabsf(cyt));
-        okf = rv1.w;
-      } else {
-        // Out of the grid: colour 1e18 away makes D ~1e18, never the argmin.
-        cp = make_float4(1e18f, 0.f, 0.f, 0.f);
-      }
-      cand[t] = cp;
-      cyv[t] = cyt;
-      cand_k[t] = kr * p.ns_c + kc;  // only read for in-grid winners
-    }
 #pragma unroll
-    for (int o = 8; o; o >>= 1) {
+    for (int t0 = 0; t0 < 9; t0 += LPC) {
+      const int t = t0 + ll;
+      if (active && t < 9) {
+        const int kr = cr + off_r(t), kc = cc + off_c(t);
+        float4 cp;
+        float cyt = 0.f;
+        if (kr >= 0 && kr < p.ns_r && kc >= 0 && kc < p.ns_c) {
+          const float4* q = reinterpret_cast<const float4*>(frec + kr * p.ns_c + kc);
+          const float4 v0 = __ldg(q), v1 = __ldg(q + 1);
+          const float cxt = __fadd_rn(v0.w, (float)(off_c(t) * S));
+          cyt = __fadd_rn(v1.x, (float)(off_r(t) * S));
+          cp = make_float4(v0.x, v0.y, v0.z, cxt);
+          mc = fmaxf(mc, v1.y);
+          mxy = fmaxf(mxy, fmaxf(fabsf(cxt), fabsf(cyt)));
+          okf = fminf(okf, v1.w);
+        } else {
+          // Out of the grid: colour 1e18 away makes D ~1e18, never the argmin.
+          cp = make_float4(1e18f, 0.f, 0.f, 0.f);
+        }
+        cand[t] = cp;
+        cyv[t] = cyt;
+        cand_k[t] = kr * p.ns_c + kc;  // only read for in-grid winners
+      }
+    }
+    // cell-wide maxima over the cell's lanes (xor butterfly inside the group)
+#pragma unroll
+    for (int o = LPC / 2; o; o >>= 1) {
       mc = fmaxf(mc, __shfl_xor_sync(0xFFFFFFFFu, mc, o));
       mxy = fmaxf(mxy, __shfl_xor_sync(0xFFFFFFFFu, mxy, o));
       okf = fminf(okf, __shfl_xor_sync(0xFFFFFFFFu, okf, o));
@@ -264,28 +238,16 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
     float two_a_cell =
         __fmaf_rn(mc, p.k_mc, __fmaf_rn(__fmaf_rn(3.f, mxy, 2.f * S), p.k_xy, p.k_const));
     if (okf == 0.f) two_a_cell = INFINITY;
-    const int x_cell = cc * S, y_cell = cr * S;  // local pixel origin
-    const int y_glob0 = (cr + p.row_off) * S;    // global y of the cell's row 0
 
-    // the next pair's geometry and staging records (loaded during this pair)
-    const bool has_next = pair + 1 < pair_end;
-    act_n = has_next && cell_rc(pair + 1, cr_n, cc_n);
-    if (SPX_XPF) load_rec(act_n, cr_n, cc_n, rv0, rv1);
-
-    for (int j = ll; j < p.runs; j += kLpc) {
+    for (int j = ll; j < p.runs; j += LPC) {
       const int row = row_n, c4 = c4_n;
       const bool ok = ok_n;
       const float4 Lv = Ln, Av = An, Bv = Bn;
-      // prefetch the lane's next run: this cell's, else the next pair's first
-      if (j + kLpc < p.runs) {
-        run_pos(j + kLpc, row_n, c4_n);
+      // prefetch the lane's next run of this cell (software pipelining)
+      if (j + LPC < p.runs) {
+        run_pos(j + LPC, row_n, c4_n);
         ok_n = active && y_cell + row_n < p.h && x_cell + c4_n < p.w;
         load_run(ok_n, y_cell + row_n, x_cell + c4_n, Ln, An, Bn);
-      } else if (SPX_XPF) {
-        row_n = row0;
-        c4_n = c40;
-        ok_n = act_n && cr_n * S + row0 < p.h && cc_n * S + c40 < p.w;
-        load_run(ok_n, cr_n * S + row0, cc_n * S + c40, Ln, An, Bn);
       }
       if (!ok) continue;
       const int y = y_cell + row, x = x_cell + c4;
@@ -314,22 +276,21 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
         const float dyf = __fsub_rn(cyv[t], yr);
         const float dyyf = __fmul_rn(dyf, dyf);
         const unsigned long long dyy = f2_pack(dyyf, dyyf);
-        struct {
-          unsigned long long l, a, b, x;
-        } c = {f2_pack(cv.x, cv.x), f2_pack(cv.y, cv.y), f2_pack(cv.z, cv.z), f2_pack(cv.w, cv.w)};
+        const unsigned long long cl = f2_pack(cv.x, cv.x), ca = f2_pack(cv.y, cv.y),
+                                 cb = f2_pack(cv.z, cv.z), cx = f2_pack(cv.w, cv.w);
         float Q[4], R[4];
         {
-          unsigned long long dl = sub2(c.l, L01), da = sub2(c.a, A01), db = sub2(c.b, B01);
+          unsigned long long dl = sub2(cl, L01), da = sub2(ca, A01), db = sub2(cb, B01);
           unsigned long long q = fma2(db, db, fma2(da, da, mul2(dl, dl)));
-          unsigned long long dx = sub2(c.x, X01);
+          unsigned long long dx = sub2(cx, X01);
           unsigned long long r = fma2(dx, dx, dyy);
           f2_unpack(q, Q[0], Q[1]);
           f2_unpack(r, R[0], R[1]);
         }
         {
-          unsigned long long dl = sub2(c.l, L23), da = sub2(c.a, A23), db = sub2(c.b, B23);
+          unsigned long long dl = sub2(cl, L23), da = sub2(ca, A23), db = sub2(cb, B23);
           unsigned long long q = fma2(db, db, fma2(da, da, mul2(dl, dl)));
-          unsigned long long dx = sub2(c.x, X23);
+          unsigned long long dx = sub2(cx, X23);
           unsigned long long r = fma2(dx, dx, dyy);
           f2_unpack(q, Q[2], Q[3]);
           f2_unpack(r, R[2], R[3]);
@@ -373,124 +334,54 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
       int lab4[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) lab4[i] = cand_k[t[i]] + p.row_off * p.ns_c;  // GLOBAL ids
-      if (ACC && SPX_ACC_MODE != 1 && !SPX_LEAD) {
+      if (ACC) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          double* d = accd + t[i] * (3 * kCS) + lane;
+          double* d = accd + t[i] * 96 + lane;
           d[0] = dadd(d[0], (double)L[i]);
-          d[kCS] = dadd(d[kCS], (double)A[i]);
-          d[2 * kCS] = dadd(d[2 * kCS], (double)B[i]);
-          acci[t[i] * kCS + lane] += 1ull | ((unsigned long long)((fl4 >> i) & 1u) << 11) |
-                                     ((unsigned long long)(c4 + i) << 22) |
-                                     ((unsigned long long)row << 43);
-        }
-      }
-      if (ACC && SPX_ACC_MODE != 1 && SPX_LEAD) {
-        // Pixels of the run that share a slot are summed in registers first
-        // and only the first of them (the leader) updates the slot's
-        // accumulator, so the four read-modify-writes touch distinct entries
-        // and overlap instead of chaining through shared memory.  (Any
-        // summation order is exact under the certified-sum condition.)
-        const bool e01 = t[1] == t[0], e02 = t[2] == t[0], e03 = t[3] == t[0];
-        const bool e12 = t[2] == t[1], e13 = t[3] == t[1], e23 = t[3] == t[2];
-        const bool lead[4] = {true, !e01, !e02 && !e12, !e03 && !e13 && !e23};
-        unsigned long long pk[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          pk[i] = 1ull | ((unsigned long long)((fl4 >> i) & 1u) << 11) |
-                  ((unsigned long long)(c4 + i) << 22) | ((unsigned long long)row << 43);
-        double g[4][3];
-        unsigned long long gi[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          g[i][0] = (double)L[i];
-          g[i][1] = (double)A[i];
-          g[i][2] = (double)B[i];
-          gi[i] = pk[i];
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if (e01) g[0][c] = dadd(g[0][c], g[1][c]);
-          if (e02) g[0][c] = dadd(g[0][c], g[2][c]);
-          if (e03) g[0][c] = dadd(g[0][c], g[3][c]);
-          if (e12) g[1][c] = dadd(g[1][c], g[2][c]);
-          if (e13) g[1][c] = dadd(g[1][c], g[3][c]);
-          if (e23) g[2][c] = dadd(g[2][c], g[3][c]);
-        }
-        if (e01) gi[0] += pk[1];
-        if (e02) gi[0] += pk[2];
-        if (e03) gi[0] += pk[3];
-        if (e12) gi[1] += pk[2];
-        if (e13) gi[1] += pk[3];
-        if (e23) gi[2] += pk[3];
-        double old[4][3];
-        unsigned long long oldi[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const double* d = accd + t[i] * (3 * kCS) + lane;
-          old[i][0] = d[0];
-          old[i][1] = d[kCS];
-          old[i][2] = d[2 * kCS];
-          oldi[i] = acci[t[i] * kCS + lane];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (lead[i]) {
-            double* d = accd + t[i] * (3 * kCS) + lane;
-            d[0] = dadd(old[i][0], g[i][0]);
-            d[kCS] = dadd(old[i][1], g[i][1]);
-            d[2 * kCS] = dadd(old[i][2], g[i][2]);
-            acci[t[i] * kCS + lane] = oldi[i] + gi[i];
-          }
+          d[32] = dadd(d[32], (double)A[i]);
+          d[64] = dadd(d[64], (double)B[i]);
+          acci[t[i] * 32 + lane] += 1ull | ((unsigned long long)((fl4 >> i) & 1u) << 11) |
+                                    ((unsigned long long)(c4 + i) << 22) |
+                                    ((unsigned long long)row << 43);
         }
       }
       *reinterpret_cast<int4*>(p.labels + pix) = make_int4(lab4[0], lab4[1], lab4[2], lab4[3]);
     }
-    if (ACC && SPX_ACC_MODE != 2) {
+    if (ACC) {
       __syncwarp();
       // ---- per-cell column reduction: 9 slots x (3 colour + 1 packed int) ---
       // column c < 27: colour (slot c/3, channel c%3); 27 <= c < 36: ints of
-      // slot c-27.  The 16 lane entries of a column are summed as a tree (any
-      // order is exact under the certified-sum condition; flagged clusters
-      // are recomputed by k_exact_clusters) and go straight into the owning
-      // cluster's accumulator with global atomics.
-      const int lane0 = ci * kLpc;
+      // slot c-27.  The LPC lane entries of a column are summed in a
+      // lane-rotated order (any order is exact under the certified-sum
+      // condition; flagged clusters are recomputed by k_exact_clusters) and
+      // go straight into the owning cluster's accumulator with global atomics.
+      constexpr int NQ = LPC / 2;  // 16-byte pairs per column
+      const int lane0 = ci * LPC;
       if (active) {
         ClusterAcc* fa = p.acc + (long long)f * K;
-#pragma unroll
-        for (int u = 0; u < 3; ++u) {
-          const int col = ll + u * kLpc;
+        for (int col = ll; col < 36; col += LPC) {
           if (col < 27) {
-            const double2* src = reinterpret_cast<const double2*>(accd + col * kCS + lane0);
-#if SPX_TREE
-            double s4[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const double2 v = src[(q + ll) & 7], w2 = src[(q + 4 + ll) & 7];
-              s4[q] = dadd(dadd(v.x, v.y), dadd(w2.x, w2.y));
-            }
-            const double sacc = dadd(dadd(s4[0], s4[1]), dadd(s4[2], s4[3]));
-#else
+            const double2* src = reinterpret_cast<const double2*>(accd + col * 32 + lane0);
             double sacc = 0.0;
-            for (int q = 0; q < 8; ++q) {
-              const double2 v = src[(q + ll) & 7];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              const double2 v = src[(q + ll) & (NQ - 1)];
               sacc = dadd(dadd(sacc, v.x), v.y);
             }
-#endif
             // an empty (or out-of-grid) slot sums to +0.0: nothing to add
-            if (SPX_ACC_MODE == 3 ? sacc == 1.2345e300 : sacc != 0.0)
-              atomicAdd(&fa[cand_k[col / 3]].s[col % 3], sacc);
-          } else if (col < 36) {
+            if (sacc != 0.0) atomicAdd(&fa[cand_k[col / 3]].s[col % 3], sacc);
+          } else {
             const ulonglong2* src =
-                reinterpret_cast<const ulonglong2*>(acci + (col - 27) * kCS + lane0);
+                reinterpret_cast<const ulonglong2*>(acci + (col - 27) * 32 + lane0);
             unsigned long long tot = 0;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const ulonglong2 v = src[(q + ll) & 7];
+            for (int q = 0; q < NQ; ++q) {
+              const ulonglong2 v = src[(q + ll) & (NQ - 1)];
               tot += v.x + v.y;  // fields cannot overflow (see packing above)
             }
             const unsigned long long cnt = tot & 2047ull;
-            if (SPX_ACC_MODE == 3 ? cnt == 2047 : cnt != 0) {
+            if (cnt) {
               ClusterAcc* o = fa + cand_k[col - 27];
               const unsigned long long flg = (tot >> 11) & 2047ull;
               atomicAdd(&o->sx, ((tot >> 22) & 0x1FFFFFull) + cnt * (unsigned long long)x_cell);
@@ -501,14 +392,7 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
         }
       }
     }
-    __syncwarp();  // smem (candidates, accumulators) is rewritten by the next pair
-    if (!SPX_XPF) {
-      load_rec(act_n, cr_n, cc_n, rv0, rv1);
-      row_n = row0;
-      c4_n = c40;
-      ok_n = act_n && cr_n * S + row0 < p.h && cc_n * S + c40 < p.w;
-      load_run(ok_n, cr_n * S + row0, cc_n * S + c40, Ln, An, Bn);
-    }
+    __syncwarp();  // smem (candidates, accumulators) is rewritten by the next group
   }
 }
 
@@ -801,9 +685,29 @@ bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
          h * w * 3 < (int64_t)1 << 40 && h < (1 << 30) && w < (1 << 30);
 }
 
-size_t cell_smem_bytes(int64_t s, bool acc) {
-  (void)s;
-  return (size_t)kWarps * (acc ? kWarpSmemAcc : kWarpSmemNoAcc);
+// Lanes per cell, measured on one B200 (tools/cellbench, random frames):
+// 4 for S <= 12 (S = 8: 0.61 vs 0.95 ms per fused pass with 16 lanes), 8 for
+// 16 <= S <= 24 (S = 16: 0.60 vs 0.64 ms), 16 for S >= 28.  Fewer lanes per
+// cell give each lane more runs over which to amortise the per-cell staging
+// and epilogue; too few leave too many cells in flight per warp.
+static int cell_lpc(int64_t s) {
+  static const int env = getenv("SPX_LPC") ? atoi(getenv("SPX_LPC")) : 0;  // development
+  if (env == 4 || env == 8 || env == 16) return env;
+  return s <= 12 ? 4 : (s <= 24 ? 8 : 16);
+}
+
+size_t cell_smem_bytes(int64_t s, bool acc) { return (size_t)kWarps * warp_smem(cell_lpc(s), acc); }
+
+template <bool ACC, int LPC>
+static int launch_cell_t(const CellParams& p, dim3 blocks, size_t smem, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    SPX_CUDA(cudaFuncSetAttribute(k_cell<ACC, LPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kWarps * warp_smem(LPC, true))));
+    configured = true;
+  }
+  k_cell<ACC, LPC><<<blocks, 128, smem, st>>>(p);
+  return SPX_OK;
 }
 
 void assoc_bound_coefficients(double xy_weight, float& w32, float& k_mp, float& k_mc, float& k_xy,
@@ -834,29 +738,26 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.runs = (int)(s * s / 4);
   p.runs_per_row = (int)(s / 4);
   p.row_magic = (unsigned)((65536 + p.runs_per_row - 1) / p.runs_per_row);
-  static const int ppw_env = getenv("SPX_PPW") ? atoi(getenv("SPX_PPW")) : kPairsPerWarp;
-  p.pairs_per_warp = ppw_env;
   p.xy_weight = xy_weight;
   assoc_bound_coefficients(xy_weight, p.w32, p.k_mp, p.k_mc, p.k_xy, p.k_const, p.k_rel);
   if (cr1 <= cr0) return SPX_OK;
-  const long long warps = ceil_div(ceil_div((cr1 - cr0) * ns_c, 2), p.pairs_per_warp);
+  const int lpc = cell_lpc(s);
+  const long long warps = ceil_div(ceil_div((cr1 - cr0) * ns_c, 32 / lpc), kGroupsPerWarp);
   const dim3 blocks((unsigned)ceil_div(warps, kWarps), (unsigned)frames);
   if (frames > 65535) {
     set_error("k_cell: at most 65535 frames per launch");
     return SPX_ERR_VALUE;
   }
   const size_t smem = cell_smem_bytes(s, acc);
-  if (acc) {
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      SPX_CUDA(cudaFuncSetAttribute(k_cell<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-      configured = smem;
-    }
-    k_cell<true><<<blocks, 128, smem, st>>>(p);
-  } else {
-    k_cell<false><<<blocks, 128, smem, st>>>(p);
-  }
+  int rc;
+  if (lpc == 4)
+    rc = acc ? launch_cell_t<true, 4>(p, blocks, smem, st) : launch_cell_t<false, 4>(p, blocks, smem, st);
+  else if (lpc == 8)
+    rc = acc ? launch_cell_t<true, 8>(p, blocks, smem, st) : launch_cell_t<false, 8>(p, blocks, smem, st);
+  else
+    rc = acc ? launch_cell_t<true, 16>(p, blocks, smem, st)
+             : launch_cell_t<false, 16>(p, blocks, smem, st);
+  if (rc) return rc;
   SPX_LAUNCH_CHECK("k_cell");
   return SPX_OK;
 }
