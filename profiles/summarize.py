@@ -105,7 +105,7 @@ def report(rep, out, traffic_json=None, pixels=None):
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if traffic_json and pixels:
-        assoc = [v for k, vs in traffic.items() if "k_cell<1>" in k or "k_cell<true>" in k for v in vs]
+        assoc = [v for k, vs in traffic.items() if "k_cell<1" in k or "k_cell<true" in k for v in vs]
         if assoc:
             json.dump({"kernel": "k_cell<ACC> (association + centre-update pass)",
                        "dram_bytes_per_pixel": sum(assoc) / len(assoc) / float(pixels),
