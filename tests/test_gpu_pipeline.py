@@ -270,3 +270,21 @@ def test_submit_host_pipeline_across_batches():
             assert got.tobytes() == ref.tobytes()
     with pytest.raises(ValueError):
         eng.submit_host(batches[1], *outs[0])
+
+
+@pytest.mark.parametrize("w,h,kw", [
+    (1920, 1080, dict(num_superpixels=8000)),              # C3 frame
+    (3840, 2160, dict(spixel_size=8, no_iters=10)),        # C4 frame
+])
+def test_large_baseline_frames_bitexact(w, h, kw):
+    """BASELINE C3 / C4 frames (reference generator, seed 0) equal the oracle."""
+    st = spx.Settings(img_width=w, img_height=h, **kw)
+    g = spx.compute_grid(st)
+    rgb = np.random.default_rng(0).integers(0, 256, (h, w, 3), dtype=np.uint8)
+    res = spx.SegEngine(st).perform_segmentation(spx.ImageRGB(rgb))
+    labels, cxy, clab, counts, _ = oracle.segment(rgb, g.s, g.ns_r, g.ns_c, st.compactness,
+                                                  no_iters=st.no_iters)
+    assert np.array_equal(res.labels.data, labels)
+    assert res.spixel_map.centers_xy.tobytes() == cxy.tobytes()
+    assert res.spixel_map.centers_lab.tobytes() == clab.tobytes()
+    assert np.array_equal(res.spixel_map.num_pixels, counts)
