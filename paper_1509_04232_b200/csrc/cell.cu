@@ -22,6 +22,7 @@
 // reference's fold, its strip tree, and our fixed-order sum all equal the
 // exact sum.  Pixels outside that range set a flag bit; the reduce kernel
 // recomputes flagged clusters with the reference's exact strip fold.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -77,6 +78,7 @@ struct CellParams {
   int row_off;             // global cell row of local row 0 (strips; 0 otherwise)
   int runs_per_row;        // S / 4
   int runs;                // S * S / 4
+  int groups_per_warp;     // cell groups walked by one warp
   unsigned row_magic;      // ceil(2^16 / runs_per_row)
   double xy_weight;
   float w32, k_mp, k_mc, k_xy, k_const, k_rel;
@@ -115,7 +117,7 @@ __device__ __noinline__ int exact_argmin(const double* __restrict__ cxy, const d
 // With LPC >= 8 the per-warp block is <= 10 KB, so 16 warps fit the 164 KB
 // shared-memory carve-out and leave 92 KB of L1 for the Lab stream.
 constexpr int kWarps = 4;
-constexpr int kGroupsPerWarp = 4;  // consecutive cell groups walked by one warp
+constexpr int kGroupsPerWarp = 4;  // max consecutive cell groups walked by one warp
 #ifndef SPX_MINB
 #define SPX_MINB 4  // resident blocks per SM the register budget is sized for
 #endif
@@ -131,7 +133,8 @@ __host__ __device__ constexpr size_t warp_smem(int lpc, bool acc) {
 }
 
 // Work unit: a group of CPW = 32 / LPC cells of one frame; a warp walks
-// kGroupsPerWarp consecutive groups.  Each cell's LPC lanes stage its 9
+// up to kGroupsPerWarp consecutive groups (fewer when the launch would not
+// fill the GPU).  Each cell's LPC lanes stage its 9
 // candidates in shared memory, then stream the cell's pixels in runs of 4
 // (one 128-bit load per planar channel); LPC = 16 for S >= 16, LPC = 4 for
 // small cells (S = 8, 12) so each lane still gets several runs per cell.
@@ -146,8 +149,8 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
   const int f = blockIdx.y;
   if (p.done && p.done[f] == 1) return;  // whole block: one frame
   const int n_cells = (p.cr1 - p.cr0) * p.ns_c;
-  const int g_begin = (blockIdx.x * kWarps + warp) * kGroupsPerWarp;
-  const int g_end = min(g_begin + kGroupsPerWarp, (n_cells + CPW - 1) / CPW);
+  const int g_begin = (blockIdx.x * kWarps + warp) * p.groups_per_warp;
+  const int g_end = min(g_begin + p.groups_per_warp, (n_cells + CPW - 1) / CPW);
   if (g_begin >= g_end) return;  // whole warp
 
   unsigned char* wbase = smem + (size_t)warp * warp_smem(LPC, ACC);
@@ -742,7 +745,12 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   assoc_bound_coefficients(xy_weight, p.w32, p.k_mp, p.k_mc, p.k_xy, p.k_const, p.k_rel);
   if (cr1 <= cr0) return SPX_OK;
   const int lpc = cell_lpc(s);
-  const long long warps = ceil_div(ceil_div((cr1 - cr0) * ns_c, 32 / lpc), kGroupsPerWarp);
+  // Walk up to kGroupsPerWarp groups per warp, but keep >= 16 warps per SM
+  // in flight for small launches (one 640x480 frame has only 300 groups).
+  const long long groups = ceil_div((cr1 - cr0) * ns_c, 32 / lpc) * (long long)frames;
+  p.groups_per_warp = (int)std::max<long long>(
+      1, std::min<long long>(kGroupsPerWarp, groups / ((long long)num_sms() * 16)));
+  const long long warps = ceil_div(ceil_div((cr1 - cr0) * ns_c, 32 / lpc), p.groups_per_warp);
   const dim3 blocks((unsigned)ceil_div(warps, kWarps), (unsigned)frames);
   if (frames > 65535) {
     set_error("k_cell: at most 65535 frames per launch");
@@ -815,7 +823,11 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   }
   k_reduce_cells<<<dim3((unsigned)ceil_div(nk, 128), (unsigned)frames), 128, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_reduce_cells");
-  k_exact_clusters<<<(unsigned)num_sms() * SPX_EXG, kExWarps * 32, 0, st>>>(p);
+  // grid-stride over the worklist; ~0.5% of clusters are flagged, so small
+  // launches get a small grid (an empty block still costs its scheduling)
+  const long long ex_blocks = std::max<long long>(
+      num_sms(), std::min<long long>((long long)num_sms() * SPX_EXG, nk * frames / 64));
+  k_exact_clusters<<<(unsigned)ex_blocks, kExWarps * 32, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_exact_clusters");
   return SPX_OK;
 }
