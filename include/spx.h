@@ -170,6 +170,10 @@ SPX_API int32_t spx_engine_submit_host(spx_engine *eng, const uint8_t *rgb_host,
                                int32_t *labels_host, double *cxy_host, double *clab_host,
                                int64_t *counts_host, int32_t *passes_host);
 SPX_API int32_t spx_engine_wait(spx_engine *eng);
+/* Ticket of the work submitted so far (read it after a submit) and a wait for
+ * that submission only, so a caller can consume batch i while i+1 runs. */
+SPX_API int64_t spx_engine_ticket(spx_engine *eng);
+SPX_API int32_t spx_engine_wait_ticket(spx_engine *eng, int64_t ticket);
 /* Frames per host-pipeline chunk (default 64, capped at max_batch); waits for
  * submitted work and re-allocates the staging buffers. */
 SPX_API int32_t spx_engine_set_host_chunk(spx_engine *eng, int64_t frames);

@@ -66,6 +66,8 @@ SIGNATURES = {
     "spx_engine_segment_host": (I32, [P, P, I64, P, P, P, P, P]),
     "spx_engine_submit_host": (I32, [P, P, I64, P, P, P, P, P]),
     "spx_engine_wait": (I32, [P]),
+    "spx_engine_ticket": (I64, [P]),
+    "spx_engine_wait_ticket": (I32, [P, I64]),
     "spx_engine_set_host_chunk": (I32, [P, I64]),
     "spx_engine_timing": (I32, [P, ctypes.POINTER(SpxTiming)]),
     "spx_engine_last_launches": (I64, [P]),

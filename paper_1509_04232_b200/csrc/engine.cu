@@ -541,6 +541,20 @@ struct Engine {
     return SPX_OK;
   }
 
+  // Wait for the submissions up to `ticket` (a value of `seq` after a submit).
+  // A slot's event may since have been re-recorded by a later chunk; waiting
+  // on it is still correct (the D2H stream is in order), only later.
+  int wait_ticket(int64_t ticket) {
+    SPX_CUDA(cudaSetDevice(device));
+    if (ticket <= 0 || !s_d2h) return SPX_OK;
+    if (ticket > seq) {
+      set_error("ticket %lld was never issued", (long long)ticket);
+      return SPX_ERR_VALUE;
+    }
+    SPX_CUDA(cudaEventSynchronize(ev_d2h[(ticket - 1) % kSlots]));
+    return SPX_OK;
+  }
+
   int wait_host() {
     SPX_CUDA(cudaSetDevice(device));
     if (!s_d2h) return SPX_OK;
@@ -638,6 +652,12 @@ int32_t spx_engine_submit_host(spx_engine* eng, const uint8_t* rgb_host, int64_t
 }
 
 int32_t spx_engine_wait(spx_engine* eng) { return eng->e.wait_host(); }
+
+int64_t spx_engine_ticket(spx_engine* eng) { return eng->e.seq; }
+
+int32_t spx_engine_wait_ticket(spx_engine* eng, int64_t ticket) {
+  return eng->e.wait_ticket(ticket);
+}
 
 int32_t spx_engine_set_host_chunk(spx_engine* eng, int64_t frames) {
   return eng->e.set_host_chunk(frames);

@@ -214,6 +214,11 @@ class SegEngine:
         p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
         _lib.check(self._lib.spx_engine_submit_host(self._h, p(rgb), b, p(labels), p(cxy),
                                                     p(clab), p(counts), p(passes)), "submit")
+        return int(self._lib.spx_engine_ticket(self._h))
+
+    def wait_ticket(self, ticket):
+        """Wait for the submission that returned `ticket` (and all before it)."""
+        _lib.check(self._lib.spx_engine_wait_ticket(self._h, int(ticket)), "wait_ticket")
 
     def set_host_chunk(self, frames):
         """Frames per H2D/compute/D2H pipeline chunk of the host-buffer path."""
@@ -287,22 +292,66 @@ def perform_segmentation(engine, img):
 def segment_stream(engine, imgs):
     """Yield one SegResult per frame, batching up to engine.max_batch frames.
 
-    A frame of the wrong size aborts the stream with DimensionMismatchError
-    naming its index, after the results of the frames before it.
+    Batches go through the engine's host pipeline with two pinned buffer sets:
+    batch i+1 is uploaded and segmented while batch i's results are returned,
+    so the copies overlap the GPU work (engine.py:238-249 runs the batches one
+    after another).  A frame of the wrong size aborts the stream with
+    DimensionMismatchError naming its index, after the results of the frames
+    before it.
     """
-    pending = []
-    start = 0
-    for i, img in enumerate(imgs):
-        try:
-            engine._check_frame(img)
-        except DimensionMismatchError as exc:
-            if pending:
-                yield from engine.perform_segmentation_batch(pending)
-            raise DimensionMismatchError(f"frame {i}: {exc}") from None
-        pending.append(img)
-        if len(pending) == engine.max_batch:
-            yield from engine.perform_segmentation_batch(pending)
-            start += len(pending)
-            pending = []
-    if pending:
-        yield from engine.perform_segmentation_batch(pending)
+    import collections
+    torch = engine._torch
+    st, k, mb = engine.settings, engine.grid.num_clusters, engine.max_batch
+    h, w = st.img_height, st.img_width
+
+    def pinned(shape, dt):
+        return torch.empty(shape, dtype=dt).pin_memory().numpy()
+
+    sets = [None, None]
+    inflight = collections.deque()
+
+    def submit(frames, slot):
+        if sets[slot] is None:
+            sets[slot] = (pinned((mb, h, w, 3), torch.uint8), pinned((mb, h, w), torch.int32),
+                          pinned((mb, k, 2), torch.float64), pinned((mb, k, 3), torch.float64),
+                          pinned((mb, k), torch.int64), pinned((mb,), torch.int32))
+        bufs = sets[slot]
+        n = len(frames)
+        for j, img in enumerate(frames):
+            bufs[0][j] = img.data
+        ticket = engine.submit_host(*(b[:n] for b in bufs))
+        inflight.append((ticket, slot, n))
+
+    def drain_one():
+        ticket, slot, n = inflight.popleft()
+        engine.wait_ticket(ticket)
+        bufs = sets[slot]
+        # copies: the pinned set is reused by the next-but-one batch
+        return engine._results(*(b[:n].copy() for b in bufs[1:]), engine.last_timing())
+
+    pending, slot = [], 0
+    try:
+        for i, img in enumerate(imgs):
+            try:
+                engine._check_frame(img)
+            except DimensionMismatchError as exc:
+                if pending:
+                    submit(pending, slot)
+                while inflight:
+                    yield from drain_one()
+                raise DimensionMismatchError(f"frame {i}: {exc}") from None
+            pending.append(img)
+            if len(pending) == mb:
+                if len(inflight) == 2:
+                    yield from drain_one()
+                submit(pending, slot)
+                slot ^= 1
+                pending = []
+        if pending:
+            if len(inflight) == 2:
+                yield from drain_one()
+            submit(pending, slot)
+        while inflight:
+            yield from drain_one()
+    finally:
+        engine.wait()

@@ -316,3 +316,54 @@ def test_graph_replay_matches_eager_and_times():
                                                   st.compactness)
     assert np.array_equal(out[0][2].cpu().numpy(), labels)
     assert out[2][2].cpu().numpy().tobytes() == clab.tobytes()
+
+
+class TestStream:
+    """segment_stream (reference test_engine.py:140-176) plus pipelined batches."""
+
+    def settings(self):
+        return spx.Settings(img_width=16, img_height=16, num_superpixels=4)
+
+    def test_matches_independent_calls(self):
+        rng = np.random.default_rng(58)
+        a = spx.ImageRGB(rng.integers(0, 256, (16, 16, 3), dtype=np.uint8))
+        b = spx.ImageRGB(rng.integers(0, 256, (16, 16, 3), dtype=np.uint8))
+        streamed = list(spx.segment_stream(spx.SegEngine(self.settings()), [a, b, a]))
+        assert len(streamed) == 3
+        assert np.array_equal(streamed[0].labels.data, streamed[2].labels.data)
+        solo = spx.SegEngine(self.settings()).perform_segmentation(b)
+        assert np.array_equal(streamed[1].labels.data, solo.labels.data)
+
+    def test_results_survive_later_frames(self):
+        rng = np.random.default_rng(59)
+        frames = [spx.ImageRGB(rng.integers(0, 256, (16, 16, 3), dtype=np.uint8))
+                  for _ in range(7)]
+        eng = spx.SegEngine(self.settings(), max_batch=2)
+        kept = [r.labels.data for r in spx.segment_stream(eng, frames)]
+        redo = [spx.SegEngine(self.settings()).perform_segmentation(f).labels.data
+                for f in frames]
+        assert all(np.array_equal(x, y) for x, y in zip(kept, redo))
+
+    def test_empty_stream(self):
+        assert list(spx.segment_stream(spx.SegEngine(self.settings()), [])) == []
+
+    def test_mismatched_frame_names_index(self):
+        eng = spx.SegEngine(self.settings(), max_batch=2)
+        ok = spx.ImageRGB(np.full((16, 16, 3), 9, np.uint8))
+        bad = spx.ImageRGB(np.zeros((16, 8, 3), np.uint8))
+        got = []
+        with pytest.raises(spx.DimensionMismatchError, match="frame 3"):
+            for r in spx.segment_stream(eng, [ok, ok, ok, bad]):
+                got.append(r)
+        assert len(got) == 3  # results of the frames before the bad one
+
+    def test_pipelined_batches_match_oracle(self):
+        st = spx.Settings(img_width=64, img_height=48, spixel_size=8)
+        g = spx.compute_grid(st)
+        rng = np.random.default_rng(60)
+        frames = [rng.integers(0, 256, (48, 64, 3), dtype=np.uint8) for _ in range(11)]
+        eng = spx.SegEngine(st, max_batch=3)
+        for f, r in zip(frames, spx.segment_stream(eng, [spx.ImageRGB(x) for x in frames])):
+            labels, cxy, clab, counts, _ = oracle.segment(f, g.s, g.ns_r, g.ns_c, st.compactness)
+            assert np.array_equal(r.labels.data, labels)
+            assert r.spixel_map.centers_lab.tobytes() == clab.tobytes()
