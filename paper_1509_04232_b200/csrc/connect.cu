@@ -65,79 +65,101 @@ __global__ void __launch_bounds__(WTW* WTH) k_weak1(const int32_t* __restrict__ 
   dst[y * w + x] = weak_rule(t, w, h, x, y, P, threadIdx.x + 1, threadIdx.y + 1);
 }
 
-// Both passes fused; frames of a batch along blockIdx.z.  Output tile
-// WT2W x WT2H per CTA of 256 threads; the source tile (2-pixel halo) is
-// loaded with 16-byte loads for the aligned interior, pass 1 is evaluated on
-// the tile plus a 1-pixel halo in shared memory, pass 2 on the tile, and the
-// result leaves as 16-byte stores.  32-bit indexing (frames < 2^31 px).
-constexpr int WT2W = 128, WT2H = 16;
-
-__device__ __forceinline__ int32_t weak_rule_g(const int32_t* t, int pitch, int lx, int ly, int x,
-                                               int y, int w, int h) {
-  const int32_t v = t[ly * pitch + lx];
-  const int32_t left = t[ly * pitch + lx - 1], right = t[ly * pitch + lx + 1];
-  const int32_t up = t[(ly - 1) * pitch + lx], down = t[(ly + 1) * pitch + lx];
-  const bool hl = x > 0, hr = x < w - 1, hu = y > 0, hd = y < h - 1;
-  if ((hl && left == v) || (hr && right == v) || (hu && up == v) || (hd && down == v)) return v;
-  return hl ? left : (hu ? up : v);
-}
-
+// Both passes fused; frames of a batch along blockIdx.z.  32-bit indexing
+// (frames < 2^31 px).
 // Output rows [y0, y1) of a buffer of h rows (row strips pass their halo
 // rows in the buffer and only their own rows as the output range; image
 // edges coincide with buffer edges, interior strip edges have >= 2 halo rows).
+//
+// Work unit: a group of 4 horizontally adjacent pixels.  The source tile
+// (WG x HG outputs, 8-column / 2-row halo) is staged as int4 groups; pass 1
+// is evaluated group-wise on the tile plus a 4-column / 1-row halo into a
+// second int4 tile, pass 2 group-wise on the output tile.  A group reads its
+// own, the upper and the lower int4 and one word on each side: 5 shared
+// loads per 4 pixels per pass.
+constexpr int WG = 128, HG = 32;
+constexpr int NG0 = WG / 4 + 4, R0G = HG + 4;  // source groups: cols [x0-8, x0+WG+8)
+constexpr int NG1 = WG / 4 + 2, R1G = HG + 2;  // pass-1 groups: cols [x0-4, x0+WG+4)
+
+// Pixels outside the image hold kOut in the tiles, a value no pipeline label
+// takes (labels are cluster ids >= 0), so "neighbour in bounds and equal"
+// is a plain comparison and "in bounds" is `!= kOut`.
+constexpr int kOut = INT_MIN;
+
+__device__ __forceinline__ int4 weak_rule4(int4 v, int4 up, int4 dn, int lft, int rgt) {
+  const int vv[4] = {v.x, v.y, v.z, v.w};
+  const int uu[4] = {up.x, up.y, up.z, up.w};
+  const int dd[4] = {dn.x, dn.y, dn.z, dn.w};
+  int o[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int L = k == 0 ? lft : vv[k - 1];
+    const int R = k == 3 ? rgt : vv[k + 1];
+    const int c = vv[k];
+    const bool keep = (L == c) | (R == c) | (uu[k] == c) | (dd[k] == c);
+    o[k] = keep ? c : (L != kOut ? L : (uu[k] != kOut ? uu[k] : c));
+  }
+  return make_int4(o[0], o[1], o[2], o[3]);
+}
+
 __global__ void __launch_bounds__(256) k_weak2(const int32_t* __restrict__ src,
                                                int32_t* __restrict__ dst, int h, int w, int y0,
                                                int y1) {
-  constexpr int P0 = WT2W + 8, R0 = WT2H + 4;  // source tile: 4-col / 2-row halo
-  constexpr int P1 = WT2W + 2, R1 = WT2H + 2;  // pass-1 tile: 1-px halo
-  __shared__ __align__(16) int32_t t0[R0 * P0];
-  __shared__ int32_t t1[R1 * P1];
+  __shared__ int4 t0[R0G][NG0];
+  __shared__ int4 t1[R1G][NG1];
   const long long fo = (long long)blockIdx.z * h * w;
   const int32_t* s = src + fo;
   int32_t* d = dst + fo;
-  const int tx0 = blockIdx.x * WT2W, ty0 = y0 + blockIdx.y * WT2H;
+  const int tx0 = blockIdx.x * WG, ty0 = y0 + blockIdx.y * HG;
   const int tid = threadIdx.x;
   const bool vec = (w & 3) == 0;
-  // load: tile columns [tx0-4, tx0+WT2W+4), rows [ty0-2, ty0+WT2H+2)
-  for (int i = tid; i < R0 * (P0 / 4); i += 256) {
-    const int ly = i / (P0 / 4), lq = i % (P0 / 4);
-    const int y = ty0 + ly - 2, x = tx0 - 4 + lq * 4;
-    int4 v = make_int4(0, 0, 0, 0);
+  for (int i = tid; i < R0G * NG0; i += 256) {
+    const int r = i / NG0, g = i - r * NG0;
+    const int y = ty0 - 2 + r, x = tx0 - 8 + 4 * g;
+    int4 v = make_int4(kOut, kOut, kOut, kOut);
     if (y >= 0 && y < h) {
+      const int32_t* row = s + (long long)y * w;
       if (vec && x >= 0 && x + 4 <= w) {
-        v = __ldg(reinterpret_cast<const int4*>(s + (long long)y * w + x));
+        v = __ldg(reinterpret_cast<const int4*>(row + x));
       } else {
-        const int32_t* row = s + (long long)y * w;
-        v.x = (x >= 0 && x < w) ? __ldg(row + x) : 0;
-        v.y = (x + 1 >= 0 && x + 1 < w) ? __ldg(row + x + 1) : 0;
-        v.z = (x + 2 >= 0 && x + 2 < w) ? __ldg(row + x + 2) : 0;
-        v.w = (x + 3 >= 0 && x + 3 < w) ? __ldg(row + x + 3) : 0;
+        v.x = (x >= 0 && x < w) ? __ldg(row + x) : kOut;
+        v.y = (x + 1 >= 0 && x + 1 < w) ? __ldg(row + x + 1) : kOut;
+        v.z = (x + 2 >= 0 && x + 2 < w) ? __ldg(row + x + 2) : kOut;
+        v.w = (x + 3 >= 0 && x + 3 < w) ? __ldg(row + x + 3) : kOut;
       }
     }
-    *reinterpret_cast<int4*>(t0 + ly * P0 + lq * 4) = v;
+    t0[r][g] = v;
   }
   __syncthreads();
-  for (int i = tid; i < R1 * P1; i += 256) {
-    const int ly = i / P1, lx = i % P1;
-    const int y = ty0 + ly - 1, x = tx0 + lx - 1;
-    t1[i] = (y >= 0 && y < h && x >= 0 && x < w) ? weak_rule_g(t0, P0, lx + 3, ly + 1, x, y, w, h) : 0;
+  // pass 1 on rows [ty0-1, ty0+HG+1), cols [tx0-4, tx0+WG+4)
+  for (int i = tid; i < R1G * NG1; i += 256) {
+    const int r = i / NG1, g = i - r * NG1;
+    int4 o = weak_rule4(t0[r + 1][g + 1], t0[r][g + 1], t0[r + 2][g + 1], t0[r + 1][g].w,
+                        t0[r + 1][g + 2].x);
+    // out-of-image positions stay kOut for pass 2 (the rule keeps c = kOut:
+    // its in-image neighbours never equal kOut, its left / up may be kOut)
+    const int4 c = t0[r + 1][g + 1];
+    o.x = c.x == kOut ? kOut : o.x;
+    o.y = c.y == kOut ? kOut : o.y;
+    o.z = c.z == kOut ? kOut : o.z;
+    o.w = c.w == kOut ? kOut : o.w;
+    t1[r][g] = o;
   }
   __syncthreads();
-  // pass 2: each thread writes 4 consecutive pixels of one row (x2 rows)
-  for (int i = tid; i < WT2H * (WT2W / 4); i += 256) {
-    const int ly = i / (WT2W / 4), lq = i % (WT2W / 4);
-    const int y = ty0 + ly, x = tx0 + lq * 4;
-    if (y >= y1) continue;
-    int o[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      o[k] = (x + k < w) ? weak_rule_g(t1, P1, lq * 4 + k + 1, ly + 1, x + k, y, w, h) : 0;
+  // pass 2 on the output tile
+  for (int i = tid; i < HG * (WG / 4); i += 256) {
+    const int r = i / (WG / 4), g = i - r * (WG / 4);
+    const int y = ty0 + r, x = tx0 + 4 * g;
+    if (y >= y1 || x >= w) continue;
+    const int4 o = weak_rule4(t1[r + 1][g + 1], t1[r][g + 1], t1[r + 2][g + 1], t1[r + 1][g].w,
+                              t1[r + 1][g + 2].x);
     int32_t* out = d + (long long)y * w + x;
-    if (vec && x + 4 <= w) {
-      *reinterpret_cast<int4*>(out) = make_int4(o[0], o[1], o[2], o[3]);
+    if (vec) {
+      *reinterpret_cast<int4*>(out) = o;
     } else {
+      const int oo[4] = {o.x, o.y, o.z, o.w};
       for (int k = 0; k < 4; ++k)
-        if (x + k < w) out[k] = o[k];
+        if (x + k < w) out[k] = oo[k];
     }
   }
 }
@@ -263,7 +285,7 @@ int launch_weak2(const int32_t* src, int32_t* dst, int64_t h, int64_t w, int fra
     set_error("weak: frame too large for the fused kernel");
     return SPX_ERR_VALUE;
   }
-  dim3 grid((unsigned)ceil_div(w, WT2W), (unsigned)ceil_div(y1 - y0, WT2H), (unsigned)frames);
+  dim3 grid((unsigned)ceil_div(w, WG), (unsigned)ceil_div(y1 - y0, HG), (unsigned)frames);
   k_weak2<<<grid, 256, 0, st>>>(src, dst, (int)h, (int)w, (int)y0, (int)y1);
   SPX_LAUNCH_CHECK("k_weak2");
   return SPX_OK;
