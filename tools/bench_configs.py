@@ -15,6 +15,9 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# eager engine calls: every stage event is live (graph replays of small
+# batches report the first call's stage breakdown)
+os.environ.setdefault("SPX_NO_GRAPHS", "1")
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
