@@ -291,7 +291,7 @@ def test_large_baseline_frames_bitexact(w, h, kw):
 
 
 def test_graph_replay_matches_eager_and_times():
-    """Calls 1 (eager), 2 (captured) and 3+ (replayed CUDA graph) with the same
+    """Calls 1-2 (eager), 3 (captured) and 4+ (replayed CUDA graph) with the same
     buffers give identical results; stage timings stay readable."""
     import torch
     st = spx.Settings(img_width=64, img_height=48, spixel_size=8)
@@ -300,7 +300,7 @@ def test_graph_replay_matches_eager_and_times():
                                                              dtype=np.uint8)).cuda()
     out = eng.allocate_outputs(3)
     ref = None
-    for call in range(4):
+    for call in range(5):
         for t in out:
             t.zero_()
         eng.segment_device(rgb, out)
