@@ -76,8 +76,8 @@ struct CellParams {
   int h, w, s, ns_r, ns_c, frames;
   int cr0, cr1;            // cell rows processed (local grid)
   int row_off;             // global cell row of local row 0 (strips; 0 otherwise)
-  int runs_per_row;        // S / 4
-  int runs;                // S * S / 4
+  int runs_per_row;        // ceil(S / 4)
+  int runs;                // S * runs_per_row
   int groups_per_warp;     // cell groups walked by one warp
   unsigned row_magic;      // ceil(2^16 / runs_per_row)
   double xy_weight;
@@ -138,7 +138,12 @@ __host__ __device__ constexpr size_t warp_smem(int lpc, bool acc) {
 // candidates in shared memory, then stream the cell's pixels in runs of 4
 // (one 128-bit load per planar channel); LPC = 16 for S >= 16, LPC = 4 for
 // small cells (S = 8, 12) so each lane still gets several runs per cell.
-template <bool ACC, int LPC>
+// AL: every run is 4 whole pixels at a 16-byte aligned address (S % 4 == 0
+// and W % 4 == 0): 128-bit loads and stores.  Otherwise a cell row ends in a
+// partial run (S % 4 pixels) and runs may start anywhere: the run's pixels
+// are loaded and stored one by one and the pixels past the cell (or image)
+// edge are masked out of the labels, the certificate and the sums.
+template <bool ACC, int LPC, bool AL>
 __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
   constexpr int CPW = 32 / LPC;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -171,12 +176,27 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
     row = (int)(((unsigned)jj * rmag) >> 16);
     c4 = (jj - row * p.runs_per_row) * 4;
   };
-  auto load_run = [&](bool ok, int y, int x, float4& Lx, float4& Ax, float4& Bx) {
-    if (ok) {
-      const float* q = fimg + (long long)y * p.w + x;
+  // valid pixels of the run starting at cell column c4, image column x
+  auto run_len = [&](int c4, int x) { return AL ? 4 : min(4, min(S - c4, p.w - x)); };
+  auto load_run = [&](bool ok, int y, int x, int nv, float4& Lx, float4& Ax, float4& Bx) {
+    if (!ok) return;
+    const float* q = fimg + (long long)y * p.w + x;
+    if (AL) {
       Lx = __ldg(reinterpret_cast<const float4*>(q));
       Ax = __ldg(reinterpret_cast<const float4*>(q + hw));
       Bx = __ldg(reinterpret_cast<const float4*>(q + 2 * hw));
+    } else {
+      float l[4] = {0.f, 0.f, 0.f, 0.f}, a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < nv) {
+          l[i] = __ldg(q + i);
+          a[i] = __ldg(q + hw + i);
+          b[i] = __ldg(q + 2 * hw + i);
+        }
+      Lx = make_float4(l[0], l[1], l[2], l[3]);
+      Ax = make_float4(a[0], a[1], a[2], a[3]);
+      Bx = make_float4(b[0], b[1], b[2], b[3]);
     }
   };
   int row0, c40;
@@ -194,7 +214,7 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
     bool ok_n = active && ll < p.runs && y_cell + row0 < p.h && x_cell + c40 < p.w;
     int row_n = row0, c4_n = c40;
     float4 Ln = make_float4(0.f, 0.f, 0.f, 0.f), An = Ln, Bn = Ln;
-    load_run(ok_n, y_cell + row0, x_cell + c40, Ln, An, Bn);
+    load_run(ok_n, y_cell + row0, x_cell + c40, run_len(c40, x_cell + c40), Ln, An, Bn);
 
     // ---- stage the 9 candidates (the cell's lanes, 9 / LPC each) --------------
     float mc = 0.f, mxy = 0.f, okf = 1.f;
@@ -250,10 +270,11 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
       if (j + LPC < p.runs) {
         run_pos(j + LPC, row_n, c4_n);
         ok_n = active && y_cell + row_n < p.h && x_cell + c4_n < p.w;
-        load_run(ok_n, y_cell + row_n, x_cell + c4_n, Ln, An, Bn);
+        load_run(ok_n, y_cell + row_n, x_cell + c4_n, run_len(c4_n, x_cell + c4_n), Ln, An, Bn);
       }
       if (!ok) continue;
       const int y = y_cell + row, x = x_cell + c4;
+      const int nv = run_len(c4, x);  // valid pixels of this run (4 when AL)
       const long long pix = img_base + (long long)y * p.w + x;  // label index
       // Channel 0 carries the certified-sum flag in its sign bit (set by the
       // engine's planar convert; channel 0 is never negative): strip it.
@@ -318,7 +339,7 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
         const float thr = __fmaf_rn(f2v, p.k_rel, __fmaf_rn(mp, p.k_mp, two_a_cell));
         const float gap = __fsub_rn(f2v, __uint_as_float(k1[i]));
         t[i] = (int)(k1[i] & 15u);
-        const bool u = !(gap > thr) || !(mp < 1e15f);
+        const bool u = (!(gap > thr) || !(mp < 1e15f)) && i < nv;
         need |= (unsigned)u << i;
         unsure |= u;
       }
@@ -340,6 +361,7 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
       if (ACC) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
+          if (!AL && i >= nv) break;
           double* d = accd + t[i] * 96 + lane;
           d[0] = dadd(d[0], (double)L[i]);
           d[32] = dadd(d[32], (double)A[i]);
@@ -349,7 +371,13 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
                                     ((unsigned long long)row << 43);
         }
       }
-      *reinterpret_cast<int4*>(p.labels + pix) = make_int4(lab4[0], lab4[1], lab4[2], lab4[3]);
+      if (AL) {
+        *reinterpret_cast<int4*>(p.labels + pix) = make_int4(lab4[0], lab4[1], lab4[2], lab4[3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < nv) p.labels[pix + i] = lab4[i];
+      }
     }
     if (ACC) {
       __syncwarp();
@@ -682,9 +710,12 @@ __global__ void k_fill_i32(int32_t* v, int n, int value) {
 
 // ---- launchers ----------------------------------------------------------------
 
+// Any S in [4, 32] (runs of 4 pixels, the last one of a cell row partial
+// when S % 4 != 0); frames with h*w % 4 == 0 (the planar convert's 4-pixel
+// groups never straddle frames); n_bl <= 32 strips for the exact fallback.
 bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
   int64_t n_bl = ceil_div(3 * s, tile_len);
-  return s % 4 == 0 && s >= 8 && s <= 32 && w % 4 == 0 && n_bl <= 32 &&
+  return s >= 4 && s <= 32 && (h * w) % 4 == 0 && n_bl <= 32 &&
          h * w * 3 < (int64_t)1 << 40 && h < (1 << 30) && w < (1 << 30);
 }
 
@@ -701,16 +732,28 @@ static int cell_lpc(int64_t s) {
 
 size_t cell_smem_bytes(int64_t s, bool acc) { return (size_t)kWarps * warp_smem(cell_lpc(s), acc); }
 
-template <bool ACC, int LPC>
+template <bool ACC, int LPC, bool AL>
 static int launch_cell_t(const CellParams& p, dim3 blocks, size_t smem, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    SPX_CUDA(cudaFuncSetAttribute(k_cell<ACC, LPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SPX_CUDA(cudaFuncSetAttribute(k_cell<ACC, LPC, AL>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kWarps * warp_smem(LPC, true))));
     configured = true;
   }
-  k_cell<ACC, LPC><<<blocks, 128, smem, st>>>(p);
+  k_cell<ACC, LPC, AL><<<blocks, 128, smem, st>>>(p);
   return SPX_OK;
+}
+
+template <int LPC>
+static int launch_cell_lpc(const CellParams& p, dim3 blocks, size_t smem, cudaStream_t st,
+                           bool acc) {
+  const bool al = p.s % 4 == 0 && p.w % 4 == 0;
+  if (al)
+    return acc ? launch_cell_t<true, LPC, true>(p, blocks, smem, st)
+               : launch_cell_t<false, LPC, true>(p, blocks, smem, st);
+  return acc ? launch_cell_t<true, LPC, false>(p, blocks, smem, st)
+             : launch_cell_t<false, LPC, false>(p, blocks, smem, st);
 }
 
 void assoc_bound_coefficients(double xy_weight, float& w32, float& k_mp, float& k_mc, float& k_xy,
@@ -738,8 +781,8 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.cr0 = (int)cr0;
   p.cr1 = (int)cr1;
   p.row_off = (int)row_off;
-  p.runs = (int)(s * s / 4);
-  p.runs_per_row = (int)(s / 4);
+  p.runs_per_row = (int)ceil_div(s, 4);
+  p.runs = (int)(s * p.runs_per_row);
   p.row_magic = (unsigned)((65536 + p.runs_per_row - 1) / p.runs_per_row);
   p.xy_weight = xy_weight;
   assoc_bound_coefficients(xy_weight, p.w32, p.k_mp, p.k_mc, p.k_xy, p.k_const, p.k_rel);
@@ -757,14 +800,9 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
     return SPX_ERR_VALUE;
   }
   const size_t smem = cell_smem_bytes(s, acc);
-  int rc;
-  if (lpc == 4)
-    rc = acc ? launch_cell_t<true, 4>(p, blocks, smem, st) : launch_cell_t<false, 4>(p, blocks, smem, st);
-  else if (lpc == 8)
-    rc = acc ? launch_cell_t<true, 8>(p, blocks, smem, st) : launch_cell_t<false, 8>(p, blocks, smem, st);
-  else
-    rc = acc ? launch_cell_t<true, 16>(p, blocks, smem, st)
-             : launch_cell_t<false, 16>(p, blocks, smem, st);
+  const int rc = lpc == 4   ? launch_cell_lpc<4>(p, blocks, smem, st, acc)
+                 : lpc == 8 ? launch_cell_lpc<8>(p, blocks, smem, st, acc)
+                            : launch_cell_lpc<16>(p, blocks, smem, st, acc);
   if (rc) return rc;
   SPX_LAUNCH_CHECK("k_cell");
   return SPX_OK;

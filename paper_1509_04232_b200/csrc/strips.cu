@@ -304,8 +304,8 @@ int32_t spx_strip_create(const spx_settings* st, int64_t row_lo, int64_t row_hi,
     set_error("strip rows [%lld, %lld) outside the grid", (long long)row_lo, (long long)row_hi);
     return SPX_ERR_INVALID_SETTINGS;
   }
-  if (!cell_path_ok(st->height, st->width, st->s, st->tile_len) || st->s < 2) {
-    set_error("row strips need the fused cell path (W %% 4 == 0, S %% 4 == 0, 8 <= S <= 32)");
+  if (!cell_path_ok(st->height, st->width, st->s, st->tile_len) || st->width % 4 != 0) {
+    set_error("row strips need the fused cell path (W %% 4 == 0, 4 <= S <= 32)");
     return SPX_ERR_INVALID_SETTINGS;
   }
   if (st->early_stop >= 0.0) {

@@ -188,12 +188,18 @@ def _images(h, w, seed):
     return {"noise": noise, "gray": gray, "smooth": smooth, "dark": dark}
 
 
-@pytest.mark.parametrize("s", [8, 12, 16, 20, 24, 32])
-def test_cell_path_grid_sizes_bitexact(s):
-    # W % 4 == 0 and 8 <= S <= 32, S % 4 == 0 select the fused cell kernels;
-    # ragged last row/column of cells included.
+@pytest.mark.parametrize("s,odd_w", [(8, False), (12, False), (16, False), (20, False),
+                                     (24, False), (32, False),
+                                     (4, False), (5, True), (6, False), (7, True), (9, False),
+                                     (10, True), (14, False), (18, True), (25, False), (31, True)])
+def test_cell_path_grid_sizes_bitexact(s, odd_w):
+    # 4 <= S <= 32 and h*w % 4 == 0 select the fused cell kernels: 128-bit
+    # runs when S % 4 == 0 and W % 4 == 0, per-pixel (partial) runs
+    # otherwise; ragged last row/column of cells included.
     h, w = 3 * s + 5, 4 * s + 4 * ((s // 4) % 3) + 8
     w -= w % 4
+    if odd_w:  # W % 4 != 0 (h chosen so that h*w % 4 == 0)
+        w, h = w + 2, h + (h % 2)
     for name, rgb in _images(h, w, s).items():
         for tile in (16, 5):
             st = spx.Settings(img_width=w, img_height=h, spixel_size=s, tile_len=tile, no_iters=3)
