@@ -22,6 +22,7 @@
 //     only be set by such a keeper);
 //   * absorbed components take the final value of their seed-left
 //     component, resolved by pointer jumping.
+#include <algorithm>
 #include <climits>
 
 #include "spx_internal.cuh"
@@ -166,7 +167,23 @@ __global__ void __launch_bounds__(256) k_weak2(const int32_t* __restrict__ src,
 
 // ---- strict -------------------------------------------------------------------
 
-__device__ __forceinline__ int32_t uf_find(const int32_t* parent, int32_t x) {
+// Union-find over pixel indices with min-index roots (ECL-CC style): links
+// only ever point to smaller indices, so concurrent path halving (each step
+// re-points x at its grandparent) keeps every pointer valid.
+__device__ __forceinline__ int32_t uf_find(int32_t* parent, int32_t x) {
+  int32_t p = parent[x];
+  while (p != x) {
+    const int32_t g = parent[p];
+    if (g != p) parent[x] = g;  // halve the path
+    x = p;
+    p = g;
+  }
+  return x;
+}
+// Read-only find, for the flatten pass: there every pixel also stores its
+// root, and a concurrent halving store could replace a stored root with a
+// mere ancestor.
+__device__ __forceinline__ int32_t uf_root(const int32_t* parent, int32_t x) {
   int32_t p = parent[x];
   while (p != x) {
     x = p;
@@ -174,7 +191,6 @@ __device__ __forceinline__ int32_t uf_find(const int32_t* parent, int32_t x) {
   }
   return x;
 }
-
 __device__ __forceinline__ void uf_unite(int32_t* parent, int32_t a, int32_t b) {
   while (true) {
     a = uf_find(parent, a);
@@ -191,71 +207,113 @@ __device__ __forceinline__ void uf_unite(int32_t* parent, int32_t a, int32_t b) 
   }
 }
 
-__global__ void k_cc_init(int32_t* parent, int32_t* size, int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    parent[i] = (int32_t)i;
-    size[i] = 0;
-  }
+// Per-pixel kernels run on a (column blocks, rows, frames) grid: pixel
+// (x, y) of frame f has global index f*h*w + y*w + x (< 2^31).
+struct PixIdx {
+  int x, y, f, i;  // i: global index
+  bool in;
+};
+__device__ __forceinline__ PixIdx pix_idx(int h, int w) {
+  PixIdx q;
+  q.x = blockIdx.x * blockDim.x + threadIdx.x;
+  q.y = blockIdx.y;
+  q.f = blockIdx.z;
+  q.in = q.x < w;
+  q.i = (q.f * h + q.y) * w + q.x;
+  return q;
 }
 
-__global__ void k_cc_union(const int32_t* __restrict__ lab, int32_t* parent, int64_t h, int64_t w,
-                           int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int64_t local = i % (h * w);
-  int64_t x = local % w, y = local / w;
-  int32_t v = lab[i];
-  if (x < w - 1 && lab[i + 1] == v) uf_unite(parent, (int32_t)i, (int32_t)(i + 1));
-  if (y < h - 1 && lab[i + w] == v) uf_unite(parent, (int32_t)i, (int32_t)(i + w));
+__global__ void k_cc_init(int32_t* parent, int32_t* size, int h, int w) {
+  const PixIdx q = pix_idx(h, w);
+  if (!q.in) return;
+  parent[q.i] = q.i;
+  size[q.i] = 0;
 }
 
-__global__ void k_cc_flatten(int32_t* parent, int32_t* size, int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int32_t r = uf_find(parent, (int32_t)i);
-  parent[i] = r;
-  atomicAdd(size + r, 1);
+__global__ void k_cc_union(const int32_t* __restrict__ lab, int32_t* parent, int h, int w) {
+  const PixIdx q = pix_idx(h, w);
+  if (!q.in) return;
+  const int32_t v = lab[q.i];
+  if (q.x < w - 1 && lab[q.i + 1] == v) uf_unite(parent, q.i, q.i + 1);
+  if (q.y < h - 1 && lab[q.i + w] == v) uf_unite(parent, q.i, q.i + w);
+}
+
+// Flatten to roots and count component sizes; lanes of a warp with the same
+// root add their count with one atomic.
+__global__ void k_cc_flatten(int32_t* parent, int32_t* size, int h, int w) {
+  const PixIdx q = pix_idx(h, w);
+  const int32_t r = q.in ? uf_root(parent, q.i) : -1;
+  if (q.in) parent[q.i] = r;
+  const unsigned grp = __match_any_sync(0xFFFFFFFFu, r);
+  if (q.in && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(size + r, __popc(grp));
 }
 
 __global__ void k_cc_first(const int32_t* __restrict__ lab, const int32_t* __restrict__ parent,
-                           const int32_t* __restrict__ size, int32_t* first, int64_t hw,
-                           int64_t n, int64_t nlab, int64_t min_size) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || parent[i] != (int32_t)i || size[i] < min_size) return;
-  int64_t f = i / hw;
-  atomicMin(first + f * nlab + lab[i], (int32_t)i);
+                           const int32_t* __restrict__ size, int32_t* first, int h, int w,
+                           int64_t nlab, int64_t min_size) {
+  const PixIdx q = pix_idx(h, w);
+  if (!q.in || parent[q.i] != q.i || size[q.i] < min_size) return;
+  atomicMin(first + q.f * nlab + lab[q.i], q.i);
 }
 
 __global__ void k_cc_next(const int32_t* __restrict__ lab, const int32_t* __restrict__ parent,
                           const int32_t* __restrict__ size, const int32_t* __restrict__ first,
-                          int32_t* nxt, int64_t w, int64_t hw, int64_t n, int64_t nlab,
-                          int64_t min_size) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || parent[i] != (int32_t)i) return;
-  int64_t f = i / hw, base = f * hw, local = i - base;
-  int32_t v = lab[i];
-  bool keep = local == 0 ||
-              (size[i] >= min_size && first[f * nlab + v] == (int32_t)i && lab[base] != v);
-  if (keep) {
-    nxt[i] = (int32_t)i;
-  } else {
-    int64_t adj = (local % w > 0) ? i - 1 : i - w;
-    nxt[i] = parent[adj];
-  }
+                          int32_t* nxt, int32_t* roots, int32_t* nroots, int h, int w,
+                          int64_t nlab, int64_t min_size) {
+  const PixIdx q = pix_idx(h, w);
+  const bool root = q.in && parent[q.i] == q.i;
+  // compact list of components (any order): one global atomic per block
+  __shared__ int bcount, bbase;
+  if (threadIdx.x == 0) bcount = 0;
+  __syncthreads();
+  const int slot = root ? atomicAdd(&bcount, 1) : 0;
+  __syncthreads();
+  if (threadIdx.x == 0) bbase = bcount ? atomicAdd(nroots, bcount) : 0;
+  __syncthreads();
+  if (!root) return;
+  roots[bbase + slot] = q.i;
+  const int base = q.f * h * w;
+  const int32_t v = lab[q.i];
+  const bool keep = q.i == base ||
+                    (size[q.i] >= min_size && first[q.f * nlab + v] == q.i && lab[base] != v);
+  // absorbed: the root of the seed's left neighbour (up in column 0)
+  nxt[q.i] = keep ? q.i : parent[q.x > 0 ? q.i - 1 : q.i - w];
 }
 
-__global__ void k_cc_jump(const int32_t* __restrict__ parent, int32_t* nxt, int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || parent[i] != (int32_t)i) return;
-  nxt[i] = nxt[nxt[i]];
+// Final value of each component: pointer jumping on nxt over the compact
+// list of components (nxt[r] <- nxt[nxt[r]]), ceil(log2(h*w)) + 1 rounds --
+// absorption chains never leave a frame and strictly decrease in seed index,
+// so they are shorter than h*w -- after which nxt[r] is r's keeper.  Racing
+// updates only ever shortcut to a later node of the same chain.  (On random
+// noise frames nearly every component is a 1-2 pixel fragment and chains run
+// to hundreds of links, which rules out per-component chain walking.)
+// Round `round` records whether it changed anything in changed[round]; a
+// round after one that changed nothing returns at once (converged).
+__global__ void k_cc_jump(const int32_t* __restrict__ roots, const int32_t* __restrict__ nroots,
+                          int32_t* nxt, int32_t* changed, int round) {
+  if (round > 0 && changed[round - 1] == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) changed[round] = 0;
+    return;
+  }
+  const int n = *nroots;
+  bool any = false;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int32_t r = roots[j];
+    const int32_t a = nxt[r], b = nxt[a];
+    if (a != b) {
+      nxt[r] = b;
+      any = true;
+    }
+  }
+  if (__syncthreads_or(any) && threadIdx.x == 0) changed[round] = 1;
 }
 
 __global__ void k_cc_write(const int32_t* __restrict__ lab, const int32_t* __restrict__ parent,
-                           const int32_t* __restrict__ nxt, int32_t* __restrict__ dst, int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  dst[i] = lab[nxt[parent[i]]];
+                           const int32_t* __restrict__ nxt, int32_t* __restrict__ dst, int h,
+                           int w) {
+  const PixIdx q = pix_idx(h, w);
+  if (!q.in) return;
+  dst[q.i] = lab[nxt[parent[q.i]]];
 }
 
 __global__ void k_max_label(const int32_t* __restrict__ lab, int64_t n, int* out, int* neg) {
@@ -291,7 +349,9 @@ int launch_weak2(const int32_t* src, int32_t* dst, int64_t h, int64_t w, int fra
   return SPX_OK;
 }
 
-// scratch: parent, size, nxt (n each) and first (frames * nlab), all int32.
+// scratch: parent, size, nxt (n each) and first (frames * nlab + kStrictExtra),
+// all int32;
+// src and dst must not overlap (dst holds the component list meanwhile).
 int launch_strict(const int32_t* src, int32_t* dst, int64_t h, int64_t w, int frames,
                   int64_t nlab, int64_t min_size, int32_t* parent, int32_t* size, int32_t* nxt,
                   int32_t* first, cudaStream_t st) {
@@ -301,17 +361,29 @@ int launch_strict(const int32_t* src, int32_t* dst, int64_t h, int64_t w, int fr
     set_error("strict_fill: %lld pixels exceed the int32 component index", (long long)n);
     return SPX_ERR_VALUE;
   }
-  unsigned b = (unsigned)ceil_div(n, 256);
-  k_cc_init<<<b, 256, 0, st>>>(parent, size, n);
+  if (h > 65535 || frames > 65535) {
+    set_error("strict_fill: at most 65535 rows and 65535 frames per launch");
+    return SPX_ERR_VALUE;
+  }
+  const dim3 grid((unsigned)ceil_div(w, 256), (unsigned)h, (unsigned)frames);
+  const int H = (int)h, W = (int)w;
+  k_cc_init<<<grid, 256, 0, st>>>(parent, size, H, W);
   SPX_CUDA(cudaMemsetAsync(first, 0x7f, (size_t)(frames * nlab) * 4, st));
-  k_cc_union<<<b, 256, 0, st>>>(src, parent, h, w, n);
-  k_cc_flatten<<<b, 256, 0, st>>>(parent, size, n);
-  k_cc_first<<<b, 256, 0, st>>>(src, parent, size, first, hw, n, nlab, min_size);
-  k_cc_next<<<b, 256, 0, st>>>(src, parent, size, first, nxt, w, hw, n, nlab, min_size);
+  k_cc_union<<<grid, 256, 0, st>>>(src, parent, H, W);
+  k_cc_flatten<<<grid, 256, 0, st>>>(parent, size, H, W);
+  k_cc_first<<<grid, 256, 0, st>>>(src, parent, size, first, H, W, nlab, min_size);
+  // The component list lives in dst until the final write; its length and
+  // the per-round change flags in the kStrictExtra ints after `first`.
+  int32_t* nroots = first + frames * nlab;
+  int32_t* changed = nroots + 1;
+  SPX_CUDA(cudaMemsetAsync(nroots, 0, kStrictExtra * sizeof(int32_t), st));
+  k_cc_next<<<grid, 256, 0, st>>>(src, parent, size, first, nxt, dst, nroots, H, W, nlab,
+                                  min_size);
   int rounds = 1;
-  while ((1ll << rounds) < n) ++rounds;
-  for (int r = 0; r <= rounds; ++r) k_cc_jump<<<b, 256, 0, st>>>(parent, nxt, n);
-  k_cc_write<<<b, 256, 0, st>>>(src, parent, nxt, dst, n);
+  while ((1ll << rounds) < hw) ++rounds;
+  const unsigned jb = (unsigned)std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 8);
+  for (int r = 0; r <= rounds; ++r) k_cc_jump<<<jb, 256, 0, st>>>(dst, nroots, nxt, changed, r);
+  k_cc_write<<<grid, 256, 0, st>>>(src, parent, nxt, dst, H, W);
   SPX_LAUNCH_CHECK("strict_fill kernels");
   return SPX_OK;
 }
@@ -338,7 +410,7 @@ int strict_fill_alloc(const int32_t* src, int32_t* dst, int64_t h, int64_t w, in
   SPX_CUDA(cudaMallocAsync(&parent, n * 4, st));
   SPX_CUDA(cudaMallocAsync(&size, n * 4, st));
   SPX_CUDA(cudaMallocAsync(&nxt, n * 4, st));
-  SPX_CUDA(cudaMallocAsync(&first, nlab * 4, st));
+  SPX_CUDA(cudaMallocAsync(&first, (nlab + kStrictExtra) * 4, st));
   rc = launch_strict(src, dst, h, w, 1, nlab, min_size, parent, size, nxt, first, st);
   cudaFreeAsync(parent, st);
   cudaFreeAsync(size, st);

@@ -142,7 +142,7 @@ struct Engine {
       SPX_CUDA(cudaMalloc(&cc_parent, B * hw * sizeof(int32_t)));
       SPX_CUDA(cudaMalloc(&cc_size, B * hw * sizeof(int32_t)));
       SPX_CUDA(cudaMalloc(&cc_nxt, B * hw * sizeof(int32_t)));
-      SPX_CUDA(cudaMalloc(&cc_first, B * K * sizeof(int32_t)));
+      SPX_CUDA(cudaMalloc(&cc_first, (B * K + kStrictExtra) * sizeof(int32_t)));
     }
     for (auto& e : ev) SPX_CUDA(cudaEventCreate(&e));
     return SPX_OK;
@@ -365,7 +365,9 @@ struct Engine {
       if ((rc = launch_strict(labels, out_labels, st.height, st.width, B, K, st.min_size,
                               cc_parent, cc_size, cc_nxt, cc_first, s)))
         return rc;
-      launches += 8;
+      int rounds = 1;  // k_cc_init, union, flatten, first, next, jump x (rounds + 1), write
+      while ((1ll << rounds) < hw) ++rounds;
+      launches += 6 + rounds + 1;
     } else {
       SPX_CUDA(cudaMemcpyAsync(out_labels, labels, (size_t)B * hw * sizeof(int32_t),
                                cudaMemcpyDeviceToDevice, s));
