@@ -123,7 +123,11 @@ __device__ __forceinline__ double scale2(double x, int n) {
 // (0, 1.2]), with no branches: frexp by bit manipulation, the factor picked
 // with selects, the exact doublings and the final ldexp as exponent adds.
 // Same rounded operations as cbrt_glibc, so the same result.
-__device__ __forceinline__ double cbrt_fast(double x, const double* fac) {
+// fx[xe + 6] = factor[2 + xe % 3] * 2^(xe / 3) for the exponents convert
+// produces (t in (eps, 1.2], or the stand-in 1.0: xe in [-6, 1]).  Scaling
+// by a power of two commutes with rounding, so RN(q * fx) equals glibc's
+// ldexp(RN(q * factor), xe / 3).
+__device__ __forceinline__ double cbrt_fast(double x, const double* fx) {
   const long long bits = __double_as_longlong(x);
   const int xe = (int)((bits >> 52) & 0x7ff) - 1022;
   const double xm = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | (1022LL << 52));
@@ -134,16 +138,9 @@ __device__ __forceinline__ double cbrt_fast(double x, const double* fac) {
   p = dadd(1.50819193781584896, dmul(p, xm));
   const double u = dadd(0.354895765043919860, dmul(p, xm));
   const double t2 = dmul(dmul(u, u), u);
-  const int m = xe % 3;  // in [-2, 2]
-  double f = fac[2];  // selects on register values (no branches)
-  f = m == 1 ? fac[3] : f;
-  f = m == 2 ? fac[4] : f;
-  f = m == -1 ? fac[1] : f;
-  f = m == -2 ? fac[0] : f;
+  const double f = fx[min(max(xe + 6, 0), 7)];  // shared memory, conflict-free
   // 2*xm and 2*t2 are exact doublings (xm in [0.5, 1), t2 > 0.04)
-  const double ym =
-      dmul(div_rn_fast(dmul(u, dadd(t2, scale2(xm, 1))), dadd(scale2(t2, 1), xm)), f);
-  return scale2(ym, xe / 3);
+  return dmul(div_rn_fast(dmul(u, dadd(t2, scale2(xm, 1))), dadd(scale2(t2, 1), xm)), f);
 }
 
 __device__ __forceinline__ double lab_lin(double t) {
@@ -151,7 +148,7 @@ __device__ __forceinline__ double lab_lin(double t) {
 }
 
 struct Factors {
-  double f[5];
+  const double* f;  // the fx table of cbrt_fast (shared memory)
 };
 
 template <int SPACE>
@@ -219,9 +216,13 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
                                                  float* __restrict__ out, int64_t p0,
                                                  int64_t p1, int vec, int64_t hw, float tau) {
   __shared__ double lut[256];
+  __shared__ double fxs[8];
+  if (threadIdx.x < 8) {
+    const int xe = (int)threadIdx.x - 6;  // C semantics of % and / (glibc s_cbrt.c)
+    fxs[threadIdx.x] = ldexp(c_factor[2 + xe % 3], xe / 3);
+  }
   Factors fc;
-#pragma unroll
-  for (int i = 0; i < 5; ++i) fc.f[i] = c_factor[i];
+  fc.f = fxs;
   if (SPACE != 0) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = g_lut[i];
     __syncthreads();
