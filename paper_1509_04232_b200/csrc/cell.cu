@@ -511,23 +511,61 @@ __device__ __forceinline__ void write_centre(const ReduceParams& p, long long gk
 // One lane per cluster: fixed-order sum of the 9 (cell, slot) partials that
 // belong to it.  Clusters with a flagged member are recomputed by the whole
 // warp with the reference strip folds + pairwise strip tree (_core.pyx:300-311).
-__global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
+__device__ __forceinline__ void centre_values(const ReduceParams& p, long long gk, int kr, int kc,
+                                              double cnt, double sl, double sa, double sb,
+                                              double sx, double sy, double* xy, double* lab,
+                                              CRec& r) {
+  if (cnt > 0.0) {  // _core.pyx:313-320
+    lab[0] = ddiv(sl, cnt);
+    lab[1] = ddiv(sa, cnt);
+    lab[2] = ddiv(sb, cnt);
+    xy[0] = ddiv(sx, cnt);
+    xy[1] = ddiv(sy, cnt);
+  } else {
+    lab[0] = p.prev_lab[3 * gk];
+    lab[1] = p.prev_lab[3 * gk + 1];
+    lab[2] = p.prev_lab[3 * gk + 2];
+    xy[0] = p.prev_xy[2 * gk];
+    xy[1] = p.prev_xy[2 * gk + 1];
+  }
+  r.l = __double2float_rn(lab[0]);
+  r.a = __double2float_rn(lab[1]);
+  r.b = __double2float_rn(lab[2]);
+  r.xr = __double2float_rn(dsub(xy[0], (double)kc * p.s));
+  r.yr = __double2float_rn(dsub(xy[1], (double)(kr + p.row_off) * p.s));
+  r.mag_lab = fmaxf(fabsf(r.l), fmaxf(fabsf(r.a), fabsf(r.b)));
+  r.mag_xy = fmaxf(fabsf(r.xr), fabsf(r.yr));
+  r.ok = (fin_small(xy[0]) && fin_small(xy[1]) && fin_small(lab[0]) && fin_small(lab[1]) &&
+          fin_small(lab[2]))
+             ? 1.f
+             : 0.f;
+}
+
+// One thread per cluster: the sums of the cell partials, divided as in
+// _core.pyx:313-320; the block's 128 consecutive clusters are staged in
+// shared memory and written out with coalesced 16-byte stores (the per-
+// cluster AoS records would otherwise leave as 8 scattered stores per
+// thread).  Flagged clusters get placeholder values here and are rewritten
+// by k_exact_clusters, which runs after this kernel.
+constexpr int kRedT = 128;
+
+__global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
+  __shared__ __align__(16) double s_xy[kRedT * 2];
+  __shared__ __align__(16) double s_lab[kRedT * 3];
+  __shared__ __align__(16) long long s_cnt[kRedT];
+  __shared__ __align__(16) CRec s_rec[kRedT];
   const int K = p.ns_r * p.ns_c;
   const int nk = (p.kr1 - p.kr0) * p.ns_c;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;  // cluster of frame blockIdx.y
-  const bool in = j < nk;
-  int f = 0, k = 0, kr = 0, kc = 0;
-  long long gk = 0;
-  bool todo = false, flagged = false;
-  if (in) {
-    f = blockIdx.y;
-    k = p.kr0 * p.ns_c + j;
-    gk = (long long)f * K + k;
-    kr = k / p.ns_c;
-    kc = k % p.ns_c;
-    todo = !(p.done && p.done[f]);
-  }
-  if (todo) {
+  const int f = blockIdx.y;
+  if (p.done && p.done[f]) return;  // whole block: one frame
+  const int j0 = blockIdx.x * kRedT;
+  const int n = min(kRedT, nk - j0);
+  const long long gk0 = (long long)f * K + p.kr0 * p.ns_c + j0;
+  const int t = threadIdx.x;
+  if (t < n) {
+    const long long gk = gk0 + t;
+    const int k = p.kr0 * p.ns_c + j0 + t;
+    const int kr = k / p.ns_c, kc = k - kr * p.ns_c;
     ClusterAcc* a = p.acc + gk;
     const double4 s012 = *reinterpret_cast<const double4*>(a);  // s[0..2], sx
     const ulonglong2 syc = *reinterpret_cast<const ulonglong2*>(&a->sy);
@@ -536,11 +574,24 @@ __global__ void __launch_bounds__(128) k_reduce_cells(ReduceParams p) {
     *reinterpret_cast<ulonglong2*>(&a->sy) = make_ulonglong2(0ull, 0ull);
     const unsigned long long sx = (unsigned long long)__double_as_longlong(s012.w);
     const unsigned long long cnt = syc.y & 0xFFFFFFFFull, fl = syc.y >> 32;
-    flagged = fl != 0;
-    if (!flagged)
-      write_centre(p, gk, kr, kc, (double)cnt, s012.x, s012.y, s012.z, (double)sx, (double)syc.x);
+    if (fl != 0) p.worklist[atomicAdd(p.worklist_n, 1)] = (int32_t)gk;
+    centre_values(p, gk, kr, kc, (double)cnt, s012.x, s012.y, s012.z, (double)sx, (double)syc.x,
+                  s_xy + 2 * t, s_lab + 3 * t, s_rec[t]);
+    s_cnt[t] = (long long)cnt;
   }
-  if (flagged) p.worklist[atomicAdd(p.worklist_n, 1)] = (int32_t)gk;
+  __syncthreads();
+  // coalesced copies of the block's contiguous output ranges
+  {
+    const double2* sx2 = reinterpret_cast<const double2*>(s_xy);
+    double2* gx2 = reinterpret_cast<double2*>(p.out_xy + 2 * gk0);
+    for (int i = t; i < n; i += kRedT) gx2[i] = sx2[i];
+    double* gl = p.out_lab + 3 * gk0;
+    for (int i = t; i < 3 * n; i += kRedT) gl[i] = s_lab[i];
+    for (int i = t; i < n; i += kRedT) p.counts[gk0 + i] = s_cnt[i];
+    const float4* sr = reinterpret_cast<const float4*>(s_rec);
+    float4* gr = reinterpret_cast<float4*>(p.rec + gk0);
+    for (int i = t; i < 2 * n; i += kRedT) gr[i] = sr[i];
+  }
 }
 
 // Exact recomputation of flagged clusters (certificate failed).  One block
