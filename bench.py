@@ -58,25 +58,61 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / clock-event reasons sampled during the timed region.
 
-    def __init__(self, index):
-        self.index = index
-        self.samples = []
+    NVML every 5 ms (nvidia-smi every 0.2 s if NVML is unavailable).
+    """
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    BITS = [0x8, 0x40, 0x20, 0x4]  # nvmlClocksEventReason* / ThrottleReason*
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.samples = []  # (sm_mhz, max_mhz, set of reason names)
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            props = torch.cuda.get_device_properties(self.dev)
+            bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            idx = int(str(self.dev).split(":")[-1]) if ":" in str(self.dev) else int(self.dev)
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
+
     def _run(self):
+        try:
+            nv, h = self._nvml_handle()
+            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
+                                  getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                bits = get_reasons(h) if get_reasons else 0
+                self.samples.append((float(sm), float(mx),
+                                     {n for n, b in zip(self.NAMES, self.BITS) if bits & b}))
+                self._stop.wait(0.005)
+            return
+        except Exception:
+            pass
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+        idx = str(self.dev).split(":")[-1]
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                out = subprocess.run(["nvidia-smi", "-i", idx, f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([v.strip() for v in out.split(",")])
+                v = [x.strip() for x in out.split(",")]
+                if len(v) >= 6 and v[0].replace(".", "").isdigit():
+                    self.samples.append((float(v[0]), float(v[1]),
+                                         {n for n, x in zip(self.NAMES, v[2:6])
+                                          if x.lower() == "active"}))
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -93,13 +129,9 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(set().union(*(s[2] for s in self.samples))),
                 "samples": len(self.samples)}
 
 
