@@ -57,6 +57,9 @@ SPX_API int32_t spx_debug_tables(double *lut, double *mat, double *white);
 /* Test hook: max relative error of the association filter's fp32 sqrt over
  * all floats in [1,4) (the error bound assumes <= 2^-21).  Synchronous. */
 SPX_API int32_t spx_debug_sqrt_error(double *out_host);
+/* Test hook: the update's branch-free division vs the IEEE division on n
+ * random operand pairs; out2_host = {mismatches, pairs that took the fast path}. */
+SPX_API int32_t spx_debug_ddiv_check(int64_t n, uint64_t seed, int64_t *out2_host);
 
 /* ---- kernel protocol: replaces pkg/src/superpix/kernels/_core.pyx ---------- */
 

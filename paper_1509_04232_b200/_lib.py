@@ -50,6 +50,7 @@ SIGNATURES = {
     "spx_abi_version": (I32, []),
     "spx_debug_tables": (I32, [P, P, P]),
     "spx_debug_sqrt_error": (I32, [P]),
+    "spx_debug_ddiv_check": (I32, [I64, ctypes.c_uint64, P]),
     "spx_convert_band": (I32, [P, P, I64, I64, I32, I64, I64, P]),
     "spx_init_centers_range": (I32, [P, I64, I64, I64, I64, P, P, I64, I64, P]),
     "spx_perturb_range": (I32, [P, I64, I64, P, P, I64, I64, P]),

@@ -516,11 +516,21 @@ __device__ __forceinline__ void centre_values(const ReduceParams& p, long long g
                                               double sx, double sy, double* xy, double* lab,
                                               CRec& r) {
   if (cnt > 0.0) {  // _core.pyx:313-320
-    lab[0] = ddiv(sl, cnt);
-    lab[1] = ddiv(sa, cnt);
-    lab[2] = ddiv(sb, cnt);
-    xy[0] = ddiv(sx, cnt);
-    xy[1] = ddiv(sy, cnt);
+    // five independent IEEE divisions: branch-free fast paths first (they
+    // interleave), the rare guarded-out operands redone with ddiv
+    const double num[5] = {sl, sa, sb, sx, sy};
+    double q[5];
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) ok &= ddiv_fastpath(num[i], cnt, q[i]);
+    if (!ok)
+#pragma unroll
+      for (int i = 0; i < 5; ++i) q[i] = ddiv(num[i], cnt);
+    lab[0] = q[0];
+    lab[1] = q[1];
+    lab[2] = q[2];
+    xy[0] = q[3];
+    xy[1] = q[4];
   } else {
     lab[0] = p.prev_lab[3 * gk];
     lab[1] = p.prev_lab[3 * gk + 1];

@@ -49,6 +49,15 @@ def test_filter_sqrt_error_within_bound():
     assert 0 < v.value <= 2.0 ** -21, v.value
 
 
+def test_update_division_fast_path_is_ieee():
+    """The centre update's branch-free division (the compiler's own fast path,
+    unrolled) equals IEEE division whenever its guard accepts the operands."""
+    out = (ctypes.c_int64 * 2)()
+    _lib.check(_lib.load().spx_debug_ddiv_check(1 << 28, 12345, out))
+    assert out[0] == 0, f"{out[0]} of {out[1]} fast-path quotients differ"
+    assert out[1] > (1 << 26)
+
+
 @pytest.mark.parametrize("space", [0, 1, 2])
 def test_convert_golden_and_bands(golden, space):
     rgb = golden["convert_rgb"]
