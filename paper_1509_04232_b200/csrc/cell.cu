@@ -23,6 +23,7 @@
 // exact sum.  Pixels outside that range set a flag bit; the reduce kernel
 // recomputes flagged clusters with the reference's exact strip fold.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 
@@ -795,12 +796,14 @@ size_t cell_smem_bytes(int64_t s, bool acc) { return (size_t)kWarps * warp_smem(
 
 template <bool ACC, int LPC, bool AL>
 static int launch_cell_t(const CellParams& p, dim3 blocks, size_t smem, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};  // function attributes are per device
+  int dev = 0;
+  SPX_CUDA(cudaGetDevice(&dev));
+  if (!(configured.load() & (1ull << (dev & 63)))) {
     SPX_CUDA(cudaFuncSetAttribute(k_cell<ACC, LPC, AL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kWarps * warp_smem(LPC, true))));
-    configured = true;
+    configured.fetch_or(1ull << (dev & 63));
   }
   k_cell<ACC, LPC, AL><<<blocks, 128, smem, st>>>(p);
   return SPX_OK;

@@ -12,6 +12,8 @@
 // arithmetic (three glibc-cbrt evaluations with a division each, three
 // divisions by the white point) makes this kernel FP64-pipe bound on B200;
 // see DESIGN.md.
+#include <atomic>
+
 #include "spx_internal.cuh"
 
 namespace spx {
@@ -25,10 +27,14 @@ __constant__ double c_inv_white[3];  // RN(1 / white[i])
 __constant__ double c_inv116;        // RN(1 / 116)
 __device__ double g_lut[256];
 
-static bool g_uploaded = false;
+// __constant__ / __device__ tables live per device: one upload per device
+static std::atomic<uint64_t> g_uploaded{0};
 
 int upload_tables() {
-  if (g_uploaded) return SPX_OK;
+  int dev = 0;
+  SPX_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (g_uploaded.load() & bit) return SPX_OK;
   const ColorTables& t = host_tables();
   SPX_CUDA(cudaMemcpyToSymbol(c_m, t.m, sizeof t.m));
   SPX_CUDA(cudaMemcpyToSymbol(c_white, t.white, sizeof t.white));
@@ -40,7 +46,7 @@ int upload_tables() {
   SPX_CUDA(cudaMemcpyToSymbol(c_inv_white, inv_w, sizeof inv_w));
   SPX_CUDA(cudaMemcpyToSymbol(c_inv116, &inv116, sizeof inv116));
   SPX_CUDA(cudaMemcpyToSymbol(g_lut, t.lut, sizeof t.lut));
-  g_uploaded = true;
+  g_uploaded.fetch_or(bit);
   return SPX_OK;
 }
 
