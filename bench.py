@@ -217,12 +217,19 @@ def run_ours(args):
     import paper_1509_04232_b200 as spx
 
     world, rank, local = dist_setup()
+    # SPX_BENCH_BACKEND=gloo: functional check of the multi-rank path on fewer
+    # GPUs than ranks (ranks share devices; never a timing configuration)
+    backend = os.environ.get("SPX_BENCH_BACKEND", "nccl")
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
+    red_dev = dev if backend == "nccl" else "cpu"  # where the max-over-ranks scalars live
     B = args.batch
     st = spx.Settings(img_width=W, img_height=H, num_superpixels=K_SPX, compactness=M,
                       no_iters=ITERS)
@@ -262,7 +269,7 @@ def run_ours(args):
     assoc_ms = [t * 1e3 for t in tm.associate]
     update_ms = [t * 1e3 for t in tm.update]
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     frames_total = B * world * args.steps
@@ -286,7 +293,7 @@ def run_ours(args):
     eng.wait()
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = B * world * e2e_steps / e2e_s
