@@ -559,36 +559,53 @@ __device__ __forceinline__ void centre_values(const ReduceParams& p, long long g
 // thread).  Flagged clusters get placeholder values here and are rewritten
 // by k_exact_clusters, which runs after this kernel.
 constexpr int kRedT = 128;
+#ifndef SPX_REDPER
+#define SPX_REDPER 1
+#endif
+constexpr int kRedPer = SPX_REDPER;  // clusters per thread: their loads are in flight together
+constexpr int kRedN = kRedT * kRedPer;
 
 __global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
-  __shared__ __align__(16) double s_xy[kRedT * 2];
-  __shared__ __align__(16) double s_lab[kRedT * 3];
-  __shared__ __align__(16) long long s_cnt[kRedT];
-  __shared__ __align__(16) CRec s_rec[kRedT];
+  __shared__ __align__(16) double s_xy[kRedN * 2];
+  __shared__ __align__(16) double s_lab[kRedN * 3];
+  __shared__ __align__(16) long long s_cnt[kRedN];
+  __shared__ __align__(16) CRec s_rec[kRedN];
   const int K = p.ns_r * p.ns_c;
   const int nk = (p.kr1 - p.kr0) * p.ns_c;
   const int f = blockIdx.y;
   if (p.done && p.done[f]) return;  // whole block: one frame
-  const int j0 = blockIdx.x * kRedT;
-  const int n = min(kRedT, nk - j0);
+  const int j0 = blockIdx.x * kRedN;
+  const int n = min(kRedN, nk - j0);
   const long long gk0 = (long long)f * K + p.kr0 * p.ns_c + j0;
   const int t = threadIdx.x;
-  if (t < n) {
-    const long long gk = gk0 + t;
-    const int k = p.kr0 * p.ns_c + j0 + t;
+  double4 s012[kRedPer];
+  ulonglong2 syc[kRedPer];
+#pragma unroll
+  for (int c = 0; c < kRedPer; ++c) {
+    const int i = c * kRedT + t;
+    if (i < n) {
+      const ClusterAcc* a = p.acc + gk0 + i;
+      s012[c] = *reinterpret_cast<const double4*>(a);  // s[0..2], sx
+      syc[c] = *reinterpret_cast<const ulonglong2*>(&a->sy);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kRedPer; ++c) {
+    const int i = c * kRedT + t;
+    if (i >= n) break;
+    const long long gk = gk0 + i;
+    const int k = p.kr0 * p.ns_c + j0 + i;
     const int kr = k / p.ns_c, kc = k - kr * p.ns_c;
     ClusterAcc* a = p.acc + gk;
-    const double4 s012 = *reinterpret_cast<const double4*>(a);  // s[0..2], sx
-    const ulonglong2 syc = *reinterpret_cast<const ulonglong2*>(&a->sy);
     // consume and clear for the next pass
     *reinterpret_cast<double4*>(a) = make_double4(0.0, 0.0, 0.0, 0.0);
     *reinterpret_cast<ulonglong2*>(&a->sy) = make_ulonglong2(0ull, 0ull);
-    const unsigned long long sx = (unsigned long long)__double_as_longlong(s012.w);
-    const unsigned long long cnt = syc.y & 0xFFFFFFFFull, fl = syc.y >> 32;
+    const unsigned long long sx = (unsigned long long)__double_as_longlong(s012[c].w);
+    const unsigned long long cnt = syc[c].y & 0xFFFFFFFFull, fl = syc[c].y >> 32;
     if (fl != 0) p.worklist[atomicAdd(p.worklist_n, 1)] = (int32_t)gk;
-    centre_values(p, gk, kr, kc, (double)cnt, s012.x, s012.y, s012.z, (double)sx, (double)syc.x,
-                  s_xy + 2 * t, s_lab + 3 * t, s_rec[t]);
-    s_cnt[t] = (long long)cnt;
+    centre_values(p, gk, kr, kc, (double)cnt, s012[c].x, s012[c].y, s012[c].z, (double)sx,
+                  (double)syc[c].x, s_xy + 2 * i, s_lab + 3 * i, s_rec[i]);
+    s_cnt[i] = (long long)cnt;
   }
   __syncthreads();
   // coalesced copies of the block's contiguous output ranges
@@ -923,7 +940,7 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
     set_error("k_reduce_cells: at most 65535 frames per launch");
     return SPX_ERR_VALUE;
   }
-  k_reduce_cells<<<dim3((unsigned)ceil_div(nk, 128), (unsigned)frames), 128, 0, st>>>(p);
+  k_reduce_cells<<<dim3((unsigned)ceil_div(nk, kRedN), (unsigned)frames), kRedT, 0, st>>>(p);
   SPX_LAUNCH_CHECK("k_reduce_cells");
   // grid-stride over the worklist; ~0.5% of clusters are flagged, so small
   // launches get a small grid (an empty block still costs its scheduling)
