@@ -633,7 +633,10 @@ __global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
 // reduced per row with REDUX, and lanes 0..2 fold the three colour channels
 // in order.  Thread 0 applies the pairwise strip tree (_core.pyx:300-311).
 // Pipeline labels never spill, so the window holds every member.
-constexpr int kRows = 8;
+#ifndef SPX_EXROWS
+#define SPX_EXROWS 4  // 71 registers, 16 KB: more resident clusters than 8 rows
+#endif
+constexpr int kRows = SPX_EXROWS;
 constexpr int kCols = 96;  // window width 3S <= 96 (S <= 32)
 #ifndef SPX_EXW
 #define SPX_EXW 3
