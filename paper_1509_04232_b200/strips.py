@@ -131,14 +131,25 @@ class LocalComm:
 class DistComm:
     """Neighbour exchange between ranks with torch.distributed send/recv.
 
-    `pack`/`unpack` are callables (the strip engine's, or stand-ins in CPU
-    tests); buffers are [[send_up, recv_up], [send_down, recv_down]].
+    Buffers are [[send_up, recv_up], [send_down, recv_down]].  With NCCL the
+    device buffers go over NVLink directly; with gloo (CPU transport, used for
+    functional tests) device buffers are staged through host memory.
     """
 
     def __init__(self, rank, world, group=None):
         self.rank, self.world, self.group = rank, world, group
 
     def exchange_buffers(self, bufs):
+        import torch.distributed as dist
+        if bufs[0][0].is_cuda and dist.get_backend(self.group) == "gloo":
+            host = [[b.cpu() for b in pair] for pair in bufs]
+            self._exchange(host)
+            for pair, hpair in zip(bufs, host):
+                pair[1].copy_(hpair[1])
+            return
+        self._exchange(bufs)
+
+    def _exchange(self, bufs):
         import torch.distributed as dist
         ops = []
         if self.rank > 0:
