@@ -340,7 +340,9 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
         const float thr = __fmaf_rn(f2v, p.k_rel, __fmaf_rn(mp, p.k_mp, two_a_cell));
         const float gap = __fsub_rn(f2v, __uint_as_float(k1[i]));
         t[i] = (int)(k1[i] & 15u);
-        const bool u = (!(gap > thr) || !(mp < 1e15f)) && i < nv;
+        // Lab comes from the engine's convert (|v| < 300): no magnitude guard
+        // needed; NaN or overflow make `gap > thr` false, i.e. unsure.
+        const bool u = !(gap > thr) && i < nv;
         need |= (unsigned)u << i;
         unsure |= u;
       }
