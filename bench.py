@@ -329,6 +329,9 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "dtype_note": "results binary64-identical to the reference; distances filtered in "
+                          "fp32 under a certified error bound (uncertain pixels redone in "
+                          "binary64), Lab conversion and all sums in binary64",
             "data": "synthetic",
             "config": {"workload": "C1: 640x480 RGB, K=1200 (S=16, 30x40 grid), m=10, 5 iters, "
                                    "LAB, weak connectivity",
@@ -347,6 +350,8 @@ def run_ours(args):
                          "bytes_note": "algorithmic = (16+16) B/px + (40+48) B/cluster per "
                                        "SURVEY §8(d); fused compulsory traffic is 12 B/px "
                                        "read + 4 B/px write + cluster sums",
+                         "limiter": "issue slots / MUFU (18 square roots per pixel), not HBM: "
+                                    "DESIGN.md section 4",
                          "mean_pass_ms": acc_mean,
                          "final_assoc": {"ms": final_ms, "bytes": final_bytes,
                                          "frac": final_bytes / (final_ms / 1e3) / 1e9 / peak},
