@@ -18,14 +18,17 @@
 
 namespace spx {
 
-__constant__ double c_m[9];
 __constant__ double c_white[3];
 __constant__ double c_eps;
 __constant__ double c_kappa;
 __constant__ double c_factor[5];
 __constant__ double c_inv_white[3];  // RN(1 / white[i])
 __constant__ double c_inv116;        // RN(1 / 116)
-__device__ double g_lut[256];
+// g_mlut[3 * i + j][v] = RN(m[3 * i + j] * lut[v]): the nine products of the
+// XYZ matrix rows with the linearised channels, tabulated (the same IEEE
+// products the reference forms, _core.pyx:64-69), so a pixel's XYZ costs six
+// binary64 adds instead of nine multiplies and six adds.
+__device__ double g_mlut[9 * 256];
 
 // __constant__ / __device__ tables live per device: one upload per device
 static std::atomic<uint64_t> g_uploaded{0};
@@ -36,7 +39,6 @@ int upload_tables() {
   const uint64_t bit = 1ull << (dev & 63);
   if (g_uploaded.load() & bit) return SPX_OK;
   const ColorTables& t = host_tables();
-  SPX_CUDA(cudaMemcpyToSymbol(c_m, t.m, sizeof t.m));
   SPX_CUDA(cudaMemcpyToSymbol(c_white, t.white, sizeof t.white));
   SPX_CUDA(cudaMemcpyToSymbol(c_eps, &t.eps, sizeof t.eps));
   SPX_CUDA(cudaMemcpyToSymbol(c_kappa, &t.kappa, sizeof t.kappa));
@@ -45,7 +47,10 @@ int upload_tables() {
   double inv116 = 1.0 / 116.0;
   SPX_CUDA(cudaMemcpyToSymbol(c_inv_white, inv_w, sizeof inv_w));
   SPX_CUDA(cudaMemcpyToSymbol(c_inv116, &inv116, sizeof inv116));
-  SPX_CUDA(cudaMemcpyToSymbol(g_lut, t.lut, sizeof t.lut));
+  static double mlut[9 * 256];
+  for (int i = 0; i < 9; ++i)
+    for (int v = 0; v < 256; ++v) mlut[i * 256 + v] = t.m[i] * t.lut[v];
+  SPX_CUDA(cudaMemcpyToSymbol(g_mlut, mlut, sizeof mlut));
   g_uploaded.fetch_or(bit);
   return SPX_OK;
 }
@@ -167,10 +172,9 @@ __device__ __forceinline__ void convert_px(const double* lut, const Factors& fc,
     o2 = __double2float_rn(ddiv((double)B, 255.0));
     return;
   }
-  double r = lut[R], g = lut[G], b = lut[B];
-  double cx = dadd(dadd(dmul(c_m[0], r), dmul(c_m[1], g)), dmul(c_m[2], b));
-  double cy = dadd(dadd(dmul(c_m[3], r), dmul(c_m[4], g)), dmul(c_m[5], b));
-  double cz = dadd(dadd(dmul(c_m[6], r), dmul(c_m[7], g)), dmul(c_m[8], b));
+  const double cx = dadd(dadd(lut[R], lut[256 + G]), lut[512 + B]);
+  const double cy = dadd(dadd(lut[768 + R], lut[1024 + G]), lut[1280 + B]);
+  const double cz = dadd(dadd(lut[1536 + R], lut[1792 + G]), lut[2048 + B]);
   if (SPACE == 1) {
     o0 = __double2float_rn(cx);
     o1 = __double2float_rn(cy);
@@ -184,13 +188,17 @@ __device__ __forceinline__ void convert_px(const double* lut, const Factors& fc,
   const double tx = div_const(cx, c_white[0], c_inv_white[0]);
   const double ty = div_const(cy, c_white[1], c_inv_white[1]);
   const double tz = div_const(cz, c_white[2], c_inv_white[2]);
-  const double eps = c_eps;
-  double fx = cbrt_fast(tx > eps ? tx : 1.0, fac);
-  double fy = cbrt_fast(ty > eps ? ty : 1.0, fac);
-  double fz = cbrt_fast(tz > eps ? tz : 1.0, fac);
-  if (!(tx > eps)) fx = lab_lin(tx);
-  if (!(ty > eps)) fy = lab_lin(ty);
-  if (!(tz > eps)) fz = lab_lin(tz);
+  // t >= 0 (non-negative matrix and LUT), so `t > eps` is an integer compare
+  // of the bit patterns (keeps the compares off the saturated FP64 pipe)
+  const long long eps = __double_as_longlong(c_eps);
+  const bool bx = __double_as_longlong(tx) > eps, by = __double_as_longlong(ty) > eps,
+             bz = __double_as_longlong(tz) > eps;
+  double fx = cbrt_fast(bx ? tx : 1.0, fac);
+  double fy = cbrt_fast(by ? ty : 1.0, fac);
+  double fz = cbrt_fast(bz ? tz : 1.0, fac);
+  if (!bx) fx = lab_lin(tx);
+  if (!by) fy = lab_lin(ty);
+  if (!bz) fz = lab_lin(tz);
   double light = dsub(dmul(116.0, fy), 16.0);
   if (light < 0.0) light = 0.0;
   if (light > 100.0) light = 100.0;
@@ -221,7 +229,7 @@ template <int SPACE, bool PLANAR>
 __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* __restrict__ rgb,
                                                  float* __restrict__ out, int64_t p0,
                                                  int64_t p1, int vec, int64_t hw, float tau) {
-  __shared__ double lut[256];
+  __shared__ double lut[SPACE == 0 ? 1 : 9 * 256];  // g_mlut (SPACE 1, 2)
   __shared__ double fxs[8];
   if (threadIdx.x < 8) {
     const int xe = (int)threadIdx.x - 6;  // C semantics of % and / (glibc s_cbrt.c)
@@ -230,7 +238,7 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
   Factors fc;
   fc.f = fxs;
   if (SPACE != 0) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = g_lut[i];
+    for (int i = threadIdx.x; i < 9 * 256; i += blockDim.x) lut[i] = g_mlut[i];
     __syncthreads();
   }
   int64_t g0 = p0 >> 2, g1 = (p1 + 3) >> 2;
