@@ -808,13 +808,20 @@ bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
 // 16 <= S <= 24 (S = 16: 0.60 vs 0.64 ms), 16 for S >= 28.  Fewer lanes per
 // cell give each lane more runs over which to amortise the per-cell staging
 // and epilogue; too few leave too many cells in flight per warp.
-static int cell_lpc(int64_t s) {
+// Lanes per cell: 4 for S <= 12, 8 for S <= 24, 16 above.  A launch with
+// fewer warps than one resident wave (16 per SM) -- small batches, e.g. one
+// VGA frame is 1,200 cells -- doubles it when every lane still gets >= 2
+// runs: shorter per-lane walks cut the pass latency (one 640x480 frame:
+// 190 -> 170 us per segmentation) while large launches keep the narrower
+// cells (batch 16: LPC 16 is 5% slower).
+static int cell_lpc(int64_t s, long long cells) {
   static const int env = getenv("SPX_LPC") ? atoi(getenv("SPX_LPC")) : 0;  // development
   if (env == 4 || env == 8 || env == 16) return env;
-  return s <= 12 ? 4 : (s <= 24 ? 8 : 16);
+  int lpc = s <= 12 ? 4 : (s <= 24 ? 8 : 16);
+  const long long runs = s * ceil_div(s, 4);
+  if (lpc < 16 && cells * lpc < (long long)num_sms() * 16 * 32 && runs >= 2 * lpc) lpc *= 2;
+  return lpc;
 }
-
-size_t cell_smem_bytes(int64_t s, bool acc) { return (size_t)kWarps * warp_smem(cell_lpc(s), acc); }
 
 template <bool ACC, int LPC, bool AL>
 static int launch_cell_t(const CellParams& p, dim3 blocks, size_t smem, cudaStream_t st) {
@@ -873,7 +880,7 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.xy_weight = xy_weight;
   assoc_bound_coefficients(xy_weight, p.w32, p.k_mp, p.k_mc, p.k_xy, p.k_const, p.k_rel);
   if (cr1 <= cr0) return SPX_OK;
-  const int lpc = cell_lpc(s);
+  const int lpc = cell_lpc(s, (cr1 - cr0) * ns_c * (long long)frames);
   // Walk up to kGroupsPerWarp groups per warp, but keep >= 16 warps per SM
   // in flight for small launches (one 640x480 frame has only 300 groups).
   const long long groups = ceil_div((cr1 - cr0) * ns_c, 32 / lpc) * (long long)frames;
@@ -885,7 +892,7 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
     set_error("k_cell: at most 65535 frames per launch");
     return SPX_ERR_VALUE;
   }
-  const size_t smem = cell_smem_bytes(s, acc);
+  const size_t smem = (size_t)kWarps * warp_smem(lpc, acc);
   const int rc = lpc == 4   ? launch_cell_lpc<4>(p, blocks, smem, st, acc)
                  : lpc == 8 ? launch_cell_lpc<8>(p, blocks, smem, st, acc)
                             : launch_cell_lpc<16>(p, blocks, smem, st, acc);

@@ -211,6 +211,32 @@ def test_cell_path_grid_sizes_bitexact(s, odd_w):
             assert np.array_equal(res.spixel_map.num_pixels, counts), (s, name, tile)
 
 
+@pytest.mark.parametrize("s,odd_w", [(6, False), (8, False), (12, False), (16, False),
+                                     (20, False), (24, False), (10, True), (18, True)])
+def test_cell_path_wide_launch_bitexact(s, odd_w):
+    # Small launches (the single-frame tests above) run with doubled lanes
+    # per cell; a batch of >= 20,000 cells keeps the narrow cells.  Both
+    # must give the oracle's results.
+    h, w = 3 * s + 5, 4 * s + 4 * ((s // 4) % 3) + 8
+    w -= w % 4
+    if odd_w:
+        w, h = w + 2, h + (h % 2)
+    imgs = list(_images(h, w, 40 + s).values())
+    st = spx.Settings(img_width=w, img_height=h, spixel_size=s, no_iters=3)
+    k = spx.compute_grid(st).num_clusters
+    n = -(-20000 // k)
+    batch = np.stack([imgs[i % len(imgs)] for i in range(n)])
+    labels, cxy, clab, counts, _ = spx.SegEngine(st, max_batch=n).segment_host(batch)
+    for i, rgb in enumerate(imgs):
+        ol, ox, oc, on, _ = _oracle_pipeline(rgb, st)
+        assert np.array_equal(labels[i], ol), (s, i)
+        assert cxy[i].tobytes() == ox.tobytes() and clab[i].tobytes() == oc.tobytes(), (s, i)
+        assert np.array_equal(counts[i], on), (s, i)
+    for i in range(len(imgs), n):  # every copy equals its first occurrence
+        j = i % len(imgs)
+        assert np.array_equal(labels[i], labels[j]) and clab[i].tobytes() == clab[j].tobytes()
+
+
 def test_cell_path_batch_gray_heavy_frames():
     h, w = 480, 640
     st = spx.Settings(img_width=w, img_height=h, num_superpixels=1200)
