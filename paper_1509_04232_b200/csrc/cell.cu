@@ -476,23 +476,12 @@ struct ReduceParams {
   int row_off;             // global cell row of local row 0
 };
 
+// Store cluster gk's new centre q = {l, a, b, x, y} (already divided, or
+// the previous centre for an empty cluster, _core.pyx:313-320), its count and
+// its fp32 record.
 __device__ __forceinline__ void write_centre(const ReduceParams& p, long long gk, int kr, int kc,
-                                             double cnt, double sl, double sa, double sb,
-                                             double sx, double sy) {
-  double l, a, b, x, y;
-  if (cnt > 0.0) {  // _core.pyx:313-320
-    l = ddiv(sl, cnt);
-    a = ddiv(sa, cnt);
-    b = ddiv(sb, cnt);
-    x = ddiv(sx, cnt);
-    y = ddiv(sy, cnt);
-  } else {
-    l = p.prev_lab[3 * gk];
-    a = p.prev_lab[3 * gk + 1];
-    b = p.prev_lab[3 * gk + 2];
-    x = p.prev_xy[2 * gk];
-    y = p.prev_xy[2 * gk + 1];
-  }
+                                             double cnt, const double* q) {
+  const double l = q[0], a = q[1], b = q[2], x = q[3], y = q[4];
   p.out_lab[3 * gk] = l;
   p.out_lab[3 * gk + 1] = a;
   p.out_lab[3 * gk + 2] = b;
@@ -625,21 +614,21 @@ __global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
 }
 
 // Exact recomputation of flagged clusters (certificate failed).  One block
-// per cluster; its warps take the cluster's row strips (strip j = rows
-// [ry0 + j*tile_len, ...) of the 3S x 3S window), each strip being an
-// independent reference fold that starts from 0.0 (_core.pyx:233-243), so a
-// cluster's latency is one strip's, not the whole window's.  A strip is
-// walked in blocks of kRows rows with the next block's label loads in flight;
-// per row, lanes own columns, matches are compacted in row-major order into
-// shared memory (ballot + popc) with cp.async value copies, x / y / count are
-// reduced per row with REDUX, and lanes 0..2 fold the three colour channels
-// in order.  Thread 0 applies the pairwise strip tree (_core.pyx:300-311).
+// per cluster, built for latency -- at small batches this kernel's chain of
+// dependent steps IS the pass's update time:
+//  (1) the worklist count and the block's first item load together;
+//  (2) the 3S x 3S window of labels is staged into shared memory with one
+//      round of cp.async (16-byte copies when aligned);
+//  (3) each warp takes row strips (strip j = rows [ry0 + j*tile_len, ...),
+//      an independent reference fold from 0.0, _core.pyx:233-243).  Lanes own
+//      (row, column-segment) pieces of the strip in row-major order: each
+//      counts its members, a warp scan gives every member its row-major
+//      position, members' L / a / b are copied with cp.async into a compact
+//      array (kExCap values per round; one round in practice), and lanes
+//      0..2 fold the three channels in order;
+//  (4) lanes 0..5 of warp 0 run the pairwise strip tree (_core.pyx:300-311)
+//      for one component each and lanes 0..4 divide one component each.
 // Pipeline labels never spill, so the window holds every member.
-#ifndef SPX_EXROWS
-#define SPX_EXROWS 4  // 71 registers, 16 KB: more resident clusters than 8 rows
-#endif
-constexpr int kRows = SPX_EXROWS;
-constexpr int kCols = 96;  // window width 3S <= 96 (S <= 32)
 #ifndef SPX_EXW
 #define SPX_EXW 3
 #endif
@@ -647,18 +636,53 @@ constexpr int kCols = 96;  // window width 3S <= 96 (S <= 32)
 #define SPX_EXG 16
 #endif
 constexpr int kExWarps = SPX_EXW;  // 3 = n_bl for the default tile_len 16 (3S / 16 strips when S = 16)
+constexpr int kExCap = 256;        // compacted members per warp and fold round
 
+size_t exact_smem_bytes(int64_t s) {  // compact values + the window's labels
+  return (size_t)kExWarps * 3 * kExCap * sizeof(float) + (size_t)9 * s * s * sizeof(int32_t);
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+#ifdef SPX_EXACT_CLOCKS  // development: phase timestamps of the first blocks
+__device__ long long g_exclk[16][16];
+#define EXCLKW(i) if (threadIdx.x == 0 && blockIdx.x < 16 && item == (int)blockIdx.x) g_exclk[blockIdx.x][i] = clock64()
+#define EXCLK(i) if (threadIdx.x == 0 && blockIdx.x < 16 && item == (int)blockIdx.x) g_exclk[blockIdx.x][i] = clock64()
+#else
+#define EXCLK(i)
+#define EXCLKW(i)
+#endif
 __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p) {
+  extern __shared__ __align__(16) unsigned char ex_smem[];
   __shared__ double strips[32][6];
-  __shared__ float cv[kExWarps][3][kRows * kCols];  // compacted l / a / b
-  __shared__ int rstart[kExWarps][kRows + 1];
+  __shared__ double qv[6];
+  float* const cv_all = reinterpret_cast<float*>(ex_smem);  // [kExWarps][3][kExCap]
+  int32_t* const win = reinterpret_cast<int32_t*>(cv_all + kExWarps * 3 * kExCap);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* const cw = cv_all + warp * 3 * kExCap;
   const int K = p.ns_r * p.ns_c;
-  const int n = *p.worklist_n;
   const long long hw = (long long)p.h * p.w;
-  const unsigned lt = (1u << lane) - 1u;
+  const long long cap = (long long)p.frames * K;  // worklist capacity
+#ifdef SPX_EXACT_CLOCKS
+  if (threadIdx.x == 0 && blockIdx.x < 16) g_exclk[blockIdx.x][6] = clock64();
+#endif
+  // (1) independent loads: the count and this block's first item (in bounds)
+  const int n = *p.worklist_n;
+  int gk_next = (long long)blockIdx.x < cap ? p.worklist[blockIdx.x] : 0;
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
-    const int gk = p.worklist[item];
+    EXCLK(0);
+    const int gk = gk_next;
+    if (item + (long long)gridDim.x < n) gk_next = p.worklist[item + gridDim.x];
     const int ff = gk / K, fk = gk - ff * K;
     const float* im = p.img + (long long)ff * 3 * hw;  // planar [3][H][W]
     const int32_t* lb = p.labels + (long long)ff * hw;
@@ -666,125 +690,183 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
     const int gid = fk + p.row_off * p.ns_c;  // labels carry global ids
     const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
     const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
-    const int ww = wx1 - wx0;
-    const int ncb = (ww + 31) >> 5;  // column blocks of 32 (<= 3)
+    const int ya0 = max(ry0, 0);
+    const int ww = wx1 - wx0, wrows = ry1 - ya0;
+    // (2) the window's labels, one round trip
+    if (((wx0 | ww | p.w) & 3) == 0) {
+      const int q4 = ww >> 2;
+#pragma unroll 1
+      for (int i = threadIdx.x; i < wrows * q4; i += blockDim.x) {
+        const int rr = i / q4, cq = i - rr * q4;
+        cp_async16(win + rr * ww + 4 * cq, lb + (long long)(ya0 + rr) * p.w + wx0 + 4 * cq);
+      }
+    } else {
+#pragma unroll 1
+      for (int i = threadIdx.x; i < wrows * ww; i += blockDim.x) {
+        const int rr = i / ww, cc = i - rr * ww;
+        cp_async4(win + i, lb + (long long)(ya0 + rr) * p.w + wx0 + cc);
+      }
+    }
+#pragma unroll 1
     for (int i = threadIdx.x; i < p.n_bl * 6; i += blockDim.x) (&strips[0][0])[i] = 0.0;
+    cp_async_wait_all();
     __syncthreads();
+    EXCLK(1);
+    // (3) strips
+#pragma unroll 1
     for (int j = warp; j < p.n_bl; j += kExWarps) {
       const int ya = max(ry0 + j * p.tile_len, 0);
       const int yz = min(ry0 + (j + 1) * p.tile_len, ry1);
       if (ya >= yz) continue;  // warp-uniform
-      double acc = 0.0;
-      long long sx = 0, sy = 0, cnt = 0;  // lane 0
-      int32_t nxt[kRows][3];
-      auto load_block = [&](int yb, int32_t (&lv)[kRows][3]) {
-#pragma unroll
-        for (int rr = 0; rr < kRows; ++rr)
-#pragma unroll
-          for (int cb = 0; cb < 3; ++cb) {
-            const int col = cb * 32 + lane;
-            lv[rr][cb] = (yb + rr < yz && col < ww)
-                             ? __ldg(lb + (long long)(yb + rr) * p.w + wx0 + col)
-                             : -1;
-          }
-      };
-      load_block(ya, nxt);
-      for (int yb = ya; yb < yz; yb += kRows) {
-        int32_t lv[kRows][3];
-#pragma unroll
-        for (int rr = 0; rr < kRows; ++rr)
-#pragma unroll
-          for (int cb = 0; cb < 3; ++cb) lv[rr][cb] = nxt[rr][cb];
-        if (yb + kRows < yz) load_block(yb + kRows, nxt);  // prefetch the next block
-        const int rows = min(kRows, yz - yb);
-        int base = 0;
-#pragma unroll
-        for (int rr = 0; rr < kRows; ++rr) {
-          if (rr >= rows) break;
-          const int y = yb + rr;
-          if (lane == 0) rstart[warp][rr] = base;
-          int rx = 0, rn = 0;
-#pragma unroll
-          for (int cb = 0; cb < 3; ++cb) {
-            if (cb >= ncb) break;
-            const int col = cb * 32 + lane;
-            const bool m = lv[rr][cb] == gid;
-            const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
-            if (m) {
-              // asynchronous global -> shared copies: the block's value loads
-              // are all in flight together (one round trip per block)
-              const int pos = base + __popc(bm & lt);
-              const float* g = im + (long long)y * p.w + wx0 + col;
-              const unsigned d0 = (unsigned)__cvta_generic_to_shared(&cv[warp][0][pos]);
-              const unsigned d1 = (unsigned)__cvta_generic_to_shared(&cv[warp][1][pos]);
-              const unsigned d2 = (unsigned)__cvta_generic_to_shared(&cv[warp][2][pos]);
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d0), "l"(g));
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d1), "l"(g + hw));
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d2), "l"(g + 2 * hw));
-            }
-            rx += (int)__reduce_add_sync(0xFFFFFFFFu, m ? (unsigned)(wx0 + col) : 0u);
-            rn += __popc(bm);
-            base += __popc(bm);
-          }
-          if (lane == 0) {
-            sx += rx;
-            sy += (long long)(y + p.row_off * p.s) * rn;
-            cnt += rn;
-          }
+      double acc = 0.0;                           // lanes 0..2: channel fold
+      unsigned long long lx = 0, ly = 0, lc = 0;  // lane sums of x, global y, count
+#pragma unroll 1
+      for (int yc = ya; yc < yz; yc += 32) {  // chunks of <= 32 rows
+        const int rc = min(32, yz - yc);
+        const int g = 32 / rc;                 // segments per row
+        const int seg = (ww + g - 1) / g;
+        const int row = lane / g, sg = lane - row * g;
+        const bool own = row < rc;
+        const int c0 = own ? min(sg * seg, ww) : 0, c1 = own ? min(c0 + seg, ww) : 0;
+        const int y = yc + row;
+        const int32_t* wrow = win + (y - ya0) * ww;
+        // members of this lane's segment as a bit mask (segments <= 96 columns)
+        unsigned m0 = 0, m1 = 0, m2 = 0, sx = 0;
+        const int len = c1 - c0;
+#pragma unroll 4
+        for (int k = 0; k < len; ++k) {
+          const bool hit = wrow[c0 + k] == gid;
+          sx += hit ? (unsigned)(wx0 + c0 + k) : 0u;
+          if (k < 32) m0 |= (unsigned)hit << k;
+          else if (k < 64) m1 |= (unsigned)hit << (k - 32);
+          else m2 |= (unsigned)hit << (k - 64);
         }
-        if (lane == 0) rstart[warp][rows] = base;
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncwarp();
-        if (lane < 3) {
-          // row-major order within the strip; channel 0 carries the
-          // certified-sum flag in its sign bit: |L|
-          const float* src = cv[warp][lane];
-          const int b1 = rstart[warp][rows];
-          const bool l0 = lane == 0;
-          int i = 0;
-          for (; i + 4 <= b1; i += 4) {
-            float v0 = src[i], v1 = src[i + 1], v2 = src[i + 2], v3 = src[i + 3];
-            if (l0) {
-              v0 = fabsf(v0);
-              v1 = fabsf(v1);
-              v2 = fabsf(v2);
-              v3 = fabsf(v3);
-            }
-            acc = dadd(acc, (double)v0);
-            acc = dadd(acc, (double)v1);
-            acc = dadd(acc, (double)v2);
-            acc = dadd(acc, (double)v3);
-          }
-          for (; i < b1; ++i) acc = dadd(acc, (double)(l0 ? fabsf(src[i]) : src[i]));
+        const int cnt = __popc(m0) + __popc(m1) + __popc(m2);
+        EXCLKW(8);
+        lx += sx;
+        lc += (unsigned)cnt;
+        ly += (unsigned long long)cnt * (unsigned long long)(y + p.row_off * p.s);
+        // exclusive scan of the counts in lane (= row-major) order
+        int off = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xFFFFFFFFu, off, o);
+          if (lane >= o) off += t;
         }
-        __syncwarp();
+        const int total = __shfl_sync(0xFFFFFFFFu, off, 31);
+        off -= cnt;
+        EXCLKW(9);
+#pragma unroll 1
+        for (int base = 0; base < total; base += kExCap) {
+          if (cnt && off < base + kExCap && off + cnt > base) {
+            int o = off;
+            const float* g0 = im + (long long)y * p.w + wx0 + c0;
+#pragma unroll
+            for (int wd = 0; wd < 3; ++wd) {
+              unsigned mw = wd == 0 ? m0 : (wd == 1 ? m1 : m2);
+#pragma unroll 1
+              while (mw) {
+                const int k = 32 * wd + __ffs(mw) - 1;
+                mw &= mw - 1;
+                if (o >= base && o < base + kExCap) {
+                  cp_async4(cw + (o - base), g0 + k);
+                  cp_async4(cw + kExCap + (o - base), g0 + hw + k);
+                  cp_async4(cw + 2 * kExCap + (o - base), g0 + 2 * hw + k);
+                }
+                ++o;
+              }
+            }
+          }
+          EXCLKW(10);
+          cp_async_wait_all();
+          __syncwarp();
+          EXCLKW(11);
+          if (lane < 3) {
+            // row-major order; channel 0 carries the certified-sum flag in
+            // its sign bit: |L|
+            const float* src = cw + lane * kExCap;
+            const int m = min(kExCap, total - base);
+            const bool l0 = lane == 0;
+            int i = 0;
+#pragma unroll 4
+            for (; i + 4 <= m; i += 4) {
+              float v0 = src[i], v1 = src[i + 1], v2 = src[i + 2], v3 = src[i + 3];
+              if (l0) {
+                v0 = fabsf(v0);
+                v1 = fabsf(v1);
+                v2 = fabsf(v2);
+                v3 = fabsf(v3);
+              }
+              acc = dadd(acc, (double)v0);
+              acc = dadd(acc, (double)v1);
+              acc = dadd(acc, (double)v2);
+              acc = dadd(acc, (double)v3);
+            }
+#pragma unroll 1
+            for (; i < m; ++i) acc = dadd(acc, (double)(l0 ? fabsf(src[i]) : src[i]));
+          }
+          __syncwarp();
+          EXCLKW(12);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        lx += __shfl_xor_sync(0xFFFFFFFFu, lx, o);
+        ly += __shfl_xor_sync(0xFFFFFFFFu, ly, o);
+        lc += __shfl_xor_sync(0xFFFFFFFFu, lc, o);
       }
       if (lane < 3) strips[j][lane] = acc;
       if (lane == 0) {
-        strips[j][3] = (double)sx;
-        strips[j][4] = (double)sy;
-        strips[j][5] = (double)cnt;
+        strips[j][3] = (double)lx;
+        strips[j][4] = (double)ly;
+        strips[j][5] = (double)lc;
       }
     }
+    EXCLK(2);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int m = p.n_bl;
-      while (m > 1) {  // pairwise strip tree, _core.pyx:300-311
-        int half = m >> 1;
-        for (int i = 0; i < half; ++i)
-          for (int comp = 0; comp < 6; ++comp)
-            strips[i][comp] = dadd(strips[2 * i][comp], strips[2 * i + 1][comp]);
-        if (m & 1)
-          for (int comp = 0; comp < 6; ++comp) strips[half][comp] = strips[m - 1][comp];
-        m = half + (m & 1);
+    EXCLK(3);
+    // (4) warp 0: lane t < 6 runs the pairwise strip tree of component t,
+    // lanes 0..4 divide, lane 0 stores
+    if (warp == 0) {
+      if (lane < 6) {
+        int m = p.n_bl;
+#pragma unroll 1
+        while (m > 1) {  // pairwise strip tree, _core.pyx:300-311
+          const int half = m >> 1;
+#pragma unroll 1
+          for (int i = 0; i < half; ++i)
+            strips[i][lane] = dadd(strips[2 * i][lane], strips[2 * i + 1][lane]);
+          if (m & 1) strips[half][lane] = strips[m - 1][lane];
+          m = half + (m & 1);
+        }
       }
-      write_centre(p, gk, r, c, strips[0][5], strips[0][0], strips[0][1], strips[0][2],
-                   strips[0][3], strips[0][4]);
+      __syncwarp();
+      const double cnt = strips[0][5];
+      if (lane < 5) {
+        double q;
+        if (cnt > 0.0) {
+          q = ddiv(strips[0][lane], cnt);
+        } else {  // empty: keep the previous centre
+          q = lane < 3 ? p.prev_lab[3LL * gk + lane] : p.prev_xy[2LL * gk + (lane - 3)];
+        }
+        qv[lane] = q;
+      }
+      __syncwarp();
+      EXCLK(4);
+      if (lane == 0) write_centre(p, gk, r, c, cnt, qv);
+      EXCLK(5);
     }
-    __syncthreads();
+    __syncthreads();  // the window and strips are reused by the next item
   }
 }
 
+#ifdef SPX_EXACT_CLOCKS
+}  // namespace
+int spx_debug_exact_clocks(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_exclk, sizeof(g_exclk));
+}
+namespace {
+#endif
 __global__ void k_fill_i32(int32_t* v, int n, int value) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = value;
@@ -958,7 +1040,7 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   // launches get a small grid (an empty block still costs its scheduling)
   const long long ex_blocks = std::max<long long>(
       num_sms(), std::min<long long>((long long)num_sms() * SPX_EXG, nk * frames / 64));
-  k_exact_clusters<<<(unsigned)ex_blocks, kExWarps * 32, 0, st>>>(p);
+  k_exact_clusters<<<(unsigned)ex_blocks, kExWarps * 32, exact_smem_bytes(s), st>>>(p);
   SPX_LAUNCH_CHECK("k_exact_clusters");
   return SPX_OK;
 }
