@@ -74,6 +74,8 @@ struct CellParams {
   int32_t* labels;         // [F][H][W]
   ClusterAcc* acc;         // [F][K]     (ACC only) atomically accumulated sums
   const int32_t* done;     // per frame, skip == 1 (may be null)
+  int32_t* wl;             // (ACC, may be null) flagged clusters are appended here
+  int32_t* wl_n;           //   by their first flagged contribution
   int h, w, s, ns_r, ns_c, frames;
   int cr0, cr1;            // cell rows processed (local grid)
   int row_off;             // global cell row of local row 0 (strips; 0 otherwise)
@@ -420,7 +422,15 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
               const unsigned long long flg = (tot >> 11) & 2047ull;
               atomicAdd(&o->sx, ((tot >> 22) & 0x1FFFFFull) + cnt * (unsigned long long)x_cell);
               atomicAdd(&o->sy, (tot >> 43) + cnt * (unsigned long long)y_glob0);
-              atomicAdd(&o->cf, cnt | (flg << 32));
+              const unsigned long long add = cnt | (flg << 32);
+              if (p.wl && flg) {
+                // the contribution that turns the cluster's flag count
+                // nonzero enqueues it for k_exact_clusters (exactly once)
+                if ((atomicAdd(&o->cf, add) >> 32) == 0)
+                  p.wl[atomicAdd(p.wl_n, 1)] = (int32_t)((long long)f * K + cand_k[col - 27]);
+              } else {
+                atomicAdd(&o->cf, add);
+              }
             }
           }
         }
@@ -471,6 +481,8 @@ struct ReduceParams {
   const int32_t* done;
   int32_t* worklist;       // flagged clusters (global index f*K + k)
   int32_t* worklist_n;
+  int32_t* wl_reset;       // (may be null) zeroed by k_reduce_cells: the next pass's count
+  bool append;             // k_reduce_cells enqueues flagged clusters (else k_cell did)
   int h, w, s, ns_r, ns_c, frames, n_bl, tile_len;
   int kr0, kr1;            // cluster rows reduced (local grid)
   int row_off;             // global cell row of local row 0
@@ -547,8 +559,8 @@ __device__ __forceinline__ void centre_values(const ReduceParams& p, long long g
 // _core.pyx:313-320; the block's 128 consecutive clusters are staged in
 // shared memory and written out with coalesced 16-byte stores (the per-
 // cluster AoS records would otherwise leave as 8 scattered stores per
-// thread).  Flagged clusters get placeholder values here and are rewritten
-// by k_exact_clusters, which runs after this kernel.
+// thread).  Flagged clusters are left to k_exact_clusters (which may run
+// concurrently on another stream).
 constexpr int kRedT = 128;
 #ifndef SPX_REDPER
 #define SPX_REDPER 1
@@ -561,6 +573,8 @@ __global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
   __shared__ __align__(16) double s_lab[kRedN * 3];
   __shared__ __align__(16) long long s_cnt[kRedN];
   __shared__ __align__(16) CRec s_rec[kRedN];
+  __shared__ bool s_fl[kRedN];  // flagged: k_exact_clusters owns its outputs
+  if (p.wl_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *p.wl_reset = 0;
   const int K = p.ns_r * p.ns_c;
   const int nk = (p.kr1 - p.kr0) * p.ns_c;
   const int f = blockIdx.y;
@@ -593,23 +607,29 @@ __global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
     *reinterpret_cast<ulonglong2*>(&a->sy) = make_ulonglong2(0ull, 0ull);
     const unsigned long long sx = (unsigned long long)__double_as_longlong(s012[c].w);
     const unsigned long long cnt = syc[c].y & 0xFFFFFFFFull, fl = syc[c].y >> 32;
-    if (fl != 0) p.worklist[atomicAdd(p.worklist_n, 1)] = (int32_t)gk;
+    if (fl != 0 && p.append) p.worklist[atomicAdd(p.worklist_n, 1)] = (int32_t)gk;
+    s_fl[i] = fl != 0;
     centre_values(p, gk, kr, kc, (double)cnt, s012[c].x, s012[c].y, s012[c].z, (double)sx,
                   (double)syc[c].x, s_xy + 2 * i, s_lab + 3 * i, s_rec[i]);
     s_cnt[i] = (long long)cnt;
   }
   __syncthreads();
-  // coalesced copies of the block's contiguous output ranges
+  // coalesced copies of the block's contiguous output ranges, flagged
+  // clusters skipped (k_exact_clusters may run concurrently and owns them)
   {
     const double2* sx2 = reinterpret_cast<const double2*>(s_xy);
     double2* gx2 = reinterpret_cast<double2*>(p.out_xy + 2 * gk0);
-    for (int i = t; i < n; i += kRedT) gx2[i] = sx2[i];
+    for (int i = t; i < n; i += kRedT)
+      if (!s_fl[i]) gx2[i] = sx2[i];
     double* gl = p.out_lab + 3 * gk0;
-    for (int i = t; i < 3 * n; i += kRedT) gl[i] = s_lab[i];
-    for (int i = t; i < n; i += kRedT) p.counts[gk0 + i] = s_cnt[i];
+    for (int i = t; i < 3 * n; i += kRedT)
+      if (!s_fl[i / 3]) gl[i] = s_lab[i];
+    for (int i = t; i < n; i += kRedT)
+      if (!s_fl[i]) p.counts[gk0 + i] = s_cnt[i];
     const float4* sr = reinterpret_cast<const float4*>(s_rec);
     float4* gr = reinterpret_cast<float4*>(p.rec + gk0);
-    for (int i = t; i < 2 * n; i += kRedT) gr[i] = sr[i];
+    for (int i = t; i < 2 * n; i += kRedT)
+      if (!s_fl[i >> 1]) gr[i] = sr[i];
   }
 }
 
@@ -684,6 +704,9 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
     const int gk = gk_next;
     if (item + (long long)gridDim.x < n) gk_next = p.worklist[item + gridDim.x];
     const int ff = gk / K, fk = gk - ff * K;
+    // a frame that stopped early has no update this pass (k_cell enqueued its
+    // clusters during its final association)
+    if (p.done && p.done[ff]) continue;  // block-uniform
     const float* im = p.img + (long long)ff * 3 * hw;  // planar [3][H][W]
     const int32_t* lb = p.labels + (long long)ff * hw;
     const int r = fk / p.ns_c, c = fk - r * p.ns_c;
@@ -937,8 +960,11 @@ void assoc_bound_coefficients(double xy_weight, float& w32, float& k_mp, float& 
 int launch_cell(const float* img, const double* cxy, const double* clab, const CRec* rec,
                 int32_t* labels, ClusterAcc* sums, const int32_t* done, int64_t h, int64_t w,
                 int64_t s, int64_t ns_r, int64_t ns_c, double xy_weight, int frames, bool acc,
-                cudaStream_t st, int64_t cr0, int64_t cr1, int64_t row_off) {
+                cudaStream_t st, int64_t cr0, int64_t cr1, int64_t row_off, int32_t* wl,
+                int32_t* wl_n) {
   CellParams p;
+  p.wl = wl;
+  p.wl_n = wl_n;
   p.img = img;
   p.cxy = cxy;
   p.clab = clab;
@@ -1001,8 +1027,11 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
                         double* out_lab, int64_t* counts, CRec* rec, const int32_t* done,
                         int32_t* worklist, int32_t* worklist_n, int64_t h, int64_t w, int64_t s,
                         int64_t ns_r, int64_t ns_c, int64_t tile_len, int frames,
-                        cudaStream_t st, int64_t kr0, int64_t kr1, int64_t row_off) {
+                        cudaStream_t st, int64_t kr0, int64_t kr1, int64_t row_off, int mode,
+                        int32_t* wl_reset) {
   ReduceParams p;
+  p.wl_reset = wl_reset;
+  p.append = mode == kReduceAndExact;
   p.acc = acc;
   p.img = img;
   p.labels = labels;
@@ -1028,14 +1057,17 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   p.kr1 = (int)kr1;
   p.row_off = (int)row_off;
   const long long nk = (kr1 - kr0) * ns_c;
-  SPX_CUDA(cudaMemsetAsync(worklist_n, 0, sizeof(int32_t), st));
+  if (mode == kReduceAndExact) SPX_CUDA(cudaMemsetAsync(worklist_n, 0, sizeof(int32_t), st));
   if (nk <= 0 || frames <= 0) return SPX_OK;
   if (frames > 65535) {
     set_error("k_reduce_cells: at most 65535 frames per launch");
     return SPX_ERR_VALUE;
   }
-  k_reduce_cells<<<dim3((unsigned)ceil_div(nk, kRedN), (unsigned)frames), kRedT, 0, st>>>(p);
-  SPX_LAUNCH_CHECK("k_reduce_cells");
+  if (mode != kExactOnly) {
+    k_reduce_cells<<<dim3((unsigned)ceil_div(nk, kRedN), (unsigned)frames), kRedT, 0, st>>>(p);
+    SPX_LAUNCH_CHECK("k_reduce_cells");
+  }
+  if (mode == kReduceOnly) return SPX_OK;
   // grid-stride over the worklist; ~0.5% of clusters are flagged, so small
   // launches get a small grid (an empty block still costs its scheduling)
   const long long ex_blocks = std::max<long long>(

@@ -30,15 +30,8 @@ int launch_weak2(const int32_t*, int32_t*, int64_t, int64_t, int, cudaStream_t, 
 int launch_strict(const int32_t*, int32_t*, int64_t, int64_t, int, int64_t, int64_t, int32_t*,
                   int32_t*, int32_t*, int32_t*, cudaStream_t);
 bool cell_path_ok(int64_t, int64_t, int64_t, int64_t);
-int launch_cell(const float*, const double*, const double*, const CRec*, int32_t*, ClusterAcc*,
-                const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, double, int, bool,
-                cudaStream_t, int64_t, int64_t, int64_t);
 int launch_records(const double*, const double*, CRec*, int64_t, int64_t, int64_t, int,
                    cudaStream_t, int64_t, int64_t, int64_t);
-int launch_reduce_cells(ClusterAcc*, const float*, const int32_t*, const double*, const double*,
-                        double*, double*, int64_t*, CRec*, const int32_t*, int32_t*, int32_t*,
-                        int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t,
-                        int64_t, int64_t, int64_t);
 int launch_fill_i32(int32_t*, int, int, cudaStream_t);
 
 namespace {
@@ -82,6 +75,11 @@ struct Engine {
   CRec* rec = nullptr;   // fp32 filter records of the current centres (cell path)
   ClusterAcc* acc = nullptr;  // per-cluster update accumulators (cell path)
   int32_t* worklist = nullptr;  // flagged clusters for the exact fallback (cell path)
+  int32_t* wl_n = nullptr;      // two worklist counts (pass parity), after the list
+  // The exact fallback runs on a side stream, concurrently with the reduce
+  // (both only need the association pass): fork / join events.
+  cudaStream_t s_side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool use_cell = false;
   cudaEvent_t ev[EV_FIXED] = {};
   std::vector<cudaEvent_t> ev_assoc, ev_update;  // start/end pairs
@@ -99,6 +97,9 @@ struct Engine {
       if (e) cudaEventDestroy(e);
     for (auto e : ev_assoc) cudaEventDestroy(e);
     for (auto e : ev_update) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (s_side) cudaStreamDestroy(s_side);
     free_graphs();
     free_staging();
   }
@@ -132,7 +133,11 @@ struct Engine {
     if (use_cell) {
       SPX_CUDA(cudaMalloc(&rec, B * K * sizeof(CRec)));
       SPX_CUDA(cudaMalloc(&acc, B * K * sizeof(ClusterAcc)));
-      SPX_CUDA(cudaMalloc(&worklist, (B * K + 1) * sizeof(int32_t)));
+      SPX_CUDA(cudaMalloc(&worklist, (B * K + 2) * sizeof(int32_t)));
+      wl_n = worklist + B * K;
+      SPX_CUDA(cudaStreamCreateWithFlags(&s_side, cudaStreamNonBlocking));
+      SPX_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      SPX_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     } else {
       SPX_CUDA(cudaMalloc(&slab, B * K * n_bl * 6 * sizeof(double)));
     }
@@ -157,11 +162,14 @@ struct Engine {
     return v[i];
   }
 
-  int associate(int cur, int frames, const int32_t* dn, bool with_update, cudaStream_t s) {
+  // Association pass `pass` (0-based); with_update passes enqueue their
+  // flagged clusters into the worklist under count wl_n[pass & 1].
+  int associate(int cur, int frames, const int32_t* dn, bool with_update, int pass,
+                cudaStream_t s) {
     stage_mark(pass_event(ev_assoc, 2 * n_assoc), s);
     int rc = use_cell ? launch_cell(lab, cxy[cur], clab[cur], rec, labels, acc, dn, st.height,
                                     st.width, st.s, st.ns_r, st.ns_c, xy_weight, frames,
-                                    with_update, s, 0, -1, 0)
+                                    with_update, s, 0, -1, 0, worklist, wl_n + (pass & 1))
                       : launch_assoc(lab, cxy[cur], clab[cur], labels, dn, st.height, st.width,
                                      st.s, st.ns_r, st.ns_c, xy_weight, 0, st.height, frames, K, s);
     stage_mark(pass_event(ev_assoc, 2 * n_assoc + 1), s);
@@ -322,15 +330,27 @@ struct Engine {
       SPX_CUDA(cudaMemsetAsync(done, 0, B * sizeof(int32_t), s));
     }
     int cur = 0, nxt = 1;
-    if ((rc = associate(cur, B, dn, true, s))) return rc;
+    if (use_cell) SPX_CUDA(cudaMemsetAsync(wl_n, 0, 2 * sizeof(int32_t), s));
+    if ((rc = associate(cur, B, dn, true, 0, s))) return rc;
     for (int it = 0; it < st.no_iters; ++it) {
       stage_mark(pass_event(ev_update, 2 * n_update), s);
       if (use_cell) {
+        // fork: the exact fallback (pass `it`'s worklist) on the side stream,
+        // the reduce (which also zeroes the next pass's count) here; join
+        SPX_CUDA(cudaEventRecord(ev_fork, s));
+        SPX_CUDA(cudaStreamWaitEvent(s_side, ev_fork, 0));
         if ((rc = launch_reduce_cells(acc, lab, labels, cxy[cur], clab[cur], cxy[nxt], clab[nxt],
-                                      out_counts, rec, dn, worklist, worklist + max_batch * K,
-                                      st.height, st.width, st.s, st.ns_r, st.ns_c, st.tile_len, B,
-                                      s, 0, -1, 0)))
+                                      out_counts, rec, dn, worklist, wl_n + (it & 1), st.height,
+                                      st.width, st.s, st.ns_r, st.ns_c, st.tile_len, B, s_side,
+                                      0, -1, 0, kExactOnly)))
           return rc;
+        SPX_CUDA(cudaEventRecord(ev_join, s_side));
+        if ((rc = launch_reduce_cells(acc, lab, labels, cxy[cur], clab[cur], cxy[nxt], clab[nxt],
+                                      out_counts, rec, dn, worklist, wl_n + (it & 1), st.height,
+                                      st.width, st.s, st.ns_r, st.ns_c, st.tile_len, B, s, 0, -1,
+                                      0, kReduceOnly, wl_n + ((it + 1) & 1))))
+          return rc;
+        SPX_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
         launches += 2;
       } else {
         if ((rc = launch_accum_range(lab, labels, st.height, st.width, slab, n_bl, st.s, st.ns_c,
@@ -351,7 +371,7 @@ struct Engine {
       }
       std::swap(cur, nxt);
       const bool more = it + 1 < st.no_iters;
-      if ((rc = associate(cur, B, dn, more, s))) return rc;
+      if ((rc = associate(cur, B, dn, more, it + 1, s))) return rc;
       if (early) {
         if ((rc = launch_commit_done(done, B, s))) return rc;
         ++launches;

@@ -29,15 +29,8 @@ namespace spx {
 int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
 int launch_init(const float*, int64_t, int64_t, int64_t, int64_t, double*, double*, int64_t,
                 int64_t, int64_t, int, int, int, cudaStream_t, int, int64_t, int64_t);
-int launch_cell(const float*, const double*, const double*, const CRec*, int32_t*, ClusterAcc*,
-                const int32_t*, int64_t, int64_t, int64_t, int64_t, int64_t, double, int, bool,
-                cudaStream_t, int64_t, int64_t, int64_t);
 int launch_records(const double*, const double*, CRec*, int64_t, int64_t, int64_t, int,
                    cudaStream_t, int64_t, int64_t, int64_t);
-int launch_reduce_cells(ClusterAcc*, const float*, const int32_t*, const double*, const double*,
-                        double*, double*, int64_t*, CRec*, const int32_t*, int32_t*, int32_t*,
-                        int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, cudaStream_t,
-                        int64_t, int64_t, int64_t);
 int launch_weak2(const int32_t*, int32_t*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
 bool cell_path_ok(int64_t, int64_t, int64_t, int64_t);
 
