@@ -754,15 +754,20 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
         const int y = yc + row;
         const int32_t* wrow = win + (y - ya0) * ww;
         // members of this lane's segment as a bit mask (segments <= 96 columns)
+        // (each row starts its walk at a different column: with the window's
+        // 16 (mod 32)-word row stride, lanes of different rows would
+        // otherwise hit the same shared-memory banks)
         unsigned m0 = 0, m1 = 0, m2 = 0, sx = 0;
         const int len = c1 - c0;
+        int k = len ? row % len : 0;
 #pragma unroll 4
-        for (int k = 0; k < len; ++k) {
+        for (int n_ = 0; n_ < len; ++n_) {
           const bool hit = wrow[c0 + k] == gid;
           sx += hit ? (unsigned)(wx0 + c0 + k) : 0u;
           if (k < 32) m0 |= (unsigned)hit << k;
           else if (k < 64) m1 |= (unsigned)hit << (k - 32);
           else m2 |= (unsigned)hit << (k - 64);
+          k = k + 1 == len ? 0 : k + 1;
         }
         const int cnt = __popc(m0) + __popc(m1) + __popc(m2);
         EXCLKW(8);
