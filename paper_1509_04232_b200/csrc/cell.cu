@@ -62,7 +62,6 @@ __device__ __forceinline__ float sqa(float x) {
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-__device__ __forceinline__ bool fin_small(double v) { return fabs(v) < 1e15; }
 
 }  // namespace
 
@@ -452,19 +451,9 @@ __global__ void k_records(const double* __restrict__ cxy, const double* __restri
   const long long f = j / nk;
   int k = k0 + (int)(j % nk);
   const long long i = f * k_per_frame + k;
-  int kr = k / ns_c + row_off, kc = k % ns_c;
-  double x = cxy[2 * i], y = cxy[2 * i + 1];
-  double l = clab[3 * i], a = clab[3 * i + 1], b = clab[3 * i + 2];
-  CRec r;
-  r.l = __double2float_rn(l);
-  r.a = __double2float_rn(a);
-  r.b = __double2float_rn(b);
-  r.xr = __double2float_rn(dsub(x, (double)kc * s));
-  r.yr = __double2float_rn(dsub(y, (double)kr * s));
-  bool ok = fin_small(x) && fin_small(y) && fin_small(l) && fin_small(a) && fin_small(b);
-  r.mag_lab = fmaxf(fabsf(r.l), fmaxf(fabsf(r.a), fabsf(r.b)));
-  r.mag_xy = fmaxf(fabsf(r.xr), fabsf(r.yr));
-  r.ok = ok ? 1.f : 0.f;
+  const int kr = k / ns_c + row_off, kc = k % ns_c;
+  const CRec r = make_record(cxy[2 * i], cxy[2 * i + 1], clab[3 * i], clab[3 * i + 1],
+                             clab[3 * i + 2], kr, kc, s);
   rec[i] = r;
 }
 
@@ -500,15 +489,7 @@ __device__ __forceinline__ void write_centre(const ReduceParams& p, long long gk
   p.out_xy[2 * gk] = x;
   p.out_xy[2 * gk + 1] = y;
   p.counts[gk] = (int64_t)cnt;
-  CRec r;
-  r.l = __double2float_rn(l);
-  r.a = __double2float_rn(a);
-  r.b = __double2float_rn(b);
-  r.xr = __double2float_rn(dsub(x, (double)kc * p.s));
-  r.yr = __double2float_rn(dsub(y, (double)(kr + p.row_off) * p.s));
-  r.mag_lab = fmaxf(fabsf(r.l), fmaxf(fabsf(r.a), fabsf(r.b)));
-  r.mag_xy = fmaxf(fabsf(r.xr), fabsf(r.yr));
-  r.ok = (fin_small(x) && fin_small(y) && fin_small(l) && fin_small(a) && fin_small(b)) ? 1.f : 0.f;
+  const CRec r = make_record(x, y, l, a, b, kr + p.row_off, kc, p.s);
   p.rec[gk] = r;
 }
 

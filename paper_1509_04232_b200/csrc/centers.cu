@@ -2,6 +2,8 @@
 // reduction and the early-stop shift.  One thread per cluster: these are
 // O(K) stages (K = 1,200 clusters per 640x480 frame) whose cost is a few
 // reads per cluster; batching frames gives the parallelism.
+#include <algorithm>
+
 #include "spx_internal.cuh"
 
 namespace spx {
@@ -53,9 +55,11 @@ __device__ __forceinline__ void perturb_one(const LabView& im, int64_t h, int64_
 __global__ void k_init(const float* __restrict__ img, int64_t h, int64_t w, int64_t s,
                        int64_t ns_c, double* __restrict__ cxy, double* __restrict__ clab,
                        int64_t k0, int64_t k1, int64_t k_stride, int frames, int perturb,
-                       int do_init, int planar, int64_t hl, int64_t row_off) {
+                       int do_init, int planar, int64_t hl, int64_t row_off, CRec* rec,
+                       ClusterAcc* acc, int32_t* zero_ints, int n_zero) {
   int64_t nk = k1 - k0;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_zero) zero_ints[i] = 0;
   if (i >= nk * frames) return;
   int64_t f = i / nk;
   int64_t k = k0 + i % nk;
@@ -76,17 +80,22 @@ __global__ void k_init(const float* __restrict__ img, int64_t h, int64_t w, int6
     lab[2] = im.get(iy, ix, 2);
   }
   if (perturb) perturb_one(im, h, w, xy, lab);
+  if (rec)
+    rec[f * k_stride + k] = make_record(xy[0], xy[1], lab[0], lab[1], lab[2],
+                                        (int)(k / ns_c + row_off), (int)(k % ns_c), (int)s);
+  if (acc) acc[f * k_stride + k] = ClusterAcc{};
 }
 
 int launch_init(const float* img, int64_t h, int64_t w, int64_t s, int64_t ns_c, double* cxy,
                 double* clab, int64_t k0, int64_t k1, int64_t k_stride, int frames, int perturb,
-                int do_init, cudaStream_t st, int planar, int64_t hl, int64_t row_off) {
-  int64_t n = (k1 - k0) * frames;
+                int do_init, cudaStream_t st, int planar, int64_t hl, int64_t row_off,
+                CRec* rec, ClusterAcc* acc, int32_t* zero_ints, int n_zero) {
+  int64_t n = std::max<int64_t>((k1 - k0) * frames, n_zero);
   if (n <= 0) return SPX_OK;
   if (hl < 0) hl = h;
   k_init<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(img, h, w, s, ns_c, cxy, clab, k0, k1,
                                                      k_stride, frames, perturb, do_init, planar,
-                                                     hl, row_off);
+                                                     hl, row_off, rec, acc, zero_ints, n_zero);
   SPX_LAUNCH_CHECK("k_init");
   return SPX_OK;
 }

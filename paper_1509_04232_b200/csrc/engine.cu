@@ -13,8 +13,6 @@
 
 namespace spx {
 int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
-int launch_init(const float*, int64_t, int64_t, int64_t, int64_t, double*, double*, int64_t,
-                int64_t, int64_t, int, int, int, cudaStream_t, int, int64_t, int64_t);
 int launch_assoc(const float*, const double*, const double*, int32_t*, const int32_t*, int64_t,
                  int64_t, int64_t, int64_t, int64_t, double, int64_t, int64_t, int, int64_t,
                  cudaStream_t);
@@ -30,20 +28,20 @@ int launch_weak2(const int32_t*, int32_t*, int64_t, int64_t, int, cudaStream_t, 
 int launch_strict(const int32_t*, int32_t*, int64_t, int64_t, int, int64_t, int64_t, int32_t*,
                   int32_t*, int32_t*, int32_t*, cudaStream_t);
 bool cell_path_ok(int64_t, int64_t, int64_t, int64_t);
-int launch_records(const double*, const double*, CRec*, int64_t, int64_t, int64_t, int,
-                   cudaStream_t, int64_t, int64_t, int64_t);
-int launch_fill_i32(int32_t*, int, int, cudaStream_t);
 
 namespace {
 
 __global__ void k_gather_centres(const double* __restrict__ xy0, const double* __restrict__ lab0,
                                  const double* __restrict__ xy1, const double* __restrict__ lab1,
-                                 const int32_t* __restrict__ passes, int64_t k, int frames,
-                                 double* __restrict__ out_xy, double* __restrict__ out_lab) {
+                                 const int32_t* __restrict__ passes, int fixed_passes, int64_t k,
+                                 int frames, double* __restrict__ out_xy,
+                                 double* __restrict__ out_lab, int32_t* __restrict__ out_passes) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= k * frames) return;
   int64_t f = i / k;
-  bool one = passes && (passes[f] & 1);
+  const int np = passes ? passes[f] : fixed_passes;
+  if (out_passes && i == f * k) out_passes[f] = np;
+  const bool one = np & 1;
   const double* sx = one ? xy1 : xy0;
   const double* sl = one ? lab1 : lab0;
   out_xy[2 * i] = sx[2 * i];
@@ -307,22 +305,24 @@ struct Engine {
       return rc;
     ++launches;
     stage_mark(ev[EV_CONVERT], s);
+    // The last init launch also writes the fp32 records (cell path), clears
+    // the accumulators and zeroes the two worklist counts.
+    CRec* i_rec = use_cell ? rec : nullptr;
+    ClusterAcc* i_acc = use_cell ? acc : nullptr;
+    int32_t* i_zero = use_cell ? wl_n : nullptr;
+    const int i_nz = use_cell ? 2 : 0;
+    const bool pert = st.perturb;
     if ((rc = launch_init(lab, st.height, st.width, st.s, st.ns_c, cxy[0], clab[0], 0, K, K, B, 0,
-                          1, s, use_cell, -1, 0)))
+                          1, s, use_cell, -1, 0, pert ? nullptr : i_rec, pert ? nullptr : i_acc,
+                          pert ? nullptr : i_zero, pert ? 0 : i_nz)))
       return rc;
     ++launches;
     stage_mark(ev[EV_INIT], s);
-    if (st.perturb) {
+    if (pert) {
       if ((rc = launch_init(lab, st.height, st.width, st.s, st.ns_c, cxy[0], clab[0], 0, K, K, B,
-                            1, 0, s, use_cell, -1, 0)))
+                            1, 0, s, use_cell, -1, 0, i_rec, i_acc, i_zero, i_nz)))
         return rc;
       ++launches;
-    }
-    if (use_cell) {
-      if ((rc = launch_records(cxy[0], clab[0], rec, st.ns_r, st.ns_c, st.s, B, s, 0, -1, 0)))
-        return rc;
-      ++launches;
-      SPX_CUDA(cudaMemsetAsync(acc, 0, (size_t)B * K * sizeof(ClusterAcc), s));
     }
     stage_mark(ev[EV_PERTURB], s);
     if (early) {
@@ -330,7 +330,6 @@ struct Engine {
       SPX_CUDA(cudaMemsetAsync(done, 0, B * sizeof(int32_t), s));
     }
     int cur = 0, nxt = 1;
-    if (use_cell) SPX_CUDA(cudaMemsetAsync(wl_n, 0, 2 * sizeof(int32_t), s));
     if ((rc = associate(cur, B, dn, true, 0, s))) return rc;
     for (int it = 0; it < st.no_iters; ++it) {
       stage_mark(pass_event(ev_update, 2 * n_update), s);
@@ -393,18 +392,14 @@ struct Engine {
                                cudaMemcpyDeviceToDevice, s));
     }
     stage_mark(ev[EV_END], s);
-    if (!early) {
-      if ((rc = launch_fill_i32(passes, B, st.no_iters, s))) return rc;
-      ++launches;
-    }
-    // Final centres: frame f ends in buffer passes[f] & 1 (ping-pong, engine.py:197).
+    // Final centres: frame f ends in buffer passes[f] & 1 (ping-pong,
+    // engine.py:197; without early stop every frame ran no_iters passes).
+    // The same launch writes the per-frame pass counts.
     k_gather_centres<<<(unsigned)ceil_div(K * B, 256), 256, 0, s>>>(
-        cxy[0], clab[0], cxy[1], clab[1], passes, K, B, out_xy, out_lab);
+        cxy[0], clab[0], cxy[1], clab[1], early ? passes : nullptr, early ? -1 : (int)st.no_iters,
+        K, B, out_xy, out_lab, out_passes);
     SPX_LAUNCH_CHECK("k_gather_centres");
     ++launches;
-    if (out_passes)
-      SPX_CUDA(cudaMemcpyAsync(out_passes, passes, B * sizeof(int32_t), cudaMemcpyDeviceToDevice,
-                               s));
     return SPX_OK;
   }
 

@@ -12,8 +12,6 @@
 
 namespace spx {
 int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
-int launch_init(const float*, int64_t, int64_t, int64_t, int64_t, double*, double*, int64_t,
-                int64_t, int64_t, int, int, int, cudaStream_t, int, int64_t, int64_t);
 int launch_records(const double*, const double*, CRec*, int64_t, int64_t, int64_t, int,
                    cudaStream_t, int64_t, int64_t, int64_t);
 }  // namespace spx
