@@ -655,14 +655,6 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-#ifdef SPX_EXACT_CLOCKS  // development: phase timestamps of the first blocks
-__device__ long long g_exclk[16][16];
-#define EXCLKW(i) if (threadIdx.x == 0 && blockIdx.x < 16 && item == (int)blockIdx.x) g_exclk[blockIdx.x][i] = clock64()
-#define EXCLK(i) if (threadIdx.x == 0 && blockIdx.x < 16 && item == (int)blockIdx.x) g_exclk[blockIdx.x][i] = clock64()
-#else
-#define EXCLK(i)
-#define EXCLKW(i)
-#endif
 __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p) {
   extern __shared__ __align__(16) unsigned char ex_smem[];
   __shared__ double strips[32][6];
@@ -674,14 +666,10 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
   const int K = p.ns_r * p.ns_c;
   const long long hw = (long long)p.h * p.w;
   const long long cap = (long long)p.frames * K;  // worklist capacity
-#ifdef SPX_EXACT_CLOCKS
-  if (threadIdx.x == 0 && blockIdx.x < 16) g_exclk[blockIdx.x][6] = clock64();
-#endif
   // (1) independent loads: the count and this block's first item (in bounds)
   const int n = *p.worklist_n;
   int gk_next = (long long)blockIdx.x < cap ? p.worklist[blockIdx.x] : 0;
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
-    EXCLK(0);
     const int gk = gk_next;
     if (item + (long long)gridDim.x < n) gk_next = p.worklist[item + gridDim.x];
     const int ff = gk / K, fk = gk - ff * K;
@@ -715,7 +703,6 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
     for (int i = threadIdx.x; i < p.n_bl * 6; i += blockDim.x) (&strips[0][0])[i] = 0.0;
     cp_async_wait_all();
     __syncthreads();
-    EXCLK(1);
     // (3) strips
 #pragma unroll 1
     for (int j = warp; j < p.n_bl; j += kExWarps) {
@@ -751,7 +738,6 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
           k = k + 1 == len ? 0 : k + 1;
         }
         const int cnt = __popc(m0) + __popc(m1) + __popc(m2);
-        EXCLKW(8);
         lx += sx;
         lc += (unsigned)cnt;
         ly += (unsigned long long)cnt * (unsigned long long)(y + p.row_off * p.s);
@@ -764,7 +750,6 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
         }
         const int total = __shfl_sync(0xFFFFFFFFu, off, 31);
         off -= cnt;
-        EXCLKW(9);
 #pragma unroll 1
         for (int base = 0; base < total; base += kExCap) {
           if (cnt && off < base + kExCap && off + cnt > base) {
@@ -786,10 +771,8 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
               }
             }
           }
-          EXCLKW(10);
           cp_async_wait_all();
           __syncwarp();
-          EXCLKW(11);
           if (lane < 3) {
             // row-major order; channel 0 carries the certified-sum flag in
             // its sign bit: |L|
@@ -815,7 +798,6 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
             for (; i < m; ++i) acc = dadd(acc, (double)(l0 ? fabsf(src[i]) : src[i]));
           }
           __syncwarp();
-          EXCLKW(12);
         }
       }
 #pragma unroll
@@ -831,9 +813,7 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
         strips[j][5] = (double)lc;
       }
     }
-    EXCLK(2);
     __syncthreads();
-    EXCLK(3);
     // (4) warp 0: lane t < 6 runs the pairwise strip tree of component t,
     // lanes 0..4 divide, lane 0 stores
     if (warp == 0) {
@@ -861,25 +841,12 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
         qv[lane] = q;
       }
       __syncwarp();
-      EXCLK(4);
       if (lane == 0) write_centre(p, gk, r, c, cnt, qv);
-      EXCLK(5);
     }
     __syncthreads();  // the window and strips are reused by the next item
   }
 }
 
-#ifdef SPX_EXACT_CLOCKS
-}  // namespace
-int spx_debug_exact_clocks(long long* out) {
-  return (int)cudaMemcpyFromSymbol(out, g_exclk, sizeof(g_exclk));
-}
-namespace {
-#endif
-__global__ void k_fill_i32(int32_t* v, int n, int value) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = value;
-}
 
 }  // namespace
 
@@ -1063,10 +1030,5 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   return SPX_OK;
 }
 
-int launch_fill_i32(int32_t* v, int n, int value, cudaStream_t st) {
-  k_fill_i32<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(v, n, value);
-  SPX_LAUNCH_CHECK("k_fill_i32");
-  return SPX_OK;
-}
 
 }  // namespace spx

@@ -30,9 +30,6 @@ __global__ void k_rand_rgb(uint8_t* p, long long n, unsigned seed) {
 #define CK(x) do { int rc_ = (x); if (rc_) { fprintf(stderr, "%s failed: %d %s\n", #x, rc_, spx_last_error()); return 1; } } while (0)
 #define CC(x) do { cudaError_t e_ = (x); if (e_) { fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e_)); return 1; } } while (0)
 
-#ifdef SPX_EXACT_CLOCKS
-namespace spx { int spx_debug_exact_clocks(long long* out); }
-#endif
 int main(int argc, char** argv) {
   const int B = argc > 1 ? atoi(argv[1]) : 256;
   const int H = argc > 2 ? atoi(argv[2]) : 480, W = argc > 3 ? atoi(argv[3]) : 640;
@@ -71,19 +68,7 @@ int main(int argc, char** argv) {
     int nflag = 0;
     CC(cudaMemcpy(&nflag, wl + B * K, 4, cudaMemcpyDeviceToHost));
     printf("pass %d: %d of %lld clusters flagged for the exact fallback\n", it, nflag, B * K);
-#ifdef SPX_EXACT_CLOCKS
-    {
-      long long ck[16][16];
-      spx::spx_debug_exact_clocks(&ck[0][0]);
-      for (int b = 0; b < 16 && b < nflag; ++b)
-        printf("  blk %d: to-item %lld window %lld strips %lld barrier %lld tree %lld centre %lld\n", b,
-               ck[b][0] - ck[b][6], ck[b][1] - ck[b][0], ck[b][2] - ck[b][1], ck[b][3] - ck[b][2],
-               ck[b][4] - ck[b][3], ck[b][5] - ck[b][4]);
-      for (int b = 0; b < 4 && b < nflag; ++b)
-        printf("    strip0: count %lld scan %lld issue %lld wait %lld fold %lld\n", ck[b][8] - ck[b][1],
-               ck[b][9] - ck[b][8], ck[b][10] - ck[b][9], ck[b][11] - ck[b][10], ck[b][12] - ck[b][11]);
-    }
-#endif
+
   }
   CC(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
