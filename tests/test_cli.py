@@ -238,3 +238,22 @@ class TestBenchGpu:
         assert one.superpixels == 16 and one.speedup is None
         assert many.speedup == pytest.approx(one.mean_s / many.mean_s, rel=1e-9)
         assert one.mean_s > 0 and many.mean_s > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("size,k,iters", [(256, 256, 5), (97, 40, 3)])
+def test_kernel_bench_engine_equals_stage_chain(size, k, iters, capsys):
+    from paper_1509_04232_b200.kernel_bench import main as kb_main
+    assert kb_main(["--size", str(size), "--superpixels", str(k), "--iters", str(iters),
+                    "--repeats", "2"]) == 0
+    out = capsys.readouterr().out
+    assert "labels identical: yes" in out
+    for stage in ("convert", "init", "associate", "update", "connectivity", "total"):
+        assert stage in out
+
+
+def test_kernel_bench_synthetic_image_is_the_reference_generator():
+    from paper_1509_04232_b200.kernel_bench import synthetic_image
+    img = synthetic_image(8, 3)
+    want = np.random.default_rng(3).integers(0, 256, size=(8, 8, 3), dtype=np.uint8)
+    assert np.array_equal(img.data, want)
