@@ -84,40 +84,54 @@ class ClockSampler:
             idx = int(str(self.dev).split(":")[-1]) if ":" in str(self.dev) else int(self.dev)
             return pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
 
-    def _run(self):
+    def _init(self):
+        """NVML setup, done before the timed region starts (it can take longer
+        than a short timed region)."""
+        self._nv = None
         try:
             nv, h = self._nvml_handle()
-            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
-                                  getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                bits = get_reasons(h) if get_reasons else 0
-                self.samples.append((float(sm), float(mx),
-                                     {n for n, b in zip(self.NAMES, self.BITS) if bits & b}))
-                self._stop.wait(0.005)
-            return
+            self._get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
+                                        getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons",
+                                                None))
+            self._max = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._nv, self._h = nv, h
         except Exception:
             pass
+
+    def _sample(self):
+        if self._nv is not None:
+            try:
+                nv, h = self._nv, self._h
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                bits = self._get_reasons(h) if self._get_reasons else 0
+                self.samples.append((float(sm), self._max,
+                                     {n for n, b in zip(self.NAMES, self.BITS) if bits & b}))
+            except Exception:
+                pass
+            return
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         idx = str(self.dev).split(":")[-1]
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", idx, f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                v = [x.strip() for x in out.split(",")]
-                if len(v) >= 6 and v[0].replace(".", "").isdigit():
-                    self.samples.append((float(v[0]), float(v[1]),
-                                         {n for n, x in zip(self.NAMES, v[2:6])
-                                          if x.lower() == "active"}))
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", idx, f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True,
+                                 text=True, timeout=5).stdout.strip()
+            v = [x.strip() for x in out.split(",")]
+            if len(v) >= 6 and v[0].replace(".", "").isdigit():
+                self.samples.append((float(v[0]), float(v[1]),
+                                     {n for n, x in zip(self.NAMES, v[2:6]) if x.lower() == "active"}))
+        except Exception:
+            pass
+
+    def _run(self):
+        period = 0.005 if self._nv is not None else 0.2
+        while not self._stop.wait(period):
+            self._sample()
 
     def __enter__(self):
+        self._init()
+        self._sample()  # one sample as the timed region opens
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -262,6 +276,7 @@ def run_ours(args):
             eng.segment_device(rgb, outs)
             launches += eng.last_launches()
         end.record(stream)
+        clk._sample()  # the queued steps are still running
         torch.cuda.synchronize()
     barrier()
     ms = start.elapsed_time(end)
