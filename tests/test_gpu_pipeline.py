@@ -237,6 +237,22 @@ def test_cell_path_wide_launch_bitexact(s, odd_w):
         assert np.array_equal(labels[i], labels[j]) and clab[i].tobytes() == clab[j].tobytes()
 
 
+def test_concurrent_exact_fallback_large_batch():
+    # Gray-heavy frames flag many clusters; at this batch size the exact
+    # fallback (side stream) overlaps the reduce for thousands of clusters.
+    h, w = 240, 320
+    st = spx.Settings(img_width=w, img_height=h, spixel_size=16)
+    kinds = ("gray", "dark", "noise", "smooth")
+    frames = np.stack([_images(h, w, 700 + i)[kinds[i % 4]] for i in range(96)])
+    eng = spx.SegEngine(st, max_batch=96)
+    labels, cxy, clab, counts, _ = eng.segment_host(frames)
+    for i in (0, 1, 2, 3, 57, 94):
+        ol, ox, oc, on, _ = _oracle_pipeline(frames[i], st)
+        assert np.array_equal(labels[i], ol), i
+        assert cxy[i].tobytes() == ox.tobytes() and clab[i].tobytes() == oc.tobytes(), i
+        assert np.array_equal(counts[i], on), i
+
+
 def test_cell_path_batch_gray_heavy_frames():
     h, w = 480, 640
     st = spx.Settings(img_width=w, img_height=h, num_superpixels=1200)
