@@ -727,16 +727,19 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
         // otherwise hit the same shared-memory banks)
         unsigned m0 = 0, m1 = 0, m2 = 0, sx = 0;
         const int len = c1 - c0;
-        int k = len ? row % len : 0;
+        const int rot = len ? row % len : 0;
+        auto scan = [&](int k0, int k1) {
 #pragma unroll 4
-        for (int n_ = 0; n_ < len; ++n_) {
-          const bool hit = wrow[c0 + k] == gid;
-          sx += hit ? (unsigned)(wx0 + c0 + k) : 0u;
-          if (k < 32) m0 |= (unsigned)hit << k;
-          else if (k < 64) m1 |= (unsigned)hit << (k - 32);
-          else m2 |= (unsigned)hit << (k - 64);
-          k = k + 1 == len ? 0 : k + 1;
-        }
+          for (int k = k0; k < k1; ++k) {
+            const bool hit = wrow[c0 + k] == gid;
+            sx += hit ? (unsigned)(wx0 + c0 + k) : 0u;
+            if (k < 32) m0 |= (unsigned)hit << k;
+            else if (k < 64) m1 |= (unsigned)hit << (k - 32);
+            else m2 |= (unsigned)hit << (k - 64);
+          }
+        };
+        scan(rot, len);
+        scan(0, rot);
         const int cnt = __popc(m0) + __popc(m1) + __popc(m2);
         lx += sx;
         lc += (unsigned)cnt;
