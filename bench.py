@@ -299,7 +299,9 @@ def run_ours(args):
              (((B, H, W), torch.int32), ((B, K, 2), torch.float64), ((B, K, 3), torch.float64),
               ((B, K), torch.int64), ((B,), torch.int32))] for _ in range(2)]
     e2e_steps = args.steps
-    eng.set_host_chunk(B)  # one chunk per step: steps overlap each other's copies
+    # one chunk per step (steps overlap each other's copies; 128-frame chunks measure
+    # the same, 64 and 32 lower); SPX_E2E_CHUNK overrides for experiments
+    eng.set_host_chunk(int(os.environ.get("SPX_E2E_CHUNK", B)))
     eng.segment_host(pin_rgb, *outs[0])  # warm staging
     barrier()
     t0 = time.perf_counter()
