@@ -289,6 +289,9 @@ __global__ void k_cc_next(const int32_t* __restrict__ lab, const int32_t* __rest
 // to hundreds of links, which rules out per-component chain walking.)
 // Round `round` records whether it changed anything in changed[round]; a
 // round after one that changed nothing returns at once (converged).
+#ifndef SPX_JU
+#define SPX_JU 4
+#endif
 __global__ void k_cc_jump(const int32_t* __restrict__ roots, const int32_t* __restrict__ nroots,
                           int32_t* nxt, int32_t* changed, int round) {
   if (round > 0 && changed[round - 1] == 0) {
@@ -297,13 +300,23 @@ __global__ void k_cc_jump(const int32_t* __restrict__ roots, const int32_t* __re
   }
   const int n = *nroots;
   bool any = false;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const int32_t r = roots[j];
-    const int32_t a = nxt[r], b = nxt[a];
-    if (a != b) {
-      nxt[r] = b;
-      any = true;
-    }
+  // four independent components per thread and step: their dependent
+  // gathers (roots -> nxt -> nxt) are in flight together
+  const int stride = gridDim.x * blockDim.x;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += SPX_JU * stride) {
+    int32_t r[SPX_JU], a[SPX_JU], b[SPX_JU];
+#pragma unroll
+    for (int u = 0; u < SPX_JU; ++u) r[u] = j + u * stride < n ? roots[j + u * stride] : -1;
+#pragma unroll
+    for (int u = 0; u < SPX_JU; ++u) a[u] = r[u] >= 0 ? nxt[r[u]] : 0;
+#pragma unroll
+    for (int u = 0; u < SPX_JU; ++u) b[u] = r[u] >= 0 ? nxt[a[u]] : 0;
+#pragma unroll
+    for (int u = 0; u < SPX_JU; ++u)
+      if (r[u] >= 0 && a[u] != b[u]) {
+        nxt[r[u]] = b[u];
+        any = true;
+      }
   }
   if (__syncthreads_or(any) && threadIdx.x == 0) changed[round] = 1;
 }
