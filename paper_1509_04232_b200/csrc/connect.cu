@@ -114,6 +114,30 @@ __global__ void __launch_bounds__(256) k_weak2(const int32_t* __restrict__ src,
   const int tx0 = blockIdx.x * WG, ty0 = y0 + blockIdx.y * HG;
   const int tid = threadIdx.x;
   const bool vec = (w & 3) == 0;
+  // interior tiles (source window and output fully inside the image, the
+  // common case) skip every bounds test and out-of-image mask
+  const bool inner = vec && tx0 >= 8 && tx0 + WG + 8 <= w && ty0 >= 2 && ty0 + HG + 2 <= h &&
+                     ty0 + HG <= y1;
+  if (inner) {
+    for (int i = tid; i < R0G * NG0; i += 256) {
+      const int r = i / NG0, g = i - r * NG0;
+      t0[r][g] = __ldg(reinterpret_cast<const int4*>(s + (long long)(ty0 - 2 + r) * w + tx0 - 8) + g);
+    }
+    __syncthreads();
+    for (int i = tid; i < R1G * NG1; i += 256) {
+      const int r = i / NG1, g = i - r * NG1;
+      t1[r][g] = weak_rule4(t0[r + 1][g + 1], t0[r][g + 1], t0[r + 2][g + 1], t0[r + 1][g].w,
+                            t0[r + 1][g + 2].x);
+    }
+    __syncthreads();
+    for (int i = tid; i < HG * (WG / 4); i += 256) {
+      const int r = i / (WG / 4), g = i - r * (WG / 4);
+      *reinterpret_cast<int4*>(d + (long long)(ty0 + r) * w + tx0 + 4 * g) =
+          weak_rule4(t1[r + 1][g + 1], t1[r][g + 1], t1[r + 2][g + 1], t1[r + 1][g].w,
+                     t1[r + 1][g + 2].x);
+    }
+    return;
+  }
   for (int i = tid; i < R0G * NG0; i += 256) {
     const int r = i / NG0, g = i - r * NG0;
     const int y = ty0 - 2 + r, x = tx0 - 8 + 4 * g;
