@@ -70,6 +70,8 @@ SIGNATURES = {
     "spx_engine_ticket": (I64, [P]),
     "spx_engine_wait_ticket": (I32, [P, I64]),
     "spx_engine_set_host_chunk": (I32, [P, I64]),
+    "spx_engine_set_lanes": (I32, [P, I32]),
+    "spx_engine_last_lanes": (I32, [P]),
     "spx_engine_timing": (I32, [P, ctypes.POINTER(SpxTiming)]),
     "spx_engine_last_launches": (I64, [P]),
     "spx_strip_create": (I32, [ctypes.POINTER(SpxSettings), I64, I64, I32, ctypes.POINTER(P)]),

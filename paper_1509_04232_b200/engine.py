@@ -224,6 +224,14 @@ class SegEngine:
         """Frames per H2D/compute/D2H pipeline chunk of the host-buffer path."""
         _lib.check(self._lib.spx_engine_set_host_chunk(self._h, int(frames)), "set_host_chunk")
 
+    def set_lanes(self, lanes):
+        """Concurrent sub-batches per call of more than 16 frames (0 = automatic:
+        one per 64 frames, at most 4).  Results do not depend on it."""
+        _lib.check(self._lib.spx_engine_set_lanes(self._h, int(lanes)), "set_lanes")
+
+    def last_lanes(self):
+        return int(self._lib.spx_engine_last_lanes(self._h))
+
     def wait(self):
         """Wait for every submitted batch; their outputs are then valid."""
         _lib.check(self._lib.spx_engine_wait(self._h), "wait")

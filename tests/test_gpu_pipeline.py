@@ -253,6 +253,41 @@ def test_concurrent_exact_fallback_large_batch():
         assert np.array_equal(counts[i], on), i
 
 
+@pytest.mark.parametrize("kw", [dict(), dict(early_stop_threshold=15.0, no_iters=8),
+                                dict(connectivity_mode=spx.ConnectivityMode.STRICT)])
+def test_lanes_split_matches_unsplit_and_oracle(kw):
+    # A call of more than 16 frames runs as concurrent sub-batches (lanes) on
+    # child engines; the split (ragged here: 130 = 44 + 44 + 42) must not
+    # change any output.
+    import torch
+    h, w = 64, 96
+    st = spx.Settings(img_width=w, img_height=h, num_superpixels=24, **kw)
+    kinds = ("gray", "dark", "noise", "smooth")
+    frames = np.stack([_images(h, w, 900 + i)[kinds[i % 4]] for i in range(130)])
+    d = torch.from_numpy(frames).cuda()
+    eng = spx.SegEngine(st, max_batch=130)
+    res = {}
+    for lanes in (1, 3, 0):
+        eng.set_lanes(lanes)
+        out = [t.clone() for t in eng.segment_device(d)]
+        torch.cuda.synchronize()
+        res[lanes] = ([t.cpu().numpy() for t in out], eng.last_lanes())
+    assert res[1][1] == 1 and res[3][1] == 3 and res[0][1] == 2  # auto: one lane per 64
+    for lanes in (3, 0):
+        for a, b in zip(res[1][0], res[lanes][0]):
+            assert a.tobytes() == b.tobytes(), lanes
+    labels, cxy, clab, counts, passes = res[3][0]
+    for i in (0, 43, 44, 87, 88, 129):  # both sides of every lane boundary
+        ol, ox, oc, on, op = _oracle_pipeline(frames[i], st)
+        assert np.array_equal(labels[i], ol), i
+        assert cxy[i].tobytes() == ox.tobytes() and clab[i].tobytes() == oc.tobytes(), i
+        assert np.array_equal(counts[i], on), i
+    t = eng.last_timing()
+    assert t.total > 0
+    with pytest.raises(ValueError):
+        eng.set_lanes(-1)
+
+
 def test_cell_path_batch_gray_heavy_frames():
     h, w = 480, 640
     st = spx.Settings(img_width=w, img_height=h, num_superpixels=1200)
