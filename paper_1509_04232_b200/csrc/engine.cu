@@ -91,7 +91,9 @@ struct Engine {
   // is a child Engine (own buffers, worklist, side stream, events) created on
   // first use; frames are independent, so the results are bitwise the same
   // as the unsplit call (tests/test_gpu_engine.py).  Measured on C1, 256
-  // frames: 1 lane 4.60 ms, 2 lanes 4.45, 4 lanes 4.31, 8 lanes 4.41.
+  // frames (tools/lanes_probe.py): 1 lane 4.59 ms, 2: 4.56, 3: 4.40, 4: 4.32,
+  // 5: 4.67, 6: 4.48, 8: 4.44.  Staggering the lanes (lane i starting after
+  // lane i-1's convert) measured 1% slower at 4 lanes.
   int lanes_req = 0;  // 0: auto (one lane per kLaneFrames frames, at most kMaxLanes)
   static constexpr int kMaxLanes = 4;
   static constexpr int64_t kLaneFrames = 64;
