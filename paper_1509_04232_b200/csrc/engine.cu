@@ -94,9 +94,9 @@ struct Engine {
   // frames (tools/lanes_probe.py): 1 lane 4.59 ms, 2: 4.56, 3: 4.40, 4: 4.32,
   // 5: 4.67, 6: 4.48, 8: 4.44.  Staggering the lanes (lane i starting after
   // lane i-1's convert) measured 1% slower at 4 lanes.
-  int lanes_req = 0;  // 0: auto (one lane per kLaneFrames frames, at most kMaxLanes)
+  int lanes_req = 0;  // 0: auto (one lane per kLanePixels pixels, at most kMaxLanes)
   static constexpr int kMaxLanes = 4;
-  static constexpr int64_t kLaneFrames = 64;
+  static constexpr int64_t kLanePixels = 16 << 20;  // ~53 VGA frames
   std::vector<Engine*> lane_eng;
   std::vector<cudaStream_t> lane_st;
   std::vector<cudaEvent_t> lane_join;
@@ -104,8 +104,12 @@ struct Engine {
   int last_lanes = 1;
 
   int lanes_for(int64_t batch) const {
-    if (batch <= kGraphMaxBatch) return 1;
-    int64_t l = lanes_req > 0 ? lanes_req : std::min<int64_t>(kMaxLanes, batch / kLaneFrames);
+    if (batch < 2) return 1;
+    int64_t l = lanes_req;
+    if (l == 0) {  // auto: one lane per kLanePixels of work; none for small calls
+      l = std::min<int64_t>(kMaxLanes, (batch * hw + kLanePixels / 2) / kLanePixels);
+      if (batch <= kGraphMaxBatch && l < 2) return 1;  // small: the CUDA-graph path
+    }
     return (int)std::max<int64_t>(1, std::min<int64_t>(l, batch));
   }
 
@@ -123,7 +127,7 @@ struct Engine {
     const int64_t per = ceil_div(max_batch, (int64_t)n);
     // a lane created for a smaller split cannot take this one's sub-batch
     for (size_t i = 0; i < lane_eng.size(); ++i)
-      if (lane_eng[i]->max_batch < per) {
+      if (lane_eng[i] && lane_eng[i]->max_batch < per) {
         delete lane_eng[i];
         lane_eng[i] = nullptr;
       }

@@ -272,7 +272,8 @@ def test_lanes_split_matches_unsplit_and_oracle(kw):
         out = [t.clone() for t in eng.segment_device(d)]
         torch.cuda.synchronize()
         res[lanes] = ([t.cpu().numpy() for t in out], eng.last_lanes())
-    assert res[1][1] == 1 and res[3][1] == 3 and res[0][1] == 2  # auto: one lane per 64
+    # auto: one lane per 16 Mpx of work, so this small batch runs unsplit
+    assert res[1][1] == 1 and res[3][1] == 3 and res[0][1] == 1
     for lanes in (3, 0):
         for a, b in zip(res[1][0], res[lanes][0]):
             assert a.tobytes() == b.tobytes(), lanes
@@ -286,6 +287,24 @@ def test_lanes_split_matches_unsplit_and_oracle(kw):
     assert t.total > 0
     with pytest.raises(ValueError):
         eng.set_lanes(-1)
+
+
+def test_lanes_resplit_sequence():
+    # Lane counts that grow and shrink: child engines sized for a finer split
+    # are replaced when a coarser split needs bigger lanes.
+    import torch
+    h, w = 64, 96
+    st = spx.Settings(img_width=w, img_height=h, num_superpixels=24)
+    frames = np.stack([_images(h, w, 950 + i)["noise"] for i in range(40)])
+    d = torch.from_numpy(frames).cuda()
+    eng = spx.SegEngine(st, max_batch=40)
+    eng.set_lanes(1)
+    want = [t.cpu().numpy() for t in eng.segment_device(d)]
+    for lanes in (2, 3, 5, 8, 4, 0, 8, 2, 40, 7):
+        eng.set_lanes(lanes)
+        got = [t.cpu().numpy() for t in eng.segment_device(d)]
+        for a, b in zip(want, got):
+            assert a.tobytes() == b.tobytes(), lanes
 
 
 def test_cell_path_batch_gray_heavy_frames():

@@ -59,11 +59,18 @@ def run(name, reps, warm):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    lanes = eng.last_lanes()
+    # stage columns: one unsplit (1-lane) call, since concurrent lanes overlap
+    eng.set_lanes(1)
+    eng.segment_device(d_rgb, out)
     tm = eng.last_timing()
+    eng.set_lanes(0)
+    torch.cuda.synchronize()
     n, k, it = h * w, g.num_clusters, st.no_iters
     bytes_frame = 15 * n + (it + 1) * (16 * n + 40 * k) + it * (16 * n + 48 * k) + 16 * n + 40 * k
     fps = b / (ms / 1e3)
     rec = {"config": name, "image": f"{w}x{h}", "S": g.s, "K": k, "iters": it, "frames": b,
+           "lanes": lanes,
            "ms_per_batch": ms, "frames_per_s": fps, "mpix_per_s": fps * n / 1e6,
            "bytes_per_frame": bytes_frame,
            "hbm_frac": bytes_frame * fps / 1e9 / PEAK,
@@ -104,14 +111,15 @@ def main():
         with open(a.md, "w") as f:
             f.write("# Device throughput per BASELINE config (one B200, tools/bench_configs.py)\n\n")
             f.write("Inputs resident in HBM; CUDA-event timing; bytes per SURVEY §8(d); "
-                    f"peak {PEAK} GB/s.\n\n")
-            f.write("| config | image | S | K | iters | frames/batch | ms/batch | frames/s | Mpix/s "
+                    f"peak {PEAK} GB/s.  Throughput with the engine's automatic lanes "
+                    "(concurrent sub-batches); stage columns from one unsplit call.\n\n")
+            f.write("| config | image | S | K | iters | frames/batch | lanes | ms/batch | frames/s | Mpix/s "
                     "| HBM frac | convert | assoc+update pass | final assoc | update | weak | "
-                    "frame 0 == oracle |\n|" + "---|" * 16 + "\n")
+                    "frame 0 == oracle |\n|" + "---|" * 17 + "\n")
             for r in recs:
                 s = r["stage_ms"]
                 f.write(f"| {r['config']} | {r['image']} | {r['S']} | {r['K']} | {r['iters']} | "
-                        f"{r['frames']} | {r['ms_per_batch']:.3f} | {r['frames_per_s']:.1f} | "
+                        f"{r['frames']} | {r['lanes']} | {r['ms_per_batch']:.3f} | {r['frames_per_s']:.1f} | "
                         f"{r['mpix_per_s']:.0f} | {r['hbm_frac']:.3f} | {s['convert']:.3f} | "
                         f"{s['associate_mean']:.3f} | {s['final_associate']:.3f} | "
                         f"{s['update_mean']:.3f} | {s['connectivity']:.3f} | "
