@@ -225,8 +225,8 @@ class SegEngine:
         _lib.check(self._lib.spx_engine_set_host_chunk(self._h, int(frames)), "set_host_chunk")
 
     def set_lanes(self, lanes):
-        """Concurrent sub-batches per call of more than 16 frames (0 = automatic:
-        one per 64 frames, at most 4).  Results do not depend on it."""
+        """Concurrent sub-batches per call (0 = automatic: one per 16 Mpx of
+        work, at most 4).  Results do not depend on it."""
         _lib.check(self._lib.spx_engine_set_lanes(self._h, int(lanes)), "set_lanes")
 
     def last_lanes(self):
