@@ -103,8 +103,10 @@ struct Engine {
   cudaEvent_t lane_fork = nullptr;
   int last_lanes = 1;
 
+  bool lanes_off = false;  // automatic lanes ran out of memory once
+
   int lanes_for(int64_t batch) const {
-    if (batch < 2) return 1;
+    if (batch < 2 || (lanes_req == 0 && lanes_off)) return 1;
     int64_t l = lanes_req;
     if (l == 0) {  // auto: one lane per kLanePixels of work; none for small calls
       l = std::min<int64_t>(kMaxLanes, (batch * hw + kLanePixels / 2) / kLanePixels);
@@ -123,6 +125,7 @@ struct Engine {
   }
 
   int ensure_lanes(int n) {
+    SPX_CUDA(cudaSetDevice(device));
     if (!lane_fork) SPX_CUDA(cudaEventCreateWithFlags(&lane_fork, cudaEventDisableTiming));
     const int64_t per = ceil_div(max_batch, (int64_t)n);
     // a lane created for a smaller split cannot take this one's sub-batch
@@ -167,8 +170,7 @@ struct Engine {
   int segment_lanes(int n, const uint8_t* rgb, int64_t batch, int32_t* out_labels,
                     double* out_xy, double* out_lab, int64_t* out_counts, int32_t* out_passes,
                     cudaStream_t s) {
-    int rc = ensure_lanes(n);
-    if (rc) return rc;
+    int rc;
     launches = 0;
     n_assoc = n_update = 0;
     cudaEventRecord(ev[EV_START], s);
@@ -345,8 +347,19 @@ struct Engine {
     last_graph = nullptr;
     last_lanes = 1;
     const int nl = lanes_for(batch);
-    if (nl > 1)
-      return segment_lanes(nl, rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes, s);
+    if (nl > 1) {
+      const int rl = ensure_lanes(nl);
+      if (rl == SPX_OK)
+        return segment_lanes(nl, rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes,
+                             s);
+      // Automatic lanes whose child buffers do not fit next to the caller's
+      // tensors: give the memory back and run unsplit from now on (same
+      // results, same kernels).  An explicit lane count reports the error.
+      if (rl != SPX_ERR_NOMEM || lanes_req != 0) return rl;
+      free_lanes();
+      cudaGetLastError();
+      lanes_off = true;
+    }
     if (!use_graphs || batch > kGraphMaxBatch)
       return segment_eager(rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes, s);
     const void* key[6] = {rgb, out_labels, out_xy, out_lab, out_counts, out_passes};
