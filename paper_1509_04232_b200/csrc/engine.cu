@@ -93,7 +93,8 @@ struct Engine {
   // as the unsplit call (tests/test_gpu_engine.py).  Measured on C1, 256
   // frames (tools/lanes_probe.py): 1 lane 4.59 ms, 2: 4.56, 3: 4.40, 4: 4.32,
   // 5: 4.67, 6: 4.48, 8: 4.44.  Staggering the lanes (lane i starting after
-  // lane i-1's convert) measured 1% slower at 4 lanes.
+  // lane i-1's convert) measured 1% slower at 4 lanes, and stream priorities
+  // by lane (either order) 7% slower: the gain needs the lanes to co-run.
   int lanes_req = 0;  // 0: auto (one lane per kLanePixels pixels, at most kMaxLanes)
   static constexpr int kMaxLanes = 4;
   static constexpr int64_t kLanePixels = 16 << 20;  // ~53 VGA frames
