@@ -223,7 +223,11 @@ __device__ __forceinline__ float with_flag(float o0, float o1, float o2, float t
 }
 
 #ifndef SPX_CONV_BPS
-#define SPX_CONV_BPS 12  // grid cap: blocks per SM, grid-stride beyond (8: -1%, 3: -5%)
+// grid cap: blocks per SM, grid-stride beyond.  3 = one resident wave
+// (SPX_CONV_MINB): unsplit calls measured 0.7% slower than a cap of 12, but
+// with concurrent lanes (engine.cu) the converts then leave SM slots to the
+// other lanes' passes: C1 x 256 in 4 lanes 4.325 -> 4.297 ms (6: 4.52 ms).
+#define SPX_CONV_BPS 3
 #endif
 #ifndef SPX_CONV_MINB
 #define SPX_CONV_MINB 3  // 80 registers, 24 warps per SM (measured ~1% faster than 4 and 6)
