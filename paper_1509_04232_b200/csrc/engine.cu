@@ -95,9 +95,9 @@ struct Engine {
   // 5: 4.67, 6: 4.48, 8: 4.44.  Staggering the lanes (lane i starting after
   // lane i-1's convert) measured 1% slower at 4 lanes, and stream priorities
   // by lane (either order) 7% slower: the gain needs the lanes to co-run.
-  int lanes_req = 0;  // 0: auto (one lane per kLanePixels pixels, at most kMaxLanes)
+  int lanes_req = 0;  // 0: auto (3 lanes, 4 from kLanePixels pixels of work)
   static constexpr int kMaxLanes = 4;
-  static constexpr int64_t kLanePixels = 16 << 20;  // ~53 VGA frames
+  static constexpr int64_t kLanePixels = 24 << 20;  // ~80 VGA frames
   std::vector<Engine*> lane_eng;
   std::vector<cudaStream_t> lane_st;
   std::vector<cudaEvent_t> lane_join;
@@ -109,9 +109,11 @@ struct Engine {
   int lanes_for(int64_t batch) const {
     if (batch < 2 || (lanes_req == 0 && lanes_off)) return 1;
     int64_t l = lanes_req;
-    if (l == 0) {  // auto: one lane per kLanePixels of work; none for small calls
-      l = std::min<int64_t>(kMaxLanes, (batch * hw + kLanePixels / 2) / kLanePixels);
-      if (batch <= kGraphMaxBatch && l < 2) return 1;  // small: the CUDA-graph path
+    if (l == 0) {  // auto (tools/lanes_probe.py, VGA frames: 32 -> 3 lanes +37%,
+                   // 64 -> 3 lanes +23%, 128 -> 4 lanes +13%, 256 -> 4 lanes +6%)
+      const bool big = batch * hw >= kLanePixels;
+      if (batch <= kGraphMaxBatch && !big) return 1;  // small: the CUDA-graph path
+      l = big ? kMaxLanes : 3;
     }
     return (int)std::max<int64_t>(1, std::min<int64_t>(l, batch));
   }

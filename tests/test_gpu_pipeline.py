@@ -272,8 +272,8 @@ def test_lanes_split_matches_unsplit_and_oracle(kw):
         out = [t.clone() for t in eng.segment_device(d)]
         torch.cuda.synchronize()
         res[lanes] = ([t.cpu().numpy() for t in out], eng.last_lanes())
-    # auto: one lane per 16 Mpx of work, so this small batch runs unsplit
-    assert res[1][1] == 1 and res[3][1] == 3 and res[0][1] == 1
+    # auto: more than 16 frames but under 24 Mpx of work -> three lanes
+    assert res[1][1] == 1 and res[3][1] == 3 and res[0][1] == 3
     for lanes in (3, 0):
         for a, b in zip(res[1][0], res[lanes][0]):
             assert a.tobytes() == b.tobytes(), lanes
