@@ -111,9 +111,12 @@ struct Engine {
     int64_t l = lanes_req;
     if (l == 0) {  // auto (tools/lanes_probe.py, VGA frames: 32 -> 3 lanes +37%,
                    // 64 -> 3 lanes +23%, 128 -> 4 lanes +13%, 256 -> 4 lanes +6%)
+      // graph-replayed calls (<= 16 frames) split too: the captured graph
+      // forks the lanes (VGA x4 0.176 -> 0.155 ms, x8 0.255 -> 0.217,
+      // x16 0.452 -> 0.344 in 4 lanes)
       const bool big = batch * hw >= kLanePixels;
-      if (batch <= kGraphMaxBatch && !big) return 1;  // small: the CUDA-graph path
-      l = big ? kMaxLanes : 3;
+      if (batch < 4) return 1;
+      l = (big || batch <= kGraphMaxBatch) ? kMaxLanes : 3;
     }
     return (int)std::max<int64_t>(1, std::min<int64_t>(l, batch));
   }
@@ -176,7 +179,7 @@ struct Engine {
     int rc;
     launches = 0;
     n_assoc = n_update = 0;
-    cudaEventRecord(ev[EV_START], s);
+    stage_mark(ev[EV_START], s);
     SPX_CUDA(cudaEventRecord(lane_fork, s));
     const int64_t per = ceil_div(batch, (int64_t)n);
     int used = 0;
@@ -194,7 +197,7 @@ struct Engine {
       SPX_CUDA(cudaStreamWaitEvent(s, lane_join[i], 0));
       ++used;
     }
-    cudaEventRecord(ev[EV_END], s);
+    stage_mark(ev[EV_END], s);
     last_lanes = used;
     return SPX_OK;
   }
@@ -308,6 +311,7 @@ struct Engine {
   struct GraphEntry {
     const void* key[6];
     int64_t batch;
+    int lanes;
     cudaGraphExec_t exec;
     int n_assoc, n_update;
     int64_t launches;
@@ -348,27 +352,33 @@ struct Engine {
     }
     SPX_CUDA(cudaSetDevice(device));
     last_graph = nullptr;
-    last_lanes = 1;
-    const int nl = lanes_for(batch);
+    int nl = lanes_for(batch);
     if (nl > 1) {
       const int rl = ensure_lanes(nl);
-      if (rl == SPX_OK)
-        return segment_lanes(nl, rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes,
-                             s);
       // Automatic lanes whose child buffers do not fit next to the caller's
       // tensors: give the memory back and run unsplit from now on (same
       // results, same kernels).  An explicit lane count reports the error.
-      if (rl != SPX_ERR_NOMEM || lanes_req != 0) return rl;
-      free_lanes();
-      cudaGetLastError();
-      lanes_off = true;
+      if (rl != SPX_OK) {
+        if (rl != SPX_ERR_NOMEM || lanes_req != 0) return rl;
+        free_lanes();
+        cudaGetLastError();
+        lanes_off = true;
+        nl = 1;
+      }
     }
-    if (!use_graphs || batch > kGraphMaxBatch)
-      return segment_eager(rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes, s);
+    // one call, eager: unsplit or in lanes (the lanes' buffers exist by now)
+    auto run = [&](cudaStream_t q) {
+      if (nl > 1)
+        return segment_lanes(nl, rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes,
+                             q);
+      last_lanes = 1;
+      return segment_eager(rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes, q);
+    };
+    if (!use_graphs || batch > kGraphMaxBatch) return run(s);
     const void* key[6] = {rgb, out_labels, out_xy, out_lab, out_counts, out_passes};
     GraphEntry* g = nullptr;
     for (auto& e : graphs)
-      if (e.batch == batch && std::memcmp(e.key, key, sizeof key) == 0) g = &e;
+      if (e.batch == batch && e.lanes == nl && std::memcmp(e.key, key, sizeof key) == 0) g = &e;
     if (!g) {  // first call with this key: eager, remember the key
       if (graphs.size() >= 8) {
         if (graphs.front().exec) cudaGraphExecDestroy(graphs.front().exec);
@@ -377,13 +387,14 @@ struct Engine {
       GraphEntry e{};
       std::memcpy(e.key, key, sizeof key);
       e.batch = batch;
+      e.lanes = nl;
       e.eager_calls = 1;
       graphs.push_back(e);
-      return segment_eager(rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes, s);
+      return run(s);
     }
     if (!g->exec && g->eager_calls < 2) {  // second call: eager and warm
       ++g->eager_calls;
-      return segment_eager(rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes, s);
+      return run(s);
     }
     if (!g->exec) {  // third call: keep the warm eager call's stage times, capture
       int rt = timing(&g->stages);
@@ -391,8 +402,7 @@ struct Engine {
       if (!s_cap) SPX_CUDA(cudaStreamCreateWithFlags(&s_cap, cudaStreamNonBlocking));
       SPX_CUDA(cudaStreamBeginCapture(s_cap, cudaStreamCaptureModeRelaxed));
       capturing = true;
-      int rc = segment_eager(rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes,
-                             s_cap);
+      int rc = run(s_cap);
       capturing = false;
       cudaGraph_t graph = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(s_cap, &graph);
@@ -420,6 +430,7 @@ struct Engine {
     n_update = g->n_update;
     launches = g->launches;
     last_graph = g;
+    last_lanes = g->lanes;
     return SPX_OK;
   }
 
@@ -543,14 +554,14 @@ struct Engine {
       cudaEventElapsedTime(&ms, a, b);
       return ms;
     };
-    if (last_lanes > 1) {  // lanes: lane 0's stages (run concurrently), measured total
-      int rc = lane_eng[0]->timing(t);
-      if (rc) return rc;
+    if (last_graph) {  // graph replay: measured total, eager-call breakdown
+      *t = last_graph->stages;
       t->total = el(ev[EV_START], ev[EV_END]);
       return SPX_OK;
     }
-    if (last_graph) {  // graph replay: measured total, eager-call breakdown
-      *t = last_graph->stages;
+    if (last_lanes > 1) {  // lanes: lane 0's stages (run concurrently), measured total
+      int rc = lane_eng[0]->timing(t);
+      if (rc) return rc;
       t->total = el(ev[EV_START], ev[EV_END]);
       return SPX_OK;
     }

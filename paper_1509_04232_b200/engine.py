@@ -225,9 +225,8 @@ class SegEngine:
         _lib.check(self._lib.spx_engine_set_host_chunk(self._h, int(frames)), "set_host_chunk")
 
     def set_lanes(self, lanes):
-        """Concurrent sub-batches per call (0 = automatic: 4 from 24 Mpx of
-        work, 3 for smaller calls of more than 16 frames, else 1).  Results do
-        not depend on it."""
+        """Concurrent sub-batches per call (0 = automatic: 1 below 4 frames,
+        3 for 17+ frames under 24 Mpx, else 4).  Results do not depend on it."""
         _lib.check(self._lib.spx_engine_set_lanes(self._h, int(lanes)), "set_lanes")
 
     def last_lanes(self):

@@ -307,6 +307,31 @@ def test_lanes_resplit_sequence():
             assert a.tobytes() == b.tobytes(), lanes
 
 
+def test_lanes_in_graph_replay():
+    # <= 16 frames take the CUDA-graph path; with lanes the captured graph
+    # forks the lanes' streams.  Replays must equal the unsplit results.
+    import torch
+    h, w = 64, 96
+    st = spx.Settings(img_width=w, img_height=h, num_superpixels=24)
+    frames = np.stack([_images(h, w, 980 + i)["noise"] for i in range(12)])
+    d = torch.from_numpy(frames).cuda()
+    eng = spx.SegEngine(st, max_batch=12)
+    eng.set_lanes(1)
+    want = [t.cpu().numpy() for t in eng.segment_device(d)]
+    for lanes in (3, 2):
+        eng.set_lanes(lanes)
+        outs = eng.allocate_outputs(12)
+        for call in range(5):  # eager, eager, capture, replay, replay
+            for t in outs:
+                t.zero_()
+            eng.segment_device(d, outs)
+            torch.cuda.synchronize()
+            assert eng.last_lanes() == lanes
+            assert eng.last_timing().total > 0
+            for a, b in zip(want, outs):
+                assert a.tobytes() == b.cpu().numpy().tobytes(), (lanes, call)
+
+
 def test_cell_path_batch_gray_heavy_frames():
     h, w = 480, 640
     st = spx.Settings(img_width=w, img_height=h, num_superpixels=1200)

@@ -43,11 +43,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C2,C3,C4")
     ap.add_argument("--batch", type=int, default=0, help="override frames per batch")
+    ap.add_argument("--lanes", default="", help="comma list overriding the lane counts")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for name in a.configs.split(","):
         w, h, kw, b, lane_set = CONFIGS[name]
         b = a.batch or b
+        if a.lanes:
+            lane_set = tuple(int(x) for x in a.lanes.split(","))
         rng = np.random.default_rng(0)
         rgb = torch.from_numpy(rng.integers(0, 256, (b, h, w, 3), dtype=np.uint8)).cuda()
         st = spx.Settings(img_width=w, img_height=h, **kw)
