@@ -111,9 +111,10 @@ struct Engine {
     int64_t l = lanes_req;
     if (l == 0) {  // auto (tools/lanes_probe.py, VGA frames: 32 -> 3 lanes +37%,
                    // 64 -> 3 lanes +23%, 128 -> 4 lanes +13%, 256 -> 4 lanes +6%)
-      // graph-replayed calls (<= 16 frames) split too: the captured graph
-      // forks the lanes (VGA x4 0.176 -> 0.155 ms, x8 0.255 -> 0.217,
-      // x16 0.452 -> 0.344 in 4 lanes)
+      // graph-replayed calls (<= kGraphMaxBatch frames) split too: the
+      // captured graph forks the lanes (VGA x4 0.176 -> 0.155 ms, x8 0.255
+      // -> 0.217, x16 0.452 -> 0.344, x32 0.825 -> 0.597, x64 1.339 -> 1.118
+      // in 4 lanes)
       const bool big = batch * hw >= kLanePixels;
       if (batch < 4) return 1;
       l = (big || batch <= kGraphMaxBatch) ? kMaxLanes : 3;
@@ -188,10 +189,15 @@ struct Engine {
       if (nb <= 0) break;
       Engine* c = lane_eng[i];
       SPX_CUDA(cudaStreamWaitEvent(lane_st[i], lane_fork, 0));
-      if ((rc = c->segment_eager(rgb + f0 * hw * 3, nb, out_labels + f0 * hw, out_xy + f0 * K * 2,
+      // under capture the child records only its start / end events, as
+      // event-record nodes (an ordinary record inside a capture would leave
+      // the event unusable for a later timing query)
+      c->capturing = capturing;
+      rc = c->segment_eager(rgb + f0 * hw * 3, nb, out_labels + f0 * hw, out_xy + f0 * K * 2,
                                  out_lab + f0 * K * 3, out_counts + f0 * K,
-                                 out_passes ? out_passes + f0 : nullptr, lane_st[i])))
-        return rc;
+                                 out_passes ? out_passes + f0 : nullptr, lane_st[i]);
+      c->capturing = false;
+      if (rc) return rc;
       launches += c->launches;
       SPX_CUDA(cudaEventRecord(lane_join[i], lane_st[i]));
       SPX_CUDA(cudaStreamWaitEvent(s, lane_join[i], 0));
@@ -307,7 +313,10 @@ struct Engine {
   // Replays record only the start/end events (an event node costs ~4 us);
   // their per-stage breakdown is the one measured on the second eager call.  Large
   // batches run eagerly with every stage event live.
-  static constexpr int64_t kGraphMaxBatch = 16;
+#ifndef SPX_GRAPH_MAX
+#define SPX_GRAPH_MAX 64
+#endif
+  static constexpr int64_t kGraphMaxBatch = SPX_GRAPH_MAX;
   struct GraphEntry {
     const void* key[6];
     int64_t batch;
