@@ -184,10 +184,10 @@ SPX_API int32_t spx_engine_set_host_chunk(spx_engine *eng, int64_t frames);
 /* Lanes: a segment call of two or more frames may be split into `lanes`
  * sub-batches on concurrent streams, each on a child engine created on first
  * use (so the per-frame buffers exist twice); the convert of one lane
- * overlaps the association of another.  Calls of <= 16 frames replay a
+ * overlaps the association of another.  Calls of <= 64 frames replay a
  * CUDA graph that forks the lanes.  0 (default) = automatic: none below 4
- * frames, three for 17+ frames under 24 Mpx, otherwise four.  Results do
- * not depend on the split.  With more
+ * frames, three for calls of more than 64 frames under 24 Mpx, otherwise
+ * four.  Results do not depend on the split.  With more
  * than one lane, spx_engine_timing reports lane 0's stage times (measured
  * while the other lanes ran) and the whole call's total. */
 SPX_API int32_t spx_engine_set_lanes(spx_engine *eng, int32_t lanes);

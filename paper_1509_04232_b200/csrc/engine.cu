@@ -109,8 +109,9 @@ struct Engine {
   int lanes_for(int64_t batch) const {
     if (batch < 2 || (lanes_req == 0 && lanes_off)) return 1;
     int64_t l = lanes_req;
-    if (l == 0) {  // auto (tools/lanes_probe.py, VGA frames: 32 -> 3 lanes +37%,
-                   // 64 -> 3 lanes +23%, 128 -> 4 lanes +13%, 256 -> 4 lanes +6%)
+    if (l == 0) {  // auto (tools/lanes_probe.py; eager VGA calls: 32 frames ->
+                   // 3 lanes +37%, 64 -> 3 lanes +23%, 128 -> 4 lanes +13%,
+                   // 256 -> 4 lanes +6%; 3 lanes remain for eager calls < 24 Mpx)
       // graph-replayed calls (<= kGraphMaxBatch frames) split too: the
       // captured graph forks the lanes (VGA x4 0.176 -> 0.155 ms, x8 0.255
       // -> 0.217, x16 0.452 -> 0.344, x32 0.825 -> 0.597, x64 1.339 -> 1.118

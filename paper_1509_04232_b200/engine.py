@@ -226,7 +226,8 @@ class SegEngine:
 
     def set_lanes(self, lanes):
         """Concurrent sub-batches per call (0 = automatic: 1 below 4 frames,
-        3 for 17+ frames under 24 Mpx, else 4).  Results do not depend on it."""
+        3 for calls of more than 64 frames under 24 Mpx, else 4).  Results do
+        not depend on it."""
         _lib.check(self._lib.spx_engine_set_lanes(self._h, int(lanes)), "set_lanes")
 
     def last_lanes(self):
