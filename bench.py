@@ -2,6 +2,9 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
 
+--gpus N > 1 outside torchrun re-executes itself as N ranks under
+torch.distributed.run (127.0.0.1); under torchrun WORLD_SIZE must equal N.
+
 One "step" segments a batch of B synthetic 640x480 frames (the reference's
 generator: np.random.default_rng(i).integers(0, 256, (480, 640, 3), uint8))
 through the whole pipeline -- convert, init, association x6, update x5, weak
@@ -183,6 +186,33 @@ def dist_setup():
     return world, rank, local
 
 
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_ranks(n):
+    """`python bench.py --gpus N` outside torchrun: re-exec this command as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1.
+    Rank 0 prints the JSON line; the exit code is the launcher's."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def bench_config(B, world):
+    """The workload both arms report (identical dicts: the driver compares them)."""
+    return {"workload": "C1: 640x480 RGB, K=1200 (S=16, 30x40 grid), m=10, 5 iters, LAB, "
+                        "weak connectivity",
+            "frames_per_gpu_per_step": B, "global_batch": B * world,
+            "parallelism": f"frame-sharded x{world} (no collective)",
+            "l2": f"inputs > L2: {B * H * W * 3 / 1e6:.0f} MB RGB + {B * H * W * 12 / 1e6:.0f} MB "
+                  f"Lab per GPU per step"}
+
+
 def run_reference(args):
     world, rank, _ = dist_setup()
     if rank != 0:
@@ -212,11 +242,13 @@ def run_reference(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C1: 640x480 RGB, K=1200 (S=16), m=10, 5 iters, LAB, weak conn",
-                   "frames_per_step": per_step, "backend": f"reference par x{cores}"},
+        "config": bench_config(args.batch, world),
         "mpix_per_s": value * W * H / 1e6,
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "reference",
-                         "sample": f"{per_step} frames per step x {args.steps} steps"},
+                         "sample": f"bounded sample of the workload: {per_step} frames (seeds "
+                                   f"0..{per_step - 1}) per step x {args.steps} steps, reference "
+                                   f"SegEngine backend=par workers={cores} (oracle/_ref: the "
+                                   f"unmodified reference compiled here)"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -359,13 +391,8 @@ def run_ours(args):
                           "fp32 under a certified error bound (uncertain pixels redone in "
                           "binary64), Lab conversion and all sums in binary64",
             "data": "synthetic",
-            "config": {"workload": "C1: 640x480 RGB, K=1200 (S=16, 30x40 grid), m=10, 5 iters, "
-                                   "LAB, weak connectivity",
-                       "frames_per_gpu_per_step": B, "global_batch": B * world,
-                       "parallelism": f"frame-sharded x{world} (no collective)",
-                       "lanes": lanes,
-                       "l2": f"inputs > L2: {h2d / 1e6:.0f} MB RGB + {n_px * 12 / 1e6:.0f} MB Lab "
-                             f"per GPU per step"},
+            "config": bench_config(B, world),
+            "engine": {"lanes": lanes, "backend": backend if world > 1 else None},
             "mpix_per_s": value * H * W / 1e6,
             "frame_roofline": {"bytes_per_frame": frame_bytes,
                                "achieved_gbs": value / world * frame_bytes / 1e9,
@@ -414,6 +441,14 @@ def main():
     ap.add_argument("--cpu-frames", type=int, default=400)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_ranks(args.gpus)
+    world = dist_setup()[0]
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -156,9 +156,9 @@ SPX_API int32_t spx_engine_segment(spx_engine *eng, const uint8_t *rgb_dev, int6
                            int64_t *counts_dev, int32_t *passes_dev, void *stream);
 
 /* Same with HOST buffers (any batch size): frames are processed in chunks of
- * up to 32 through double-buffered device staging on three streams, so the
- * H2D copy of the next chunk and the D2H copy of the previous one overlap the
- * compute of the current one.  Pinned host buffers make the copies
+ * up to 64 (spx_engine_set_host_chunk) through three device staging slots on
+ * three streams (H2D, compute, D2H), so the H2D copy of the next chunk and the
+ * D2H copy of the previous one overlap the compute of the current one.  Pinned host buffers make the copies
  * asynchronous (pageable ones are correct but serialised).  Synchronous. */
 SPX_API int32_t spx_engine_segment_host(spx_engine *eng, const uint8_t *rgb_host, int64_t batch,
                                 int32_t *labels_host, double *cxy_host, double *clab_host,
@@ -177,6 +177,10 @@ SPX_API int32_t spx_engine_wait(spx_engine *eng);
  * that submission only, so a caller can consume batch i while i+1 runs. */
 SPX_API int64_t spx_engine_ticket(spx_engine *eng);
 SPX_API int32_t spx_engine_wait_ticket(spx_engine *eng, int64_t ticket);
+/* Device time (ms, compute stream) of the submission that returned `ticket`
+ * (kept for the last 8 submissions); waits for that submission's compute
+ * only -- unlike spx_engine_timing, which describes the newest call. */
+SPX_API int32_t spx_engine_ticket_time(spx_engine *eng, int64_t ticket, float *ms);
 /* Frames per host-pipeline chunk (default 64, capped at max_batch); waits for
  * submitted work and re-allocates the staging buffers. */
 SPX_API int32_t spx_engine_set_host_chunk(spx_engine *eng, int64_t frames);

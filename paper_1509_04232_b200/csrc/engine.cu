@@ -136,12 +136,18 @@ struct Engine {
     SPX_CUDA(cudaSetDevice(device));
     if (!lane_fork) SPX_CUDA(cudaEventCreateWithFlags(&lane_fork, cudaEventDisableTiming));
     const int64_t per = ceil_div(max_batch, (int64_t)n);
-    // a lane created for a smaller split cannot take this one's sub-batch
+    // a lane created for a smaller split cannot take this one's sub-batch;
+    // graphs captured over the old children hold their buffer pointers, so
+    // every lane graph goes with them (a later call with the same key
+    // re-captures over the new children)
+    bool replaced = false;
     for (size_t i = 0; i < lane_eng.size(); ++i)
       if (lane_eng[i] && lane_eng[i]->max_batch < per) {
         delete lane_eng[i];
         lane_eng[i] = nullptr;
+        replaced = true;
       }
+    if (replaced) drop_lane_graphs();
     while ((int)lane_eng.size() < n) {
       lane_eng.push_back(nullptr);
       cudaStream_t q;
@@ -165,6 +171,7 @@ struct Engine {
   }
 
   void free_lanes() {
+    drop_lane_graphs();
     for (auto c : lane_eng) delete c;
     lane_eng.clear();
     for (auto q : lane_st) cudaStreamDestroy(q);
@@ -326,8 +333,14 @@ struct Engine {
     int n_assoc, n_update;
     int64_t launches;
     int eager_calls;
+    uint64_t id;
+    bool stages_ok;  // `stages` holds this key's warm eager breakdown
     spx_timing stages;
   };
+  uint64_t next_graph_id = 1;
+  // id of the entry whose second (warm) eager call was the engine's last
+  // call: timing() of that call also fills the entry's stage breakdown
+  uint64_t stage_pending = 0;
   const GraphEntry* last_graph = nullptr;
   std::vector<GraphEntry> graphs;
   cudaStream_t s_cap = nullptr;
@@ -346,6 +359,20 @@ struct Engine {
   }
   const bool use_graphs = getenv("SPX_NO_GRAPHS") == nullptr;
 
+  // Graph entries whose capture forked into the lane children (lanes > 1).
+  void drop_lane_graphs() {
+    last_graph = nullptr;
+    std::vector<GraphEntry> keep;
+    for (auto& g : graphs) {
+      if (g.lanes > 1) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+      } else {
+        keep.push_back(g);
+      }
+    }
+    graphs.swap(keep);
+  }
+
   void free_graphs() {
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -362,6 +389,8 @@ struct Engine {
     }
     SPX_CUDA(cudaSetDevice(device));
     last_graph = nullptr;
+    const uint64_t prev_pending = stage_pending;
+    stage_pending = 0;
     int nl = lanes_for(batch);
     if (nl > 1) {
       const int rl = ensure_lanes(nl);
@@ -399,16 +428,27 @@ struct Engine {
       e.batch = batch;
       e.lanes = nl;
       e.eager_calls = 1;
+      e.id = next_graph_id++;
       graphs.push_back(e);
       return run(s);
     }
     if (!g->exec && g->eager_calls < 2) {  // second call: eager and warm
       ++g->eager_calls;
-      return run(s);
+      const int rc = run(s);
+      if (rc == SPX_OK) stage_pending = g->id;
+      return rc;
     }
-    if (!g->exec) {  // third call: keep the warm eager call's stage times, capture
-      int rt = timing(&g->stages);
-      if (rt) return rt;
+    if (!g->exec) {  // third call: capture
+      // The stage breakdown replays report is the warm eager call's: taken
+      // by timing() if the caller asked for it, else here when that call
+      // was this engine's last one (its events are still the newest).  An
+      // interleaved key in between leaves the breakdown unknown (zeros;
+      // replays still measure their total).
+      if (!g->stages_ok && prev_pending == g->id) {
+        int rt = timing(&g->stages);
+        if (rt) return rt;
+        g->stages_ok = true;
+      }
       if (!s_cap) SPX_CUDA(cudaStreamCreateWithFlags(&s_cap, cudaStreamNonBlocking));
       SPX_CUDA(cudaStreamBeginCapture(s_cap, cudaStreamCaptureModeRelaxed));
       capturing = true;
@@ -573,6 +613,7 @@ struct Engine {
       int rc = lane_eng[0]->timing(t);
       if (rc) return rc;
       t->total = el(ev[EV_START], ev[EV_END]);
+      keep_pending_stages(*t);
       return SPX_OK;
     }
     t->convert = el(ev[EV_START], ev[EV_CONVERT]);
@@ -584,7 +625,18 @@ struct Engine {
     t->n_update = std::min(n_update, 1024);
     for (int i = 0; i < t->n_associate; ++i) t->associate[i] = el(ev_assoc[2 * i], ev_assoc[2 * i + 1]);
     for (int i = 0; i < t->n_update; ++i) t->update[i] = el(ev_update[2 * i], ev_update[2 * i + 1]);
+    keep_pending_stages(*t);
     return SPX_OK;
+  }
+
+  void keep_pending_stages(const spx_timing& t) {
+    if (!stage_pending) return;
+    for (auto& g : graphs)
+      if (g.id == stage_pending && !g.stages_ok) {
+        g.stages = t;
+        g.stages_ok = true;
+      }
+    stage_pending = 0;
   }
 
   // ---- host-buffer entry point: chunked, triple-buffered, three streams -------
@@ -637,6 +689,11 @@ struct Engine {
       h_cnt[i] = nullptr, h_pass[i] = nullptr;
       ev_h2d[i] = ev_comp[i] = ev_d2h[i] = nullptr;
     }
+    for (auto& r : subs) {
+      if (r.a) cudaEventDestroy(r.a);
+      if (r.b) cudaEventDestroy(r.b);
+      r = SubRec();
+    }
     for (cudaStream_t q : {s_h2d, s_comp, s_d2h})
       if (q) cudaStreamDestroy(q);
     s_h2d = s_comp = s_d2h = nullptr;
@@ -664,6 +721,15 @@ struct Engine {
   // only the very first H2D and the last D2H are exposed.
   int64_t seq = 0;
   std::vector<cudaEvent_t> tl;  // SPX_DEBUG_TIMELINE=1 per-chunk timeline
+  // Device time of each submission (compute stream: first chunk's start to
+  // last chunk's end), kept for the last kSubRing submissions so a consumer
+  // of batch i can read its time without waiting for batch i+1.
+  static constexpr int kSubRing = 8;
+  struct SubRec {
+    int64_t ticket = 0;
+    cudaEvent_t a = nullptr, b = nullptr;
+  } subs[kSubRing];
+  int64_t n_subs = 0;
 
   int submit_host(const uint8_t* rgb, int64_t batch, int32_t* out_labels, double* out_xy,
                   double* out_lab, int64_t* out_counts, int32_t* out_passes) {
@@ -675,6 +741,11 @@ struct Engine {
       return SPX_ERR_VALUE;
     }
     const int64_t nchunks = ceil_div(batch, chunk);
+    SubRec& sr = subs[n_subs % kSubRing];
+    if (!sr.a) {
+      SPX_CUDA(cudaEventCreate(&sr.a));
+      SPX_CUDA(cudaEventCreate(&sr.b));
+    }
     static const bool dbg = getenv("SPX_DEBUG_TIMELINE") != nullptr;
     auto mark = [&](cudaStream_t q) {
       if (!dbg) return;
@@ -694,11 +765,13 @@ struct Engine {
       SPX_CUDA(cudaEventRecord(ev_h2d[sl], s_h2d));
       SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_h2d[sl], 0));
       if (seq >= kSlots) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
+      if (c == 0) SPX_CUDA(cudaEventRecord(sr.a, s_comp));
       mark(s_comp);
       if ((rc = segment(h_rgb[sl], nb, h_lab[sl], h_xy[sl], h_cl[sl], h_cnt[sl], h_pass[sl],
                         s_comp)))
         return rc;
       mark(s_comp);
+      if (c == nchunks - 1) SPX_CUDA(cudaEventRecord(sr.b, s_comp));
       SPX_CUDA(cudaEventRecord(ev_comp[sl], s_comp));
       SPX_CUDA(cudaStreamWaitEvent(s_d2h, ev_comp[sl], 0));
       mark(s_d2h);
@@ -720,7 +793,24 @@ struct Engine {
       mark(s_d2h);
       SPX_CUDA(cudaEventRecord(ev_d2h[sl], s_d2h));
     }
+    sr.ticket = seq;
+    ++n_subs;
     return SPX_OK;
+  }
+
+  // Compute-stream time (ms) of the submission that returned `ticket`; waits
+  // for that submission's compute only.
+  int ticket_time(int64_t ticket, float* ms) {
+    SPX_CUDA(cudaSetDevice(device));
+    for (auto& r : subs)
+      if (r.a && r.ticket == ticket && ticket > 0) {
+        SPX_CUDA(cudaEventSynchronize(r.b));
+        SPX_CUDA(cudaEventElapsedTime(ms, r.a, r.b));
+        return SPX_OK;
+      }
+    set_error("no timing kept for ticket %lld (the last %d submissions are kept)",
+              (long long)ticket, kSubRing);
+    return SPX_ERR_VALUE;
   }
 
   // Wait for the submissions up to `ticket` (a value of `seq` after a submit).
@@ -839,6 +929,10 @@ int64_t spx_engine_ticket(spx_engine* eng) { return eng->e.seq; }
 
 int32_t spx_engine_wait_ticket(spx_engine* eng, int64_t ticket) {
   return eng->e.wait_ticket(ticket);
+}
+
+int32_t spx_engine_ticket_time(spx_engine* eng, int64_t ticket, float* ms) {
+  return eng->e.ticket_time(ticket, ms);
 }
 
 int32_t spx_engine_set_host_chunk(spx_engine* eng, int64_t frames) {

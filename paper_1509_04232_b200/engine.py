@@ -149,9 +149,15 @@ class SegEngine:
             raise DimensionMismatchError(
                 f"frames must be contiguous CUDA uint8 (B, {st.img_height}, {st.img_width}, 3), "
                 f"got {tuple(rgb.shape)} {rgb.dtype}")
+        dev = t.device("cuda", self.device)
+        if rgb.device != dev:
+            raise DimensionMismatchError(f"frames are on {rgb.device}, engine runs on {dev}")
         b = rgb.shape[0]
+        if b < 1 or b > self.max_batch:
+            raise DimensionMismatchError(f"batch {b} outside [1, {self.max_batch}] (max_batch)")
         if out is None:
             out = self.allocate_outputs(b)
+        self._check_outputs(out, b)
         labels, cxy, clab, counts, passes = out
         s = stream if stream is not None else t.cuda.current_stream(self.device)
         _lib.check(self._lib.spx_engine_segment(
@@ -160,6 +166,28 @@ class SegEngine:
             ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(passes.data_ptr()),
             ctypes.c_void_p(s.cuda_stream)), "segment")
         return out
+
+    def _check_outputs(self, out, b):
+        """Output tensors must hold (at least) `b` frames: the kernels write
+        b frames' worth of results through raw pointers."""
+        t = self._torch
+        st = self.settings
+        k = self.grid.num_clusters
+        if not isinstance(out, (tuple, list)) or len(out) != 5:
+            raise DimensionMismatchError("out must be (labels, cxy, clab, counts, passes)")
+        dev = t.device("cuda", self.device)
+        for name, a, shape, dt in (("labels", out[0], (st.img_height, st.img_width), t.int32),
+                                   ("cxy", out[1], (k, 2), t.float64),
+                                   ("clab", out[2], (k, 3), t.float64),
+                                   ("counts", out[3], (k,), t.int64),
+                                   ("passes", out[4], (), t.int32)):
+            if (not isinstance(a, t.Tensor) or a.dtype != dt or a.device != dev
+                    or not a.is_contiguous() or a.dim() != 1 + len(shape)
+                    or tuple(a.shape[1:]) != shape or a.shape[0] < b):
+                got = (tuple(a.shape), a.dtype, str(a.device)) if isinstance(a, t.Tensor) else type(a)
+                raise DimensionMismatchError(
+                    f"out {name} must be a contiguous {dt} tensor on {dev} of shape "
+                    f"(>= {b}, {', '.join(map(str, shape))}), got {got}")
 
     def segment_host(self, rgb, labels=None, cxy=None, clab=None, counts=None, passes=None):
         """Segment host uint8 frames (B, H, W, 3) through the C ABI's host-buffer call.
@@ -219,6 +247,14 @@ class SegEngine:
     def wait_ticket(self, ticket):
         """Wait for the submission that returned `ticket` (and all before it)."""
         _lib.check(self._lib.spx_engine_wait_ticket(self._h, int(ticket)), "wait_ticket")
+
+    def ticket_time(self, ticket):
+        """Device time (seconds) of the submission that returned `ticket`;
+        waits for that submission's compute only."""
+        ms = ctypes.c_float()
+        _lib.check(self._lib.spx_engine_ticket_time(self._h, int(ticket), ctypes.byref(ms)),
+                   "ticket_time")
+        return ms.value * 1e-3
 
     def set_host_chunk(self, frames):
         """Frames per H2D/compute/D2H pipeline chunk of the host-buffer path."""
@@ -335,8 +371,15 @@ def segment_stream(engine, imgs):
         ticket, slot, n = inflight.popleft()
         engine.wait_ticket(ticket)
         bufs = sets[slot]
+        # This batch's own device time (engine.last_timing() would describe,
+        # and wait for, the newest submission); per-stage times are not kept
+        # per submission and read 0.
+        total = engine.ticket_time(ticket)
+        passes = bufs[5][:n]
+        n_up = int(passes.max()) if n else 0
+        tm = StageTiming(0.0, 0.0, 0.0, (0.0,) * (n_up + 1), (0.0,) * n_up, 0.0, total)
         # copies: the pinned set is reused by the next-but-one batch
-        return engine._results(*(b[:n].copy() for b in bufs[1:]), engine.last_timing())
+        return engine._results(*(b[:n].copy() for b in bufs[1:]), tm)
 
     pending, slot = [], 0
     try:

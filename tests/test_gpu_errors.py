@@ -47,6 +47,34 @@ def test_segment_device_rejects_bad_tensors():
     labels = eng.segment_device(good)[0]
     torch.cuda.synchronize()
     assert tuple(labels.shape) == (2, 16, 32)
+    # caller-supplied outputs: too few frames, wrong dtype, not contiguous,
+    # wrong device, wrong arity -- all rejected before any kernel runs
+    outs = eng.allocate_outputs(2)
+    small = eng.allocate_outputs(1)
+    for i in range(5):
+        bad = list(outs)
+        bad[i] = small[i]
+        with pytest.raises(spx.DimensionMismatchError):
+            eng.segment_device(good, tuple(bad))
+    bad = list(outs)
+    bad[1] = outs[1].float()
+    with pytest.raises(spx.DimensionMismatchError):
+        eng.segment_device(good, tuple(bad))
+    bad = list(outs)
+    bad[0] = torch.empty((2, 32, 16), dtype=torch.int32, device="cuda").transpose(1, 2)
+    with pytest.raises(spx.DimensionMismatchError):
+        eng.segment_device(good, tuple(bad))
+    bad = list(outs)
+    bad[3] = outs[3].cpu()
+    with pytest.raises(spx.DimensionMismatchError):
+        eng.segment_device(good, tuple(bad))
+    with pytest.raises(spx.DimensionMismatchError):
+        eng.segment_device(good, outs[:4])
+    # a larger output set is fine (the first b frames are written)
+    big = spx.SegEngine(st, max_batch=3).allocate_outputs(3)
+    eng.segment_device(good, big)
+    torch.cuda.synchronize()
+    assert np.array_equal(big[0][:2].cpu().numpy(), labels.cpu().numpy())
 
 
 def test_batch_larger_than_engine():

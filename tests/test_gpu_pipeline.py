@@ -332,6 +332,44 @@ def test_lanes_in_graph_replay():
                 assert a.tobytes() == b.cpu().numpy().tobytes(), (lanes, call)
 
 
+def test_lanes_graph_cache_survives_child_replacement():
+    # an automatic 4-lane graph captured over 8-frame children,
+    # then a call whose 3-lane split needs bigger children (they are
+    # replaced), then the first key again -- the old graph must not replay
+    # over the freed children.  Same with explicit lane counts 3 -> 2 -> 3.
+    import torch
+    h, w = 64, 96
+    st = spx.Settings(img_width=w, img_height=h, num_superpixels=24)
+    frames = np.stack([_images(h, w, 1200 + i)["noise"] for i in range(32)])
+    d = torch.from_numpy(frames).cuda()
+    ref = spx.SegEngine(st, max_batch=32)
+    ref.set_lanes(1)
+    want = [t.cpu().numpy() for t in ref.segment_device(d)]
+
+    def check(eng, outs, n):
+        for t in outs:
+            t.zero_()
+        eng.segment_device(d[:n], tuple(t[:n] for t in outs))
+        torch.cuda.synchronize()
+        for a, b in zip(want, outs):
+            assert a[:n].tobytes() == b[:n].cpu().numpy().tobytes(), n
+
+    eng = spx.SegEngine(st, max_batch=32)
+    outs = eng.allocate_outputs(32)
+    for _ in range(4):  # eager, eager, capture, replay (4 lanes of 8)
+        check(eng, outs, 8)
+    eng.set_lanes(3)  # children of ceil(32 / 3) = 11 frames replace the 8-frame ones
+    for _ in range(4):
+        check(eng, outs, 12)
+    eng.set_lanes(0)
+    for _ in range(3):
+        check(eng, outs, 8)
+    for lanes in (3, 2, 3):
+        eng.set_lanes(lanes)
+        for _ in range(4):
+            check(eng, outs, 16)
+
+
 def test_cell_path_batch_gray_heavy_frames():
     h, w = 480, 640
     st = spx.Settings(img_width=w, img_height=h, num_superpixels=1200)

@@ -171,6 +171,20 @@ def test_frame_hashes(golden_meta, case):
     assert sha(cxy) == m["cxy"] and sha(clab) == m["clab"] and sha(counts) == m["counts"]
 
 
+@pytest.mark.parametrize("case", ["large_C3_f0", "large_T1_963x1024_k2000",
+                                  "large_T1_933x800_k1000"])
+def test_large_frame_hashes(golden_meta, case):
+    """Reference hashes of tests/golden/make_golden_large.py (BASELINE C3,
+    PAPER.md Table 1 sizes with W % 4 != 0) pin the oracle at full size."""
+    m = golden_meta["hashes"][case]
+    rgb = np.random.default_rng(m["seed"]).integers(0, 256, (m["h"], m["w"], 3), dtype=np.uint8)
+    s, ns_r, ns_c = _grid(m["w"], m["h"], m["settings"])
+    labels, cxy, clab, counts, _ = oracle.segment(rgb, s, ns_r, ns_c, 10.0,
+                                                  no_iters=m["settings"].get("no_iters", 5))
+    assert sha(labels) == m["labels"]
+    assert sha(cxy) == m["cxy"] and sha(clab) == m["clab"] and sha(counts) == m["counts"]
+
+
 def test_center_shift_matches_numpy():
     rng = np.random.default_rng(5)
     for k in (1, 3, 4, 7, 60, 64, 65, 200, 1200, 8160, 50000):
