@@ -164,6 +164,12 @@ SPX_API int32_t spx_engine_segment_host(spx_engine *eng, const uint8_t *rgb_host
                                 int32_t *labels_host, double *cxy_host, double *clab_host,
                                 int64_t *counts_host, int32_t *passes_host);
 
+/* Byte offsets of the five outputs of `batch` frames laid out in ONE host
+ * block: out6 = {labels, cxy, clab, counts, passes, total bytes}.  Host
+ * outputs placed at these offsets from labels_host (pinned) are copied back
+ * with a single D2H per call (batch <= the host chunk). */
+SPX_API int32_t spx_engine_output_layout(spx_engine *eng, int64_t batch, int64_t *out6);
+
 /* Asynchronous form of spx_engine_segment_host for streams of batches: enqueues
  * the batch's H2D / compute / D2H chunks and returns.  Consecutive submits
  * continue one pipeline, so the copies of batch i overlap the compute of

@@ -70,6 +70,7 @@ SIGNATURES = {
     "spx_engine_ticket": (I64, [P]),
     "spx_engine_wait_ticket": (I32, [P, I64]),
     "spx_engine_ticket_time": (I32, [P, I64, ctypes.POINTER(ctypes.c_float)]),
+    "spx_engine_output_layout": (I32, [P, I64, P]),
     "spx_engine_set_host_chunk": (I32, [P, I64]),
     "spx_engine_set_lanes": (I32, [P, I32]),
     "spx_engine_last_lanes": (I32, [P]),

@@ -123,7 +123,10 @@ constexpr int kGroupsPerWarp = 4;  // max consecutive cell groups walked by one 
 #ifndef SPX_MINB
 #define SPX_MINB 4  // resident blocks per SM the register budget is sized for
 #endif
-__host__ __device__ constexpr size_t cand_bytes(int lpc) { return (size_t)(32 / lpc) * 9 * 24; }
+// (rounded up to 16 bytes: the accumulators behind it take 16-byte accesses)
+__host__ __device__ constexpr size_t cand_bytes(int lpc) {
+  return ((size_t)(32 / lpc) * 9 * 24 + 15) & ~(size_t)15;
+}
 // Accumulator columns start on bank 0 (stride 32 entries), so the per-pixel
 // updates (lane l touches entry l of its slot's column) are conflict-free
 // whatever slots the lanes pick; in the epilogue, where a lane sums a whole
@@ -877,10 +880,12 @@ bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
 // cells (batch 16: LPC 16 is 5% slower).
 static int cell_lpc(int64_t s, long long cells) {
   static const int env = getenv("SPX_LPC") ? atoi(getenv("SPX_LPC")) : 0;  // development
-  if (env == 4 || env == 8 || env == 16) return env;
+  if (env == 4 || env == 8 || env == 16 || env == 32) return env;
   int lpc = s <= 12 ? 4 : (s <= 24 ? 8 : 16);
   const long long runs = s * ceil_div(s, 4);
-  if (lpc < 16 && cells * lpc < (long long)num_sms() * 16 * 32 && runs >= 2 * lpc) lpc *= 2;
+  // up to two doublings (a single 640x480 frame: 8 -> 32 lanes per cell)
+  for (int d = 0; d < 2; ++d)
+    if (lpc < 32 && cells * lpc < (long long)num_sms() * 16 * 32 && runs >= 2 * lpc) lpc *= 2;
   return lpc;
 }
 
@@ -957,9 +962,10 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
     return SPX_ERR_VALUE;
   }
   const size_t smem = (size_t)kWarps * warp_smem(lpc, acc);
-  const int rc = lpc == 4   ? launch_cell_lpc<4>(p, blocks, smem, st, acc)
-                 : lpc == 8 ? launch_cell_lpc<8>(p, blocks, smem, st, acc)
-                            : launch_cell_lpc<16>(p, blocks, smem, st, acc);
+  const int rc = lpc == 4    ? launch_cell_lpc<4>(p, blocks, smem, st, acc)
+                 : lpc == 8  ? launch_cell_lpc<8>(p, blocks, smem, st, acc)
+                 : lpc == 16 ? launch_cell_lpc<16>(p, blocks, smem, st, acc)
+                             : launch_cell_lpc<32>(p, blocks, smem, st, acc);
   if (rc) return rc;
   SPX_LAUNCH_CHECK("k_cell");
   return SPX_OK;

@@ -650,24 +650,32 @@ struct Engine {
   // with the next upload, is the longest of the three stages).
   static constexpr int kSlots = 3;
   uint8_t* h_rgb[kSlots] = {};
-  int32_t* h_lab[kSlots] = {};
-  double* h_xy[kSlots] = {};
-  double* h_cl[kSlots] = {};
-  int64_t* h_cnt[kSlots] = {};
-  int32_t* h_pass[kSlots] = {};
+  uint8_t* h_out[kSlots] = {};  // one block per slot, carved by out_layout(nb)
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_h2d[kSlots] = {}, ev_comp[kSlots] = {}, ev_d2h[kSlots] = {};
+
+  // Byte offsets of the five outputs of `nb` frames in one block (256-byte
+  // aligned): labels, cxy, clab, counts, passes, total.  A caller whose host
+  // outputs follow the same layout (spx_engine_output_layout) gets one D2H
+  // copy per chunk instead of five.
+  void out_layout(int64_t nb, int64_t* o) const {
+    auto al = [](int64_t v) { return (v + 255) & ~(int64_t)255; };
+    o[0] = 0;
+    o[1] = al(nb * hw * 4);
+    o[2] = o[1] + al(nb * K * 16);
+    o[3] = o[2] + al(nb * K * 24);
+    o[4] = o[3] + al(nb * K * 8);
+    o[5] = o[4] + nb * 4;
+  }
 
   int ensure_staging() {
     if (s_comp) return SPX_OK;
     chunk = std::max<int64_t>(1, std::min<int64_t>(max_batch, chunk_req));
+    int64_t lay[6];
+    out_layout(chunk, lay);
     for (int i = 0; i < kSlots; ++i) {
       SPX_CUDA(cudaMalloc(&h_rgb[i], chunk * hw * 3));
-      SPX_CUDA(cudaMalloc(&h_lab[i], chunk * hw * sizeof(int32_t)));
-      SPX_CUDA(cudaMalloc(&h_xy[i], chunk * K * 2 * sizeof(double)));
-      SPX_CUDA(cudaMalloc(&h_cl[i], chunk * K * 3 * sizeof(double)));
-      SPX_CUDA(cudaMalloc(&h_cnt[i], chunk * K * sizeof(int64_t)));
-      SPX_CUDA(cudaMalloc(&h_pass[i], chunk * sizeof(int32_t)));
+      SPX_CUDA(cudaMalloc(&h_out[i], lay[5]));
       SPX_CUDA(cudaEventCreateWithFlags(&ev_h2d[i], cudaEventDisableTiming));
       SPX_CUDA(cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming));
       SPX_CUDA(cudaEventCreateWithFlags(&ev_d2h[i], cudaEventDisableTiming));
@@ -680,13 +688,11 @@ struct Engine {
 
   void free_staging() {
     for (int i = 0; i < kSlots; ++i) {
-      for (void* q : {(void*)h_rgb[i], (void*)h_lab[i], (void*)h_xy[i], (void*)h_cl[i],
-                      (void*)h_cnt[i], (void*)h_pass[i]})
+      for (void* q : {(void*)h_rgb[i], (void*)h_out[i]})
         if (q) cudaFree(q);
       for (cudaEvent_t e : {ev_h2d[i], ev_comp[i], ev_d2h[i]})
         if (e) cudaEventDestroy(e);
-      h_rgb[i] = nullptr, h_lab[i] = nullptr, h_xy[i] = nullptr, h_cl[i] = nullptr;
-      h_cnt[i] = nullptr, h_pass[i] = nullptr;
+      h_rgb[i] = nullptr, h_out[i] = nullptr;
       ev_h2d[i] = ev_comp[i] = ev_d2h[i] = nullptr;
     }
     for (auto& r : subs) {
@@ -731,8 +737,12 @@ struct Engine {
   } subs[kSubRing];
   int64_t n_subs = 0;
 
+  // `sync`: the caller waits for this call right away (segment_host).  A
+  // one-chunk synchronous call then runs H2D, compute and D2H on the compute
+  // stream alone (no cross-stream event hops: one 640x480 frame's call is
+  // latency-bound), still ordered after earlier submissions of the slot.
   int submit_host(const uint8_t* rgb, int64_t batch, int32_t* out_labels, double* out_xy,
-                  double* out_lab, int64_t* out_counts, int32_t* out_passes) {
+                  double* out_lab, int64_t* out_counts, int32_t* out_passes, bool sync = false) {
     SPX_CUDA(cudaSetDevice(device));
     int rc = ensure_staging();
     if (rc) return rc;
@@ -741,6 +751,17 @@ struct Engine {
       return SPX_ERR_VALUE;
     }
     const int64_t nchunks = ceil_div(batch, chunk);
+    const bool one_stream = sync && nchunks == 1;
+    cudaStream_t q_h2d = one_stream ? s_comp : s_h2d, q_d2h = one_stream ? s_comp : s_d2h;
+    // host outputs laid out as one block (spx_engine_output_layout): one D2H
+    int64_t hl[6];
+    out_layout(batch, hl);
+    const char* hb = reinterpret_cast<const char*>(out_labels);
+    const bool host_block = nchunks == 1 && out_labels &&
+                            reinterpret_cast<const char*>(out_xy) == hb + hl[1] &&
+                            reinterpret_cast<const char*>(out_lab) == hb + hl[2] &&
+                            reinterpret_cast<const char*>(out_counts) == hb + hl[3] &&
+                            reinterpret_cast<const char*>(out_passes) == hb + hl[4];
     SubRec& sr = subs[n_subs % kSubRing];
     if (!sr.a) {
       SPX_CUDA(cudaEventCreate(&sr.a));
@@ -757,46 +778,61 @@ struct Engine {
     for (int64_t c = 0; c < nchunks; ++c, ++seq) {
       const int sl = (int)(seq % kSlots);
       const int64_t f0 = c * chunk, nb = std::min(chunk, batch - f0);
-      if (seq >= kSlots) SPX_CUDA(cudaStreamWaitEvent(s_h2d, ev_comp[sl], 0));
-      mark(s_h2d);
+      int64_t lay[6];
+      out_layout(nb, lay);
+      uint8_t* ob = h_out[sl];
+      int32_t* d_lab = reinterpret_cast<int32_t*>(ob + lay[0]);
+      double* d_xy = reinterpret_cast<double*>(ob + lay[1]);
+      double* d_cl = reinterpret_cast<double*>(ob + lay[2]);
+      int64_t* d_cnt = reinterpret_cast<int64_t*>(ob + lay[3]);
+      int32_t* d_pass = reinterpret_cast<int32_t*>(ob + lay[4]);
+      if (seq >= kSlots) SPX_CUDA(cudaStreamWaitEvent(q_h2d, ev_comp[sl], 0));
+      if (seq >= kSlots && one_stream) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
+      mark(q_h2d);
       SPX_CUDA(cudaMemcpyAsync(h_rgb[sl], rgb + f0 * hw * 3, nb * hw * 3, cudaMemcpyHostToDevice,
-                               s_h2d));
-      mark(s_h2d);
-      SPX_CUDA(cudaEventRecord(ev_h2d[sl], s_h2d));
-      SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_h2d[sl], 0));
-      if (seq >= kSlots) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
+                               q_h2d));
+      mark(q_h2d);
+      if (!one_stream) {
+        SPX_CUDA(cudaEventRecord(ev_h2d[sl], s_h2d));
+        SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_h2d[sl], 0));
+        if (seq >= kSlots) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
+      }
       if (c == 0) SPX_CUDA(cudaEventRecord(sr.a, s_comp));
       mark(s_comp);
-      if ((rc = segment(h_rgb[sl], nb, h_lab[sl], h_xy[sl], h_cl[sl], h_cnt[sl], h_pass[sl],
-                        s_comp)))
-        return rc;
+      if ((rc = segment(h_rgb[sl], nb, d_lab, d_xy, d_cl, d_cnt, d_pass, s_comp))) return rc;
       mark(s_comp);
       if (c == nchunks - 1) SPX_CUDA(cudaEventRecord(sr.b, s_comp));
       SPX_CUDA(cudaEventRecord(ev_comp[sl], s_comp));
-      SPX_CUDA(cudaStreamWaitEvent(s_d2h, ev_comp[sl], 0));
-      mark(s_d2h);
-      if (out_labels)
-        SPX_CUDA(cudaMemcpyAsync(out_labels + f0 * hw, h_lab[sl], nb * hw * 4,
-                                 cudaMemcpyDeviceToHost, s_d2h));
-      if (out_xy)
-        SPX_CUDA(cudaMemcpyAsync(out_xy + f0 * K * 2, h_xy[sl], nb * K * 16, cudaMemcpyDeviceToHost,
-                                 s_d2h));
-      if (out_lab)
-        SPX_CUDA(cudaMemcpyAsync(out_lab + f0 * K * 3, h_cl[sl], nb * K * 24,
-                                 cudaMemcpyDeviceToHost, s_d2h));
-      if (out_counts)
-        SPX_CUDA(cudaMemcpyAsync(out_counts + f0 * K, h_cnt[sl], nb * K * 8,
-                                 cudaMemcpyDeviceToHost, s_d2h));
-      if (out_passes)
-        SPX_CUDA(cudaMemcpyAsync(out_passes + f0, h_pass[sl], nb * 4, cudaMemcpyDeviceToHost,
-                                 s_d2h));
-      mark(s_d2h);
-      SPX_CUDA(cudaEventRecord(ev_d2h[sl], s_d2h));
+      if (!one_stream) SPX_CUDA(cudaStreamWaitEvent(s_d2h, ev_comp[sl], 0));
+      mark(q_d2h);
+      if (host_block) {
+        SPX_CUDA(cudaMemcpyAsync(out_labels, ob, lay[5], cudaMemcpyDeviceToHost, q_d2h));
+      } else {
+        if (out_labels)
+          SPX_CUDA(cudaMemcpyAsync(out_labels + f0 * hw, d_lab, nb * hw * 4,
+                                   cudaMemcpyDeviceToHost, q_d2h));
+        if (out_xy)
+          SPX_CUDA(cudaMemcpyAsync(out_xy + f0 * K * 2, d_xy, nb * K * 16,
+                                   cudaMemcpyDeviceToHost, q_d2h));
+        if (out_lab)
+          SPX_CUDA(cudaMemcpyAsync(out_lab + f0 * K * 3, d_cl, nb * K * 24,
+                                   cudaMemcpyDeviceToHost, q_d2h));
+        if (out_counts)
+          SPX_CUDA(cudaMemcpyAsync(out_counts + f0 * K, d_cnt, nb * K * 8,
+                                   cudaMemcpyDeviceToHost, q_d2h));
+        if (out_passes)
+          SPX_CUDA(cudaMemcpyAsync(out_passes + f0, d_pass, nb * 4, cudaMemcpyDeviceToHost,
+                                   q_d2h));
+      }
+      mark(q_d2h);
+      SPX_CUDA(cudaEventRecord(ev_d2h[sl], q_d2h));
     }
     sr.ticket = seq;
     ++n_subs;
+    last_sync = one_stream;
     return SPX_OK;
   }
+  bool last_sync = false;
 
   // Compute-stream time (ms) of the submission that returned `ticket`; waits
   // for that submission's compute only.
@@ -831,6 +867,7 @@ struct Engine {
     SPX_CUDA(cudaSetDevice(device));
     if (!s_d2h) return SPX_OK;
     SPX_CUDA(cudaStreamSynchronize(s_d2h));
+    SPX_CUDA(cudaStreamSynchronize(s_comp));  // one-stream calls end there
     if (!tl.empty()) {
       for (size_t i = 0; i + 5 < tl.size(); i += 6) {
         float a0, a1, b0, b1, c0, c1;
@@ -851,7 +888,7 @@ struct Engine {
 
   int segment_host(const uint8_t* rgb, int64_t batch, int32_t* out_labels, double* out_xy,
                    double* out_lab, int64_t* out_counts, int32_t* out_passes) {
-    int rc = submit_host(rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes);
+    int rc = submit_host(rgb, batch, out_labels, out_xy, out_lab, out_counts, out_passes, true);
     int rw = wait_host();
     return rc ? rc : rw;
   }
@@ -929,6 +966,15 @@ int64_t spx_engine_ticket(spx_engine* eng) { return eng->e.seq; }
 
 int32_t spx_engine_wait_ticket(spx_engine* eng, int64_t ticket) {
   return eng->e.wait_ticket(ticket);
+}
+
+int32_t spx_engine_output_layout(spx_engine* eng, int64_t batch, int64_t* out6) {
+  if (batch < 1) {
+    spx::set_error("batch must be >= 1");
+    return SPX_ERR_VALUE;
+  }
+  eng->e.out_layout(batch, out6);
+  return SPX_OK;
 }
 
 int32_t spx_engine_ticket_time(spx_engine* eng, int64_t ticket, float* ms) {

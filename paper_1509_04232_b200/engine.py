@@ -308,11 +308,59 @@ class SegEngine:
                                  timing=tm))
         return out
 
+    def _pinned_outputs(self, b):
+        """Fresh result arrays for `b` frames carved from ONE pinned host block
+        (torch's caching host allocator) in the engine's output layout, so the
+        device results come back with a single D2H copy and need no copy-out.
+        The block lives as long as the returned arrays do."""
+        cache = self.__dict__.setdefault("_layouts", {})
+        spec = cache.get(b)
+        if spec is None:
+            st = self.settings
+            k = self.grid.num_clusters
+            lay = (ctypes.c_int64 * 6)()
+            _lib.check(self._lib.spx_engine_output_layout(self._h, b, lay), "output_layout")
+            shapes = (((b, st.img_height, st.img_width), np.int32), ((b, k, 2), np.float64),
+                      ((b, k, 3), np.float64), ((b, k), np.int64), ((b,), np.int32))
+            spec = (int(lay[5]), [(int(lay[i]), int(np.prod(sh)) * np.dtype(dt).itemsize, sh,
+                                   np.dtype(dt)) for i, (sh, dt) in enumerate(shapes)])
+            cache[b] = spec
+        total, parts = spec
+        blk = self._torch.empty((total,), dtype=self._torch.uint8, pin_memory=True).numpy()
+        return tuple(blk[o:o + n].view(dt).reshape(sh) for o, n, sh, dt in parts)
+
+    def _pinned_input(self, b):
+        """Engine-owned pinned staging for `b` input frames (grown on demand)."""
+        st = self.settings
+        buf = getattr(self, "_pin_in", None)
+        if buf is None or buf.shape[0] < b:
+            t = self._torch
+            buf = t.empty((b, st.img_height, st.img_width, 3), dtype=t.uint8,
+                          pin_memory=True).numpy()
+            self._pin_in = buf
+        return buf[:b]
+
     def perform_segmentation(self, img):
-        """Run the full pipeline on one ImageRGB frame (engine.py:125-230)."""
+        """Run the full pipeline on one ImageRGB frame (engine.py:125-230).
+
+        The frame is staged through an engine-owned pinned buffer and the
+        results land in a fresh pinned block (one D2H); the call is
+        synchronous, as the reference's."""
         self._check_frame(img)
-        res = self.segment_host(img.data)
-        return self._results(*res, self.last_timing())[0]
+        pin = self._pinned_input(1)
+        np.copyto(pin[0], img.data)
+        outs = self._pinned_outputs(1)
+        p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        _lib.check(self._lib.spx_engine_segment_host(self._h, p(pin), 1, *(p(a) for a in outs)),
+                   "segment")
+        labels, cxy, clab, counts, passes = outs
+        n_up = int(passes[0])
+        tm = self.last_timing()
+        tm = StageTiming(tm.convert, tm.init, tm.perturb, tm.associate[:n_up + 1],
+                         tm.update[:n_up], tm.connectivity, tm.total)
+        return SegResult(labels=LabelMap._trusted(labels[0]),
+                         spixel_map=SuperpixelMap(self.grid, cxy[0], clab[0], counts[0]),
+                         timing=tm)
 
     def perform_segmentation_batch(self, imgs):
         """Segment a list of same-sized frames in batches of max_batch."""
