@@ -245,6 +245,10 @@ SPX_API int32_t spx_strip_finish(spx_strip *s, int32_t *labels, double *cxy, dou
 /* Number of kernel launches the last segment call enqueued. */
 SPX_API int64_t spx_engine_last_launches(spx_engine *eng);
 
+/* 1 when the engine runs the fused cell kernels (4 <= S <= 255 and
+ * ceil(3S / tile_len) <= 64 strips), 0 for the generic per-stage kernels. */
+SPX_API int32_t spx_engine_fused_path(spx_engine *eng);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,7 @@ SIGNATURES = {
     "spx_engine_last_lanes": (I32, [P]),
     "spx_engine_timing": (I32, [P, ctypes.POINTER(SpxTiming)]),
     "spx_engine_last_launches": (I64, [P]),
+    "spx_engine_fused_path": (I32, [P]),
     "spx_strip_create": (I32, [ctypes.POINTER(SpxSettings), I64, I64, I32, ctypes.POINTER(P)]),
     "spx_strip_destroy": (I32, [P]),
     "spx_strip_geometry": (I32, [P, P]),

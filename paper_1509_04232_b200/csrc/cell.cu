@@ -76,12 +76,13 @@ struct CellParams {
   int32_t* wl;             // (ACC, may be null) flagged clusters are appended here
   int32_t* wl_n;           //   by their first flagged contribution
   int h, w, s, ns_r, ns_c, frames;
+  long long plane;         // planar Lab channel stride (plane_of(h * w))
   int cr0, cr1;            // cell rows processed (local grid)
   int row_off;             // global cell row of local row 0 (strips; 0 otherwise)
   int runs_per_row;        // ceil(S / 4)
   int runs;                // S * runs_per_row
   int groups_per_warp;     // cell groups walked by one warp
-  unsigned row_magic;      // ceil(2^16 / runs_per_row)
+  unsigned row_magic;      // ceil(2^32 / runs_per_row)
   double xy_weight;
   float w32, k_mp, k_mc, k_xy, k_const, k_rel;
 };
@@ -119,6 +120,7 @@ __device__ __noinline__ int exact_argmin(const double* __restrict__ cxy, const d
 // With LPC >= 8 the per-warp block is <= 10 KB, so 16 warps fit the 164 KB
 // shared-memory carve-out and leave 92 KB of L1 for the Lab stream.
 constexpr int kWarps = 4;
+constexpr int kCellMaxS = 255;
 constexpr int kGroupsPerWarp = 4;  // max consecutive cell groups walked by one warp
 #ifndef SPX_MINB
 #define SPX_MINB 4  // resident blocks per SM the register budget is sized for
@@ -171,14 +173,14 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
   unsigned long long* acci =
       reinterpret_cast<unsigned long long*>(wbase + cand_bytes(LPC) + 9 * 3 * 32 * sizeof(double));
 
-  const long long hw = (long long)p.h * p.w;
-  const float* fimg = p.img + (long long)f * 3 * hw;
+  const long long hw = (long long)p.h * p.w, pl = p.plane;
+  const float* fimg = p.img + (long long)f * 3 * pl;
   const CRec* frec = p.rec + (long long)f * K;
   const long long img_base = (long long)f * hw;
   const unsigned rmag = p.row_magic;
-  // row = j / runs_per_row via a 16-bit reciprocal (exact for j <= 256, rpr <= 8)
+  // row = j / runs_per_row via a 32-bit reciprocal (exact for j, rpr < 2^16)
   auto run_pos = [&](int jj, int& row, int& c4) {
-    row = (int)(((unsigned)jj * rmag) >> 16);
+    row = rmag ? (int)__umulhi((unsigned)jj, rmag) : jj;  // rmag = 0: one run per row
     c4 = (jj - row * p.runs_per_row) * 4;
   };
   // valid pixels of the run starting at cell column c4, image column x
@@ -188,16 +190,16 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
     const float* q = fimg + (long long)y * p.w + x;
     if (AL) {
       Lx = __ldg(reinterpret_cast<const float4*>(q));
-      Ax = __ldg(reinterpret_cast<const float4*>(q + hw));
-      Bx = __ldg(reinterpret_cast<const float4*>(q + 2 * hw));
+      Ax = __ldg(reinterpret_cast<const float4*>(q + pl));
+      Bx = __ldg(reinterpret_cast<const float4*>(q + 2 * pl));
     } else {
       float l[4] = {0.f, 0.f, 0.f, 0.f}, a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         if (i < nv) {
           l[i] = __ldg(q + i);
-          a[i] = __ldg(q + hw + i);
-          b[i] = __ldg(q + 2 * hw + i);
+          a[i] = __ldg(q + pl + i);
+          b[i] = __ldg(q + 2 * pl + i);
         }
       Lx = make_float4(l[0], l[1], l[2], l[3]);
       Ax = make_float4(a[0], a[1], a[2], a[3]);
@@ -412,18 +414,36 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
           } else {
             const ulonglong2* src =
                 reinterpret_cast<const ulonglong2*>(acci + (col - 27) * 32 + lane0);
-            unsigned long long tot = 0;
+            // Each lane entry packs count | flags << 11 | sum_x << 22 |
+            // sum_y << 43 of at most 2047 pixels (cell_path_ok).  Up to
+            // S = 45 a cell has <= 2047 pixels, so the packed entries of its
+            // lanes add without carries between fields; larger cells unpack.
+            unsigned long long cnt = 0, flg = 0, sxr = 0, syr = 0;
+            if (S <= 45) {
+              unsigned long long tot = 0;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-              const ulonglong2 v = src[(q + ll) & (NQ - 1)];
-              tot += v.x + v.y;  // fields cannot overflow (see packing above)
+              for (int q = 0; q < NQ; ++q) {
+                const ulonglong2 v = src[(q + ll) & (NQ - 1)];
+                tot += v.x + v.y;
+              }
+              cnt = tot & 2047ull;
+              flg = (tot >> 11) & 2047ull;
+              sxr = (tot >> 22) & 0x1FFFFFull;
+              syr = tot >> 43;
+            } else {
+#pragma unroll
+              for (int q = 0; q < NQ; ++q) {
+                const ulonglong2 v = src[(q + ll) & (NQ - 1)];
+                cnt += (v.x & 2047ull) + (v.y & 2047ull);
+                flg += ((v.x >> 11) & 2047ull) + ((v.y >> 11) & 2047ull);
+                sxr += ((v.x >> 22) & 0x1FFFFFull) + ((v.y >> 22) & 0x1FFFFFull);
+                syr += (v.x >> 43) + (v.y >> 43);
+              }
             }
-            const unsigned long long cnt = tot & 2047ull;
             if (cnt) {
               ClusterAcc* o = fa + cand_k[col - 27];
-              const unsigned long long flg = (tot >> 11) & 2047ull;
-              atomicAdd(&o->sx, ((tot >> 22) & 0x1FFFFFull) + cnt * (unsigned long long)x_cell);
-              atomicAdd(&o->sy, (tot >> 43) + cnt * (unsigned long long)y_glob0);
+              atomicAdd(&o->sx, sxr + cnt * (unsigned long long)x_cell);
+              atomicAdd(&o->sy, syr + cnt * (unsigned long long)y_glob0);
               const unsigned long long add = cnt | (flg << 32);
               if (p.wl && flg) {
                 // the contribution that turns the cluster's flag count
@@ -476,6 +496,8 @@ struct ReduceParams {
   int32_t* wl_reset;       // (may be null) zeroed by k_reduce_cells: the next pass's count
   bool append;             // k_reduce_cells enqueues flagged clusters (else k_cell did)
   int h, w, s, ns_r, ns_c, frames, n_bl, tile_len;
+  long long plane;         // planar Lab channel stride (plane_of(h * w))
+  bool win_staged;         // k_exact_clusters stages the label window in smem
   int kr0, kr1;            // cluster rows reduced (local grid)
   int row_off;             // global cell row of local row 0
 };
@@ -642,8 +664,15 @@ __global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
 constexpr int kExWarps = SPX_EXW;  // 3 = n_bl for the default tile_len 16 (3S / 16 strips when S = 16)
 constexpr int kExCap = 256;        // compacted members per warp and fold round
 
-size_t exact_smem_bytes(int64_t s) {  // compact values + the window's labels
-  return (size_t)kExWarps * 3 * kExCap * sizeof(float) + (size_t)9 * s * s * sizeof(int32_t);
+constexpr int kExMaxStrips = 64;   // n_bl <= 64 (cell_path_ok)
+// The 3S x 3S window of labels is staged in shared memory up to this size;
+// larger windows (S > 48) are read from global memory (L2) in place.
+constexpr size_t kExWinSmemMax = 88 * 1024;
+size_t exact_win_bytes(int64_t s) { return (size_t)9 * s * s * sizeof(int32_t); }
+bool exact_win_staged(int64_t s) { return exact_win_bytes(s) <= kExWinSmemMax; }
+size_t exact_smem_bytes(int64_t s) {  // compact values + the window's labels (staged)
+  return (size_t)kExWarps * 3 * kExCap * sizeof(float) +
+         (exact_win_staged(s) ? exact_win_bytes(s) : 0);
 }
 
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
@@ -660,10 +689,11 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p) {
   extern __shared__ __align__(16) unsigned char ex_smem[];
-  __shared__ double strips[32][6];
+  __shared__ double strips[kExMaxStrips][6];
   __shared__ double qv[6];
   float* const cv_all = reinterpret_cast<float*>(ex_smem);  // [kExWarps][3][kExCap]
-  int32_t* const win = reinterpret_cast<int32_t*>(cv_all + kExWarps * 3 * kExCap);
+  int32_t* const win_s = reinterpret_cast<int32_t*>(cv_all + kExWarps * 3 * kExCap);
+  const bool staged = p.win_staged;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* const cw = cv_all + warp * 3 * kExCap;
   const int K = p.ns_r * p.ns_c;
@@ -679,7 +709,7 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
     // a frame that stopped early has no update this pass (k_cell enqueued its
     // clusters during its final association)
     if (p.done && p.done[ff]) continue;  // block-uniform
-    const float* im = p.img + (long long)ff * 3 * hw;  // planar [3][H][W]
+    const float* im = p.img + (long long)ff * 3 * p.plane;  // planar [3][plane]
     const int32_t* lb = p.labels + (long long)ff * hw;
     const int r = fk / p.ns_c, c = fk - r * p.ns_c;
     const int gid = fk + p.row_off * p.ns_c;  // labels carry global ids
@@ -687,19 +717,23 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
     const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
     const int ya0 = max(ry0, 0);
     const int ww = wx1 - wx0, wrows = ry1 - ya0;
+    // the window's labels: staged (row stride ww) or in place (row stride w)
+    const int32_t* const win = staged ? win_s : lb + (long long)ya0 * p.w + wx0;
+    const int wst = staged ? ww : p.w;
     // (2) the window's labels, one round trip
-    if (((wx0 | ww | p.w) & 3) == 0) {
+    if (!staged) {
+    } else if (((wx0 | ww | p.w) & 3) == 0) {
       const int q4 = ww >> 2;
 #pragma unroll 1
       for (int i = threadIdx.x; i < wrows * q4; i += blockDim.x) {
         const int rr = i / q4, cq = i - rr * q4;
-        cp_async16(win + rr * ww + 4 * cq, lb + (long long)(ya0 + rr) * p.w + wx0 + 4 * cq);
+        cp_async16(win_s + rr * ww + 4 * cq, lb + (long long)(ya0 + rr) * p.w + wx0 + 4 * cq);
       }
     } else {
 #pragma unroll 1
       for (int i = threadIdx.x; i < wrows * ww; i += blockDim.x) {
         const int rr = i / ww, cc = i - rr * ww;
-        cp_async4(win + i, lb + (long long)(ya0 + rr) * p.w + wx0 + cc);
+        cp_async4(win_s + i, lb + (long long)(ya0 + rr) * p.w + wx0 + cc);
       }
     }
 #pragma unroll 1
@@ -723,28 +757,41 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
         const bool own = row < rc;
         const int c0 = own ? min(sg * seg, ww) : 0, c1 = own ? min(c0 + seg, ww) : 0;
         const int y = yc + row;
-        const int32_t* wrow = win + (y - ya0) * ww;
-        // members of this lane's segment as a bit mask (segments <= 96 columns)
-        // (each row starts its walk at a different column: with the window's
-        // 16 (mod 32)-word row stride, lanes of different rows would
-        // otherwise hit the same shared-memory banks)
-        unsigned m0 = 0, m1 = 0, m2 = 0, sx = 0;
+        const int32_t* wrow = win + (long long)(y - ya0) * wst;
+        // Members of this lane's segment as bit masks of <= 96 columns; a
+        // longer segment (S > 32) is walked in sub-chunks of 96 columns,
+        // re-scanned when its members are copied.  Each row starts its walk
+        // at a different column: with the staged window's 16 (mod 32)-word
+        // row stride, lanes of different rows would otherwise hit the same
+        // shared-memory banks.
         const int len = c1 - c0;
-        const int rot = len ? row % len : 0;
-        auto scan = [&](int k0, int k1) {
+        const int nsub = (len + 95) / 96;
+        auto scan = [&](int a0, int a1, unsigned& m0, unsigned& m1, unsigned& m2) -> unsigned {
+          m0 = m1 = m2 = 0;
+          unsigned sxx = 0;
+          const int sl = a1 - a0;
+          const int rot = sl ? row % sl : 0;
+          auto part = [&](int k0, int k1) {
 #pragma unroll 4
-          for (int k = k0; k < k1; ++k) {
-            const bool hit = wrow[c0 + k] == gid;
-            sx += hit ? (unsigned)(wx0 + c0 + k) : 0u;
-            if (k < 32) m0 |= (unsigned)hit << k;
-            else if (k < 64) m1 |= (unsigned)hit << (k - 32);
-            else m2 |= (unsigned)hit << (k - 64);
-          }
+            for (int k = k0; k < k1; ++k) {
+              const bool hit = wrow[a0 + k] == gid;
+              sxx += hit ? (unsigned)(wx0 + a0 + k) : 0u;
+              if (k < 32) m0 |= (unsigned)hit << k;
+              else if (k < 64) m1 |= (unsigned)hit << (k - 32);
+              else m2 |= (unsigned)hit << (k - 64);
+            }
+          };
+          part(rot, sl);
+          part(0, rot);
+          return sxx;
         };
-        scan(rot, len);
-        scan(0, rot);
-        const int cnt = __popc(m0) + __popc(m1) + __popc(m2);
-        lx += sx;
+        unsigned m0 = 0, m1 = 0, m2 = 0;
+        int cnt = 0;
+        for (int sb = 0; sb < nsub; ++sb) {
+          const int a0 = c0 + 96 * sb, a1 = min(a0 + 96, c1);
+          lx += scan(a0, a1, m0, m1, m2);
+          cnt += __popc(m0) + __popc(m1) + __popc(m2);
+        }
         lc += (unsigned)cnt;
         ly += (unsigned long long)cnt * (unsigned long long)(y + p.row_off * p.s);
         // exclusive scan of the counts in lane (= row-major) order
@@ -760,20 +807,24 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
         for (int base = 0; base < total; base += kExCap) {
           if (cnt && off < base + kExCap && off + cnt > base) {
             int o = off;
-            const float* g0 = im + (long long)y * p.w + wx0 + c0;
+            for (int sb = 0; sb < nsub && o < base + kExCap; ++sb) {
+              const int a0 = c0 + 96 * sb, a1 = min(a0 + 96, c1);
+              if (nsub > 1) scan(a0, a1, m0, m1, m2);  // one sub-chunk: masks kept
+              const float* g0 = im + (long long)y * p.w + wx0 + a0;
 #pragma unroll
-            for (int wd = 0; wd < 3; ++wd) {
-              unsigned mw = wd == 0 ? m0 : (wd == 1 ? m1 : m2);
+              for (int wd = 0; wd < 3; ++wd) {
+                unsigned mw = wd == 0 ? m0 : (wd == 1 ? m1 : m2);
 #pragma unroll 1
-              while (mw) {
-                const int k = 32 * wd + __ffs(mw) - 1;
-                mw &= mw - 1;
-                if (o >= base && o < base + kExCap) {
-                  cp_async4(cw + (o - base), g0 + k);
-                  cp_async4(cw + kExCap + (o - base), g0 + hw + k);
-                  cp_async4(cw + 2 * kExCap + (o - base), g0 + 2 * hw + k);
+                while (mw) {
+                  const int k = 32 * wd + __ffs(mw) - 1;
+                  mw &= mw - 1;
+                  if (o >= base && o < base + kExCap) {
+                    cp_async4(cw + (o - base), g0 + k);
+                    cp_async4(cw + kExCap + (o - base), g0 + p.plane + k);
+                    cp_async4(cw + 2 * kExCap + (o - base), g0 + 2 * p.plane + k);
+                  }
+                  ++o;
                 }
-                ++o;
               }
             }
           }
@@ -858,12 +909,13 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
 
 // ---- launchers ----------------------------------------------------------------
 
-// Any S in [4, 32] (runs of 4 pixels, the last one of a cell row partial
-// when S % 4 != 0); frames with h*w % 4 == 0 (the planar convert's 4-pixel
-// groups never straddle frames); n_bl <= 32 strips for the exact fallback.
+// Any S in [4, 255] (runs of 4 pixels, the last one of a cell row partial
+// when S % 4 != 0; a lane walks at most ceil(S/4) * S / 32 runs, i.e. <= 2047
+// pixels, the width of the packed per-lane count) and any frame size (planar
+// planes padded to a multiple of 4); n_bl <= 64 strips for the exact fallback.
 bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
   int64_t n_bl = ceil_div(3 * s, tile_len);
-  return s >= 4 && s <= 32 && (h * w) % 4 == 0 && n_bl <= 32 &&
+  return s >= 4 && s <= kCellMaxS && n_bl <= kExMaxStrips &&
          h * w * 3 < (int64_t)1 << 40 && h < (1 << 30) && w < (1 << 30);
 }
 
@@ -880,8 +932,9 @@ bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
 // cells (batch 16: LPC 16 is 5% slower).
 static int cell_lpc(int64_t s, long long cells) {
   static const int env = getenv("SPX_LPC") ? atoi(getenv("SPX_LPC")) : 0;  // development
-  if (env == 4 || env == 8 || env == 16 || env == 32) return env;
-  int lpc = s <= 12 ? 4 : (s <= 24 ? 8 : 16);
+  if (s <= 64 && (env == 4 || env == 8 || env == 16 || env == 32)) return env;
+  // S > 64: 32 lanes per cell (the per-lane pixel count must stay <= 2047)
+  int lpc = s <= 12 ? 4 : (s <= 24 ? 8 : (s <= 64 ? 16 : 32));
   const long long runs = s * ceil_div(s, 4);
   // up to two doublings (a single 640x480 frame: 8 -> 32 lanes per cell)
   for (int d = 0; d < 2; ++d)
@@ -939,13 +992,16 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.ns_r = (int)ns_r;
   p.ns_c = (int)ns_c;
   p.frames = frames;
+  p.plane = plane_of(h * w);
   if (cr1 < 0) cr1 = ns_r;
   p.cr0 = (int)cr0;
   p.cr1 = (int)cr1;
   p.row_off = (int)row_off;
   p.runs_per_row = (int)ceil_div(s, 4);
   p.runs = (int)(s * p.runs_per_row);
-  p.row_magic = (unsigned)((65536 + p.runs_per_row - 1) / p.runs_per_row);
+  p.row_magic = p.runs_per_row == 1
+                    ? 0u
+                    : (unsigned)(((1ull << 32) + p.runs_per_row - 1) / p.runs_per_row);
   p.xy_weight = xy_weight;
   assoc_bound_coefficients(xy_weight, p.w32, p.k_mp, p.k_mc, p.k_xy, p.k_const, p.k_rel);
   if (cr1 <= cr0) return SPX_OK;
@@ -1012,6 +1068,8 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   p.ns_r = (int)ns_r;
   p.ns_c = (int)ns_c;
   p.frames = frames;
+  p.plane = plane_of(h * w);
+  p.win_staged = exact_win_staged(s);
   p.n_bl = (int)ceil_div(3 * s, tile_len);
   p.tile_len = (int)tile_len;
   if (kr1 < 0) kr1 = ns_r;
@@ -1034,7 +1092,19 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   // launches get a small grid (an empty block still costs its scheduling)
   const long long ex_blocks = std::max<long long>(
       num_sms(), std::min<long long>((long long)num_sms() * SPX_EXG, nk * frames / 64));
-  k_exact_clusters<<<(unsigned)ex_blocks, kExWarps * 32, exact_smem_bytes(s), st>>>(p);
+  const size_t ex_smem = exact_smem_bytes(s);
+  {  // dynamic + static shared memory may exceed the default 48 KB
+    static std::atomic<uint64_t> configured{0};  // per device
+    int dev = 0;
+    SPX_CUDA(cudaGetDevice(&dev));
+    if (!(configured.load() & (1ull << (dev & 63)))) {
+      SPX_CUDA(cudaFuncSetAttribute(k_exact_clusters, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(kExWarps * 3 * kExCap * sizeof(float) +
+                                          kExWinSmemMax)));
+      configured.fetch_or(1ull << (dev & 63));
+    }
+  }
+  k_exact_clusters<<<(unsigned)ex_blocks, kExWarps * 32, ex_smem, st>>>(p);
   SPX_LAUNCH_CHECK("k_exact_clusters");
   return SPX_OK;
 }

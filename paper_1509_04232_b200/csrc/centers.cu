@@ -63,7 +63,8 @@ __global__ void k_init(const float* __restrict__ img, int64_t h, int64_t w, int6
   if (i >= nk * frames) return;
   int64_t f = i / nk;
   int64_t k = k0 + i % nk;
-  LabView im{img + f * hl * w * 3, w, hl * w, planar != 0};
+  const int64_t pst = planar ? plane_of(hl * w) : hl * w;
+  LabView im{img + f * pst * 3, w, pst, planar != 0};
   im.yoff = row_off * s;
   double* xy = cxy + (f * k_stride + k) * 2;
   double* lab = clab + (f * k_stride + k) * 3;

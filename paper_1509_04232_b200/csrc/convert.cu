@@ -209,8 +209,8 @@ __device__ __forceinline__ void convert_px(const double* lut, const Factors& fc,
 
 // Pixels [p0, p1) of a flat HWC raster (frames of a batch are contiguous, so
 // a batch is one range).  `vec` requires rgb 4-byte and out 16-byte aligned.
-// PLANAR: out is [frames][3][hw] (the engine's internal layout) instead of
-// HWC; requires hw % 4 == 0 so a 4-pixel group never straddles frames.
+// PLANAR: out is [frames][3][plane_of(hw)] (the engine's internal layout)
+// instead of HWC.
 // Certified-sum flag of one output pixel (cell.cu): some channel is nonzero
 // with |v| < tau, or |v| >= 128 / non-finite.
 __device__ __forceinline__ bool sum_flag(float v, float tau) {
@@ -248,19 +248,25 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
     for (int i = threadIdx.x; i < 9 * 256; i += blockDim.x) lut[i] = g_mlut[i];
     __syncthreads();
   }
-  int64_t g0 = p0 >> 2, g1 = (p1 + 3) >> 2;
+  // HWC: groups of 4 consecutive pixels of the flat range [p0, p1).
+  // PLANAR (p0 = 0, p1 = frames * hw): groups of 4 pixels of ONE frame --
+  // ceil(hw / 4) per frame, the last one partial when hw % 4 != 0 -- written
+  // to the frame's planes of stride plane_of(hw); (frame, group) advance
+  // incrementally (no 64-bit division in the loop).
+  const int64_t gpf = PLANAR ? (hw + 3) >> 2 : 0, pst = PLANAR ? plane_of(hw) : 0;
+  int64_t g0 = PLANAR ? 0 : p0 >> 2, g1 = PLANAR ? (p1 / hw) * gpf : (p1 + 3) >> 2;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t g = g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  // PLANAR: frame index / offset of pixel q = 4g, advanced incrementally (no
-  // 64-bit division in the loop)
-  int64_t pf = 0, pr = 0;
+  int64_t pf = 0, pr = 0;  // PLANAR: frame, first pixel of the group in the frame
   if (PLANAR) {
-    pf = (g << 2) / hw;
-    pr = (g << 2) - pf * hw;
+    pf = g / gpf;
+    pr = (g - pf * gpf) << 2;
   }
   for (; g < g1; g += stride) {
-    int64_t q = g << 2;
-    if (vec && q >= p0 && q + 4 <= p1) {
+    // source pixel index (HWC, flat) of the group's first pixel, and its end
+    const int64_t q = PLANAR ? pf * hw + pr : g << 2;
+    const int64_t qe = PLANAR ? pf * hw + hw : p1;
+    if (vec && q >= p0 && q + 4 <= qe && (!PLANAR || ((q * 3) & 3) == 0)) {
       const uint32_t* src = reinterpret_cast<const uint32_t*>(rgb + q * 3);
       uint32_t w0 = __ldg(src), w1 = __ldg(src + 1), w2 = __ldg(src + 2);
       uint8_t c[12];
@@ -276,12 +282,12 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
         convert_px<SPACE>(lut, fc, c[3 * i], c[3 * i + 1], c[3 * i + 2], o[3 * i], o[3 * i + 1],
                           o[3 * i + 2]);
       if (PLANAR) {
-        float* base = out + pf * 3 * hw + pr;
+        float* base = out + pf * 3 * pst + pr;
         *reinterpret_cast<float4*>(base) =
             make_float4(with_flag(o[0], o[1], o[2], tau), with_flag(o[3], o[4], o[5], tau),
                         with_flag(o[6], o[7], o[8], tau), with_flag(o[9], o[10], o[11], tau));
-        *reinterpret_cast<float4*>(base + hw) = make_float4(o[1], o[4], o[7], o[10]);
-        *reinterpret_cast<float4*>(base + 2 * hw) = make_float4(o[2], o[5], o[8], o[11]);
+        *reinterpret_cast<float4*>(base + pst) = make_float4(o[1], o[4], o[7], o[10]);
+        *reinterpret_cast<float4*>(base + 2 * pst) = make_float4(o[2], o[5], o[8], o[11]);
       } else {
         float4* dst = reinterpret_cast<float4*>(out + q * 3);
         dst[0] = make_float4(o[0], o[1], o[2], o[3]);
@@ -290,14 +296,14 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
       }
     } else {
       for (int64_t p = q; p < q + 4; ++p) {
-        if (p < p0 || p >= p1) continue;
+        if (p < p0 || p >= qe) continue;
         float o0, o1, o2;
         convert_px<SPACE>(lut, fc, rgb[p * 3], rgb[p * 3 + 1], rgb[p * 3 + 2], o0, o1, o2);
         if (PLANAR) {
-          const int64_t f = p / hw, r = p - f * hw;
-          out[f * 3 * hw + r] = with_flag(o0, o1, o2, tau);
-          out[f * 3 * hw + hw + r] = o1;
-          out[f * 3 * hw + 2 * hw + r] = o2;
+          float* base = out + pf * 3 * pst + pr + (p - q);
+          base[0] = with_flag(o0, o1, o2, tau);
+          base[pst] = o1;
+          base[2 * pst] = o2;
         } else {
           out[p * 3] = o0;
           out[p * 3 + 1] = o1;
@@ -307,8 +313,8 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
     }
     if (PLANAR) {
       pr += stride << 2;
-      while (pr >= hw) {
-        pr -= hw;
+      while (pr >= gpf << 2) {
+        pr -= gpf << 2;
         ++pf;
       }
     }
@@ -325,11 +331,13 @@ int launch_convert(const uint8_t* rgb, float* out, int64_t p0, int64_t p1, int s
   if (rc) return rc;
   int vec = ((uintptr_t)rgb % 4 == 0) && ((uintptr_t)out % 16 == 0);
   const bool planar = planar_hw > 0;
-  if (planar && (planar_hw % 4 != 0 || !vec)) {
-    set_error("planar convert needs h*w %% 4 == 0 and aligned buffers");
+  if (planar && (p0 != 0 || p1 % planar_hw != 0 || (uintptr_t)out % 16 != 0)) {
+    set_error("planar convert needs whole frames and a 16-byte aligned output");
     return SPX_ERR_VALUE;
   }
-  int64_t groups = ((p1 + 3) >> 2) - (p0 >> 2);
+  if (planar) vec = (uintptr_t)rgb % 4 == 0;
+  int64_t groups = planar ? (p1 / planar_hw) * ((planar_hw + 3) >> 2)
+                          : ((p1 + 3) >> 2) - (p0 >> 2);
   int64_t blocks = ceil_div(groups, 256);
   int64_t cap = (int64_t)num_sms() * SPX_CONV_BPS;
   if (blocks > cap) blocks = cap;

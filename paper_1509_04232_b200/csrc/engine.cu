@@ -251,7 +251,7 @@ struct Engine {
     hw = st.width * st.height;
     xy_weight = st.compactness / (double)st.s;  // engine.py:143
     size_t B = (size_t)mb;
-    SPX_CUDA(cudaMalloc(&lab, B * hw * 3 * sizeof(float)));
+    SPX_CUDA(cudaMalloc(&lab, B * plane_of(hw) * 3 * sizeof(float)));
     SPX_CUDA(cudaMalloc(&labels, B * hw * sizeof(int32_t)));
     SPX_CUDA(cudaMalloc(&scratch, B * hw * sizeof(int32_t)));
     for (int i = 0; i < 2; ++i) {
@@ -992,5 +992,7 @@ int32_t spx_engine_set_lanes(spx_engine* eng, int32_t lanes) { return eng->e.set
 int32_t spx_engine_last_lanes(spx_engine* eng) { return eng->e.last_lanes; }
 
 int64_t spx_engine_last_launches(spx_engine* eng) { return eng->e.launches; }
+
+int32_t spx_engine_fused_path(spx_engine* eng) { return eng->e.use_cell ? 1 : 0; }
 
 }  // extern "C"

@@ -100,7 +100,7 @@ struct Strip {
     n_bl = ceil_div(3 * g.s, g.tile_len);
     xy_weight = g.compactness / (double)g.s;
     const int64_t hw = hl * g.width;
-    SPX_CUDA(cudaMalloc(&lab, hw * 3 * sizeof(float)));
+    SPX_CUDA(cudaMalloc(&lab, plane_of(hw) * 3 * sizeof(float)));
     SPX_CUDA(cudaMalloc(&labels, hw * sizeof(int32_t)));
     SPX_CUDA(cudaMalloc(&out, hw * sizeof(int32_t)));
     SPX_CUDA(cudaMemset(labels, 0xff, hw * sizeof(int32_t)));
@@ -295,8 +295,8 @@ int32_t spx_strip_create(const spx_settings* st, int64_t row_lo, int64_t row_hi,
     set_error("strip rows [%lld, %lld) outside the grid", (long long)row_lo, (long long)row_hi);
     return SPX_ERR_INVALID_SETTINGS;
   }
-  if (!cell_path_ok(st->height, st->width, st->s, st->tile_len) || st->width % 4 != 0) {
-    set_error("row strips need the fused cell path (W %% 4 == 0, 4 <= S <= 32)");
+  if (!cell_path_ok(st->height, st->width, st->s, st->tile_len)) {
+    set_error("row strips need the fused cell path (4 <= S <= 255, ceil(3S / tile_len) <= 64)");
     return SPX_ERR_INVALID_SETTINGS;
   }
   if (st->early_stop >= 0.0) {

@@ -287,6 +287,11 @@ class SegEngine:
     def last_launches(self):
         return int(self._lib.spx_engine_last_launches(self._h))
 
+    @property
+    def fused_path(self):
+        """True when the engine runs the fused cell kernels (4 <= S <= 255)."""
+        return bool(self._lib.spx_engine_fused_path(self._h))
+
     # ---- reference API ---------------------------------------------------------------
 
     def _check_frame(self, img):

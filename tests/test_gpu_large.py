@@ -97,6 +97,8 @@ TABLE1 = ["1024x1024", "3631x3859", "963x1024", "1002x1002", "933x800"]
 @pytest.mark.parametrize("size", TABLE1)
 def test_paper_table1_sizes(golden_meta, size, k):
     m = golden_meta["hashes"][f"large_T1_{size}_k{k}"]
-    res = spx.SegEngine(settings(m)).perform_segmentation(spx.ImageRGB(frame(m)))
+    eng = spx.SegEngine(settings(m))
+    assert eng.fused_path  # every Table-1 shape (S = 19 ... 118) runs the fused kernels
+    res = eng.perform_segmentation(spx.ImageRGB(frame(m)))
     assert_matches(m, res.labels.data, res.spixel_map.centers_xy, res.spixel_map.centers_lab,
                    res.spixel_map.num_pixels, f"{size} K={k}")

@@ -211,6 +211,50 @@ def test_cell_path_grid_sizes_bitexact(s, odd_w):
             assert np.array_equal(res.spixel_map.num_pixels, counts), (s, name, tile)
 
 
+@pytest.mark.parametrize("s,h,w", [
+    (16, 99, 123),    # h*w odd: padded planar planes, partial last convert group
+    (5, 37, 51), (8, 41, 66), (12, 50, 77),
+    (33, 104, 137), (40, 125, 161), (47, 140, 201), (64, 197, 261),   # LPC 16, S > 32
+    (84, 253, 339), (118, 300, 355), (160, 330, 480),                  # LPC 32, global window
+])
+def test_cell_path_large_cells_and_odd_frames(s, h, w):
+    # S > 32 (per-lane field unpacking, sub-chunked exact-fallback segments,
+    # the label window read in place when 9 S^2 labels exceed the smem
+    # budget) and frames with h*w % 4 != 0 run the fused cell kernels and
+    # equal the oracle bit for bit.
+    for name, rgb in _images(h, w, s + 1).items():
+        for tile in (16, 9):
+            st = spx.Settings(img_width=w, img_height=h, spixel_size=s, tile_len=tile, no_iters=3)
+            eng = spx.SegEngine(st)
+            assert eng.fused_path, (s, h, w, tile)
+            res = eng.perform_segmentation(spx.ImageRGB(rgb))
+            labels, cxy, clab, counts, _ = _oracle_pipeline(rgb, st)
+            assert np.array_equal(res.labels.data, labels), (s, name, tile)
+            assert res.spixel_map.centers_xy.tobytes() == cxy.tobytes(), (s, name, tile)
+            assert res.spixel_map.centers_lab.tobytes() == clab.tobytes(), (s, name, tile)
+            assert np.array_equal(res.spixel_map.num_pixels, counts), (s, name, tile)
+
+
+def test_odd_frame_batches_and_strips():
+    # a batch of frames with h*w odd (frame f's pixels start at an unaligned
+    # RGB offset for odd f) and a row-strip split of such a frame
+    from paper_1509_04232_b200.strips import segment_strips_local
+    h, w = 75, 93
+    st = spx.Settings(img_width=w, img_height=h, spixel_size=9, no_iters=4)
+    frames = [_images(h, w, 70 + i)["noise"] for i in range(5)]
+    eng = spx.SegEngine(st, max_batch=5)
+    labels, cxy, clab, counts, _ = eng.segment_host(np.stack(frames))
+    for i, rgb in enumerate(frames):
+        ol, ox, oc, on, _ = _oracle_pipeline(rgb, st)
+        assert np.array_equal(labels[i], ol), i
+        assert cxy[i].tobytes() == ox.tobytes() and clab[i].tobytes() == oc.tobytes(), i
+        assert np.array_equal(counts[i], on), i
+    sl, sx, sc, sn = segment_strips_local(st, frames[1], 3)
+    ol, ox, oc, on, _ = _oracle_pipeline(frames[1], st)
+    assert np.array_equal(sl, ol) and sx.tobytes() == ox.tobytes()
+    assert sc.tobytes() == oc.tobytes() and np.array_equal(sn, on)
+
+
 @pytest.mark.parametrize("s,odd_w", [(6, False), (8, False), (12, False), (16, False),
                                      (20, False), (24, False), (10, True), (18, True)])
 def test_cell_path_wide_launch_bitexact(s, odd_w):
