@@ -687,6 +687,39 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// Warp 0 of an exact-fallback block, after the strips' sums are in
+// strips[0..n_bl): lane t < 6 runs the pairwise strip tree of component t
+// (_core.pyx:300-311), lanes 0..4 divide one component each
+// (_core.pyx:313-320), lane 0 stores.
+__device__ __forceinline__ void finish_cluster(const ReduceParams& p, double (*strips)[6],
+                                               double* qv, int gk, int r, int c, int lane) {
+  if (lane < 6) {
+    int m = p.n_bl;
+#pragma unroll 1
+    while (m > 1) {
+      const int half = m >> 1;
+#pragma unroll 1
+      for (int i = 0; i < half; ++i)
+        strips[i][lane] = dadd(strips[2 * i][lane], strips[2 * i + 1][lane]);
+      if (m & 1) strips[half][lane] = strips[m - 1][lane];
+      m = half + (m & 1);
+    }
+  }
+  __syncwarp();
+  const double cnt = strips[0][5];
+  if (lane < 5) {
+    double q;
+    if (cnt > 0.0) {
+      q = ddiv(strips[0][lane], cnt);
+    } else {  // empty: keep the previous centre
+      q = lane < 3 ? p.prev_lab[3LL * gk + lane] : p.prev_xy[2LL * gk + (lane - 3)];
+    }
+    qv[lane] = q;
+  }
+  __syncwarp();
+  if (lane == 0) write_centre(p, gk, r, c, cnt, qv);
+}
+
 __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p) {
   extern __shared__ __align__(16) unsigned char ex_smem[];
   __shared__ double strips[kExMaxStrips][6];
@@ -871,38 +904,120 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
       }
     }
     __syncthreads();
-    // (4) warp 0: lane t < 6 runs the pairwise strip tree of component t,
-    // lanes 0..4 divide, lane 0 stores
-    if (warp == 0) {
-      if (lane < 6) {
-        int m = p.n_bl;
-#pragma unroll 1
-        while (m > 1) {  // pairwise strip tree, _core.pyx:300-311
-          const int half = m >> 1;
-#pragma unroll 1
-          for (int i = 0; i < half; ++i)
-            strips[i][lane] = dadd(strips[2 * i][lane], strips[2 * i + 1][lane]);
-          if (m & 1) strips[half][lane] = strips[m - 1][lane];
-          m = half + (m & 1);
-        }
-      }
-      __syncwarp();
-      const double cnt = strips[0][5];
-      if (lane < 5) {
-        double q;
-        if (cnt > 0.0) {
-          q = ddiv(strips[0][lane], cnt);
-        } else {  // empty: keep the previous centre
-          q = lane < 3 ? p.prev_lab[3LL * gk + lane] : p.prev_xy[2LL * gk + (lane - 3)];
-        }
-        qv[lane] = q;
-      }
-      __syncwarp();
-      if (lane == 0) write_centre(p, gk, r, c, cnt, qv);
-    }
+    // (4) warp 0: strip tree, divisions, store
+    if (warp == 0) finish_cluster(p, strips, qv, gk, r, c, lane);
     __syncthreads();  // the window and strips are reused by the next item
   }
 }
+
+// Exact recomputation for large cells (S > 32), where most clusters are
+// flagged (the certified range 2^k <= |v| < 128 narrows as 9 S^2 grows) and
+// a strip holds thousands of members.  One block of kWideWarps warps per
+// cluster, warp w folding strips w, w + kWideWarps, ...; a strip is walked
+// in row-major units of (row, 256 columns): the unit's labels and Lab
+// values are loaded coalesced (8 per lane, the next unit's loads in flight
+// while this one is folded), members found by ballot, and lanes 0..2 fold
+// channel 0..2 of each member in order, the values arriving by shuffle.
+constexpr int kWideWarps = 8;
+__global__ void __launch_bounds__(kWideWarps * 32) k_exact_wide(ReduceParams p) {
+  __shared__ double strips[kExMaxStrips][6];
+  __shared__ double qv[6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = p.ns_r * p.ns_c;
+  const long long hw = (long long)p.h * p.w;
+  const int n = *p.worklist_n;
+  for (int item = blockIdx.x; item < n; item += gridDim.x) {
+    const int gk = p.worklist[item];
+    const int ff = gk / K, fk = gk - ff * K;
+    if (p.done && p.done[ff]) continue;  // block-uniform
+    const float* im = p.img + (long long)ff * 3 * p.plane;
+    const int32_t* lb = p.labels + (long long)ff * hw;
+    const int r = fk / p.ns_c, c = fk - r * p.ns_c;
+    const int gid = fk + p.row_off * p.ns_c;
+    const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
+    const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
+    const int nseg = (wx1 - wx0 + 255) >> 8;
+#pragma unroll 1
+    for (int i = threadIdx.x; i < p.n_bl * 6; i += blockDim.x) (&strips[0][0])[i] = 0.0;
+    __syncthreads();
+#pragma unroll 1
+    for (int j = warp; j < p.n_bl; j += kWideWarps) {
+      const int ya = max(ry0 + j * p.tile_len, 0);
+      const int yz = min(ry0 + (j + 1) * p.tile_len, ry1);
+      if (ya >= yz) continue;  // warp-uniform
+      const int units = (yz - ya) * nseg;
+      double acc = 0.0;
+      unsigned long long lx = 0, ly = 0, lc = 0;
+      int lb_n[8];
+      float l_n[8], a_n[8], b_n[8];
+      auto load = [&](int u) {
+        const int y = ya + u / nseg, x0 = wx0 + (u % nseg) * 256 + lane;
+        const long long row = (long long)y * p.w;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          const int x = x0 + 32 * ch;
+          const bool v = x < wx1;
+          lb_n[ch] = v ? __ldg(lb + row + x) : -1;
+          l_n[ch] = v ? __ldg(im + row + x) : 0.f;
+          a_n[ch] = v ? __ldg(im + p.plane + row + x) : 0.f;
+          b_n[ch] = v ? __ldg(im + 2 * p.plane + row + x) : 0.f;
+        }
+      };
+      load(0);
+#pragma unroll 1
+      for (int u = 0; u < units; ++u) {
+        int lbv[8];
+        float lv[8], av[8], bv[8];
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          lbv[ch] = lb_n[ch];
+          lv[ch] = l_n[ch];
+          av[ch] = a_n[ch];
+          bv[ch] = b_n[ch];
+        }
+        if (u + 1 < units) load(u + 1);
+        const int y = ya + u / nseg, x0 = wx0 + (u % nseg) * 256 + lane;
+        const unsigned long long yg = (unsigned long long)(y + p.row_off * p.s);
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          const bool hit = lbv[ch] == gid;
+          unsigned m = __ballot_sync(0xFFFFFFFFu, hit);
+          if (hit) {
+            lx += (unsigned long long)(x0 + 32 * ch);
+            ly += yg;
+            ++lc;
+          }
+          while (m) {  // warp-uniform: members in column order
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            const float v0 = __shfl_sync(0xFFFFFFFFu, lv[ch], b);
+            const float v1 = __shfl_sync(0xFFFFFFFFu, av[ch], b);
+            const float v2 = __shfl_sync(0xFFFFFFFFu, bv[ch], b);
+            // channel 0 carries the certified-sum flag in its sign bit
+            const float v = lane == 0 ? fabsf(v0) : (lane == 1 ? v1 : v2);
+            if (lane < 3) acc = dadd(acc, (double)v);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        lx += __shfl_xor_sync(0xFFFFFFFFu, lx, o);
+        ly += __shfl_xor_sync(0xFFFFFFFFu, ly, o);
+        lc += __shfl_xor_sync(0xFFFFFFFFu, lc, o);
+      }
+      if (lane < 3) strips[j][lane] = acc;
+      if (lane == 0) {
+        strips[j][3] = (double)lx;
+        strips[j][4] = (double)ly;
+        strips[j][5] = (double)lc;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) finish_cluster(p, strips, qv, gk, r, c, lane);
+    __syncthreads();  // strips are reused by the next item
+  }
+}
+
 
 
 }  // namespace
@@ -1088,6 +1203,14 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
     SPX_LAUNCH_CHECK("k_reduce_cells");
   }
   if (mode == kReduceOnly) return SPX_OK;
+  if (s > 32) {
+    // large cells: most clusters are flagged, one block per cluster
+    const long long wb = std::max<long long>(
+        1, std::min<long long>((long long)num_sms() * 8, nk * frames));
+    k_exact_wide<<<(unsigned)wb, kWideWarps * 32, 0, st>>>(p);
+    SPX_LAUNCH_CHECK("k_exact_wide");
+    return SPX_OK;
+  }
   // grid-stride over the worklist; ~0.5% of clusters are flagged, so small
   // launches get a small grid (an empty block still costs its scheduling)
   const long long ex_blocks = std::max<long long>(
