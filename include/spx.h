@@ -116,6 +116,10 @@ SPX_API int32_t spx_strict_fill(const int32_t *src, int32_t *dst, int64_t h, int
  * it (numpy pairwise summation order).  Device inputs, device output. */
 SPX_API int32_t spx_center_shift(const double *new_xy, const double *old_xy, int64_t k,
                          double *out_dev, void *stream);
+/* numpy's pairwise summation (np.add.reduce over a contiguous float64
+ * array, the tree the shift above uses) of n device doubles into out_dev[0];
+ * the row strips' early-stop shift over the gathered per-cluster |delta|. */
+SPX_API int32_t spx_pairwise_sum(const double *x, int64_t n, double *out_dev, void *stream);
 
 /* ---- engine: replaces SegEngine (engine.py:86-230) ------------------------- */
 
@@ -219,7 +223,8 @@ SPX_API int32_t spx_engine_timing(spx_engine *eng, spx_timing *out);
  * Sequence: begin, xchg centres, { associate(1), xchg sums+labels, update,
  * xchg centres } x no_iters, associate(0), xchg labels, finish.
  * Results equal the single-GPU engine bit for bit.  Weak or no connectivity,
- * no early stop, fused-cell geometry only. */
+ * fused-cell geometry (4 <= S <= 255); early stop through
+ * spx_strip_shift_local + spx_pairwise_sum over the gathered shifts. */
 typedef struct spx_strip spx_strip;
 SPX_API int32_t spx_strip_create(const spx_settings *st, int64_t row_lo, int64_t row_hi,
                                  int32_t device, spx_strip **out);
@@ -229,6 +234,22 @@ SPX_API int32_t spx_strip_geometry(spx_strip *s, int64_t *out6);
 SPX_API int32_t spx_strip_begin(spx_strip *s, const uint8_t *rgb_window, void *stream);
 SPX_API int32_t spx_strip_associate(spx_strip *s, int32_t with_update, void *stream);
 SPX_API int32_t spx_strip_update(spx_strip *s, void *stream);
+/* The same steps split so the exchanges overlap compute: part 1 = interior
+ * own cell rows / clusters (need nothing from the neighbours), part 2 =
+ * boundary rows / clusters (after the neighbours' centres, respectively
+ * partial sums and labels, are unpacked), part 0 = all.  Per iteration:
+ * associate(1, interior), unpack centres, associate(1, boundary), start the
+ * sums + labels exchange, update(interior), unpack sums + labels,
+ * update(boundary) [which runs the exact fallback], start the centres
+ * exchange. */
+SPX_API int32_t spx_strip_associate_part(spx_strip *s, int32_t with_update, int32_t part,
+                                         void *stream);
+SPX_API int32_t spx_strip_update_part(spx_strip *s, int32_t part, void *stream);
+/* Early stop: |new - old| of the own clusters' centres after an update
+ * ((row_hi - row_lo) * ns_c * 2 doubles, cluster order); the ranks' arrays
+ * concatenated in rank order are the whole image's, whose spx_pairwise_sum
+ * is the reference's shift (engine.py:196). */
+SPX_API int32_t spx_strip_shift_local(spx_strip *s, double *out, void *stream);
 SPX_API int32_t spx_strip_pack_centres(spx_strip *s, double *up, double *down, void *stream);
 SPX_API int32_t spx_strip_unpack_centres(spx_strip *s, const double *from_up,
                                          const double *from_down, void *stream);

@@ -61,6 +61,7 @@ SIGNATURES = {
     "spx_weak_band": (I32, [P, P, I64, I64, I64, I64, P]),
     "spx_strict_fill": (I32, [P, P, I64, I64, I64, P]),
     "spx_center_shift": (I32, [P, P, I64, P, P]),
+    "spx_pairwise_sum": (I32, [P, I64, P, P]),
     "spx_engine_create": (I32, [ctypes.POINTER(SpxSettings), I64, I32, ctypes.POINTER(P)]),
     "spx_engine_destroy": (I32, [P]),
     "spx_engine_segment": (I32, [P, P, I64, P, P, P, P, P, P]),
@@ -83,6 +84,9 @@ SIGNATURES = {
     "spx_strip_begin": (I32, [P, P, P]),
     "spx_strip_associate": (I32, [P, I32, P]),
     "spx_strip_update": (I32, [P, P]),
+    "spx_strip_associate_part": (I32, [P, I32, I32, P]),
+    "spx_strip_update_part": (I32, [P, I32, P]),
+    "spx_strip_shift_local": (I32, [P, P, P]),
     "spx_strip_pack_centres": (I32, [P, P, P, P]),
     "spx_strip_unpack_centres": (I32, [P, P, P, P]),
     "spx_strip_pack_sums": (I32, [P, P, P, P]),

@@ -1164,7 +1164,8 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
                         int32_t* wl_reset) {
   ReduceParams p;
   p.wl_reset = wl_reset;
-  p.append = mode == kReduceAndExact;
+  p.append = mode == kReduceAndExact || mode == kReduceAppendFirst ||
+             mode == kReduceAppendLast || mode == kReduceAppend;
   p.acc = acc;
   p.img = img;
   p.labels = labels;
@@ -1192,7 +1193,8 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   p.kr1 = (int)kr1;
   p.row_off = (int)row_off;
   const long long nk = (kr1 - kr0) * ns_c;
-  if (mode == kReduceAndExact) SPX_CUDA(cudaMemsetAsync(worklist_n, 0, sizeof(int32_t), st));
+  if (mode == kReduceAndExact || mode == kReduceAppendFirst)
+    SPX_CUDA(cudaMemsetAsync(worklist_n, 0, sizeof(int32_t), st));
   if (nk <= 0 || frames <= 0) return SPX_OK;
   if (frames > 65535) {
     set_error("k_reduce_cells: at most 65535 frames per launch");
@@ -1202,7 +1204,7 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
     k_reduce_cells<<<dim3((unsigned)ceil_div(nk, kRedN), (unsigned)frames), kRedT, 0, st>>>(p);
     SPX_LAUNCH_CHECK("k_reduce_cells");
   }
-  if (mode == kReduceOnly) return SPX_OK;
+  if (mode == kReduceOnly || mode == kReduceAppendFirst || mode == kReduceAppend) return SPX_OK;
   if (s > 32) {
     // large cells: most clusters are flagged, one block per cluster
     const long long wb = std::max<long long>(

@@ -4,6 +4,9 @@
 // reads per cluster; batching frames gives the parallelism.
 #include <algorithm>
 
+#include <functional>
+#include <vector>
+
 #include "spx_internal.cuh"
 
 namespace spx {
@@ -220,6 +223,150 @@ __global__ void k_shift(const double* __restrict__ new_xy, const double* __restr
   if (done && threshold >= 0.0 && sh < threshold) done[f] = 2;
 }
 
+// ---- the same sum with the recursion tree evaluated in parallel -------------
+// numpy's pairwise_sum is a fixed binary tree over n values (leaves: the
+// <= 128-element blocks summed with eight accumulators; inner nodes:
+// left + right).  ShiftTree builds that tree once per n on the host; the
+// kernel sums every leaf in parallel, then evaluates the inner nodes level by
+// level (height 1 first: nodes of equal height are independent), one block
+// per frame -- the same additions in the same association as the recursion,
+// so bit-identical to numpy (tests: engine early stop vs the oracle).
+
+// Sum of the n values x[i] (or |x[i] - y[i]| when y != null) of one leaf.
+__device__ double leaf_sum(const double* x, const double* y, int n) {
+  auto v = [&](int i) { return y ? fabs(dsub(x[i], y[i])) : x[i]; };
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = dadd(res, v(i));
+    return res;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = v(j);
+  int i;
+  for (i = 8; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = dadd(r[j], v(i + j));
+  double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+  for (; i < n; ++i) res = dadd(res, v(i));
+  return res;
+}
+
+struct TreeDev {
+  const long long* leaf_off;
+  const int* leaf_n;
+  const int3* inner;      // (dst, left, right) value indices, by height
+  const int* lev_start;   // nlev + 1 offsets into inner
+  int nleaf, ninner, nlev, nvals, root;
+};
+
+__global__ void __launch_bounds__(256) k_shift_tree(const double* __restrict__ x,
+                                                    const double* __restrict__ y,
+                                                    int64_t frame_stride, TreeDev t,
+                                                    double* __restrict__ scratch,
+                                                    double* __restrict__ shift_out,
+                                                    int32_t* __restrict__ done,
+                                                    int32_t* __restrict__ passes,
+                                                    double threshold) {
+  const int f = blockIdx.x;
+  if (done && done[f]) return;  // block-uniform
+  const double* xf = x + (int64_t)f * frame_stride;
+  const double* yf = y ? y + (int64_t)f * frame_stride : nullptr;
+  double* vals = scratch + (int64_t)f * t.nvals;
+  for (int i = threadIdx.x; i < t.nleaf; i += blockDim.x)
+    vals[i] = leaf_sum(xf + t.leaf_off[i], yf ? yf + t.leaf_off[i] : nullptr, t.leaf_n[i]);
+  __syncthreads();
+  for (int l = 0; l < t.nlev; ++l) {
+    for (int j = t.lev_start[l] + threadIdx.x; j < t.lev_start[l + 1]; j += blockDim.x) {
+      const int3 q = t.inner[j];
+      vals[q.x] = dadd(vals[q.y], vals[q.z]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double sh = vals[t.root];
+    if (shift_out) shift_out[f] = sh;
+    if (passes) passes[f] += 1;
+    if (done && threshold >= 0.0 && sh < threshold) done[f] = 2;
+  }
+}
+
+void ShiftTree::release() {
+  for (void* q : {(void*)leaf_off, (void*)leaf_n, (void*)inner, (void*)lev_start, (void*)scratch})
+    if (q) cudaFree(q);
+  leaf_off = nullptr, leaf_n = nullptr, inner = nullptr, lev_start = nullptr, scratch = nullptr;
+  n = -1;
+}
+
+ShiftTree::~ShiftTree() { release(); }
+
+int ShiftTree::build(int64_t n_values, int max_frames) {
+  if (n == n_values && frames >= max_frames) return SPX_OK;
+  release();
+  std::vector<long long> loff;
+  std::vector<int> ln;
+  struct Node { int dst, l, r, h; };
+  std::vector<Node> nodes;
+  // returns (value index, height); inner value indices are assigned after
+  // the leaves are counted, so record them as negative placeholders first
+  std::function<std::pair<int, int>(int64_t, int64_t)> rec = [&](int64_t off, int64_t m) {
+    if (m <= 128) {
+      loff.push_back(off);
+      ln.push_back((int)m);
+      return std::make_pair((int)loff.size() - 1, 0);
+    }
+    int64_t m2 = m / 2;
+    m2 -= m2 % 8;
+    auto L = rec(off, m2);
+    auto R = rec(off + m2, m - m2);
+    nodes.push_back({-(int)nodes.size() - 1, L.first, R.first, 1 + std::max(L.second, R.second)});
+    return std::make_pair(nodes.back().dst, nodes.back().h);
+  };
+  const auto top = rec(0, std::max<int64_t>(n_values, 0));
+  const int nl = (int)loff.size();
+  auto fix = [&](int v) { return v < 0 ? nl + (-v - 1) : v; };
+  int hmax = 0;
+  for (auto& q : nodes) hmax = std::max(hmax, q.h);
+  std::vector<int3> in;
+  std::vector<int> ls(1, 0);
+  for (int h = 1; h <= hmax; ++h) {
+    for (auto& q : nodes)
+      if (q.h == h) in.push_back(make_int3(fix(q.dst), fix(q.l), fix(q.r)));
+    ls.push_back((int)in.size());
+  }
+  n = n_values;
+  frames = std::max(1, max_frames);
+  nleaf = nl;
+  ninner = (int)in.size();
+  nlev = hmax;
+  nvals = nl + ninner;
+  root = fix(top.first);
+  SPX_CUDA(cudaMalloc(&leaf_off, nl * sizeof(long long)));
+  SPX_CUDA(cudaMalloc(&leaf_n, nl * sizeof(int)));
+  SPX_CUDA(cudaMalloc(&inner, std::max<size_t>(1, in.size()) * sizeof(int3)));
+  SPX_CUDA(cudaMalloc(&lev_start, ls.size() * sizeof(int)));
+  SPX_CUDA(cudaMalloc(&scratch, (size_t)frames * nvals * sizeof(double)));
+  SPX_CUDA(cudaMemcpy(leaf_off, loff.data(), nl * sizeof(long long), cudaMemcpyHostToDevice));
+  SPX_CUDA(cudaMemcpy(leaf_n, ln.data(), nl * sizeof(int), cudaMemcpyHostToDevice));
+  if (!in.empty())
+    SPX_CUDA(cudaMemcpy(inner, in.data(), in.size() * sizeof(int3), cudaMemcpyHostToDevice));
+  SPX_CUDA(cudaMemcpy(lev_start, ls.data(), ls.size() * sizeof(int), cudaMemcpyHostToDevice));
+  return SPX_OK;
+}
+
+int ShiftTree::launch(const double* x, const double* y, int64_t frame_stride, int nframes,
+                      double* shift_out, int32_t* done, int32_t* passes, double threshold,
+                      cudaStream_t st) {
+  if (nframes > frames) {
+    set_error("shift tree built for %d frames, %d requested", frames, nframes);
+    return SPX_ERR_VALUE;
+  }
+  if (nframes <= 0) return SPX_OK;
+  TreeDev t{leaf_off, leaf_n, inner, lev_start, nleaf, ninner, nlev, nvals, root};
+  k_shift_tree<<<(unsigned)nframes, 256, 0, st>>>(x, y, frame_stride, t, scratch, shift_out, done,
+                                                  passes, threshold);
+  SPX_LAUNCH_CHECK("k_shift_tree");
+  return SPX_OK;
+}
+
 // done: 0 running, 2 = stops after the next association, 1 = stopped.
 __global__ void k_commit_done(int32_t* done, int frames) {
   int f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -277,5 +424,30 @@ extern "C" int32_t spx_reduce_range(double* slab, int64_t n_bl, const double* pr
 
 extern "C" int32_t spx_center_shift(const double* new_xy, const double* old_xy, int64_t k,
                                     double* out_dev, void* stream) {
-  return launch_shift(new_xy, old_xy, k, 1, out_dev, nullptr, nullptr, -1.0, as_stream(stream));
+  if (k < 0) {
+    set_error("center_shift: negative cluster count");
+    return SPX_ERR_VALUE;
+  }
+  // per-call tree (the API form; the engine keeps its tree)
+  ShiftTree t;
+  int rc = t.build(2 * k, 1);
+  if (rc) return rc;
+  rc = t.launch(new_xy, old_xy, 0, 1, out_dev, nullptr, nullptr, -1.0, as_stream(stream));
+  if (rc) return rc;
+  SPX_CUDA(cudaStreamSynchronize(as_stream(stream)));  // the tree is freed on return
+  return SPX_OK;
+}
+
+extern "C" int32_t spx_pairwise_sum(const double* x, int64_t n, double* out_dev, void* stream) {
+  if (n < 0) {
+    set_error("pairwise_sum: negative length");
+    return SPX_ERR_VALUE;
+  }
+  ShiftTree t;
+  int rc = t.build(n, 1);
+  if (rc) return rc;
+  rc = t.launch(x, nullptr, 0, 1, out_dev, nullptr, nullptr, -1.0, as_stream(stream));
+  if (rc) return rc;
+  SPX_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  return SPX_OK;
 }

@@ -70,6 +70,7 @@ struct Engine {
   int32_t* done = nullptr;
   int32_t* passes = nullptr;
   int32_t *cc_parent = nullptr, *cc_size = nullptr, *cc_nxt = nullptr, *cc_first = nullptr;
+  ShiftTree shift_tree;  // early stop: numpy's pairwise sum of |new - old| (engine.py:196)
   CRec* rec = nullptr;   // fp32 filter records of the current centres (cell path)
   ClusterAcc* acc = nullptr;  // per-cluster update accumulators (cell path)
   int32_t* worklist = nullptr;  // flagged clusters for the exact fallback (cell path)
@@ -271,6 +272,10 @@ struct Engine {
       SPX_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     } else {
       SPX_CUDA(cudaMalloc(&slab, B * K * n_bl * 6 * sizeof(double)));
+    }
+    if (st.early_stop >= 0.0) {
+      const int rt = shift_tree.build(2 * K, (int)B);
+      if (rt) return rt;
     }
     SPX_CUDA(cudaMalloc(&done, B * sizeof(int32_t)));
     SPX_CUDA(cudaMalloc(&passes, B * sizeof(int32_t)));
@@ -556,7 +561,8 @@ struct Engine {
       ++n_update;
       if (early) {
         // shift + per-frame pass count (engine.py:196); flags early stop
-        if ((rc = launch_shift(cxy[nxt], cxy[cur], K, B, nullptr, done, passes, st.early_stop, s)))
+        if ((rc = shift_tree.launch(cxy[nxt], cxy[cur], 2 * K, B, nullptr, done, passes,
+                                    st.early_stop, s)))
           return rc;
         ++launches;
       }

@@ -35,6 +35,12 @@ bool cell_path_ok(int64_t, int64_t, int64_t, int64_t);
 namespace {
 
 // dst[i] += src[i] for n accumulators (integer fields added as integers).
+__global__ void k_absdiff(const double* __restrict__ a, const double* __restrict__ b,
+                          double* __restrict__ out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fabs(dsub(a[i], b[i]));
+}
+
 __global__ void k_add_acc(ClusterAcc* __restrict__ dst, const ClusterAcc* __restrict__ src, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -138,21 +144,79 @@ struct Strip {
     return launch_records(cxy[0], clab[0], rec, nrl, g.ns_c, g.s, 1, s, k0, k1, rl0);
   }
 
-  int associate(bool with_update, cudaStream_t s) {
-    SPX_CUDA(cudaSetDevice(device));
-    return launch_cell(lab, cxy[cur], clab[cur], rec, labels, acc, nullptr, hl, g.width, g.s, nrl,
-                       g.ns_c, xy_weight, 1, with_update, s, own0, own1, rl0);
+  // Own cell rows split for overlapping the exchanges: the boundary rows
+  // (own0 with an upper neighbour, own1 - 1 with a lower one) are the only
+  // ones whose association reads halo centres and whose pixels contribute to
+  // halo clusters / label halos; the interior rows need nothing from the
+  // neighbours.  part: 0 all own rows, 1 interior, 2 boundary.
+  void rows_of(int part, int64_t r[4]) const {  // up to two ranges [r0,r1), [r2,r3)
+    const int64_t up = has_up() ? 1 : 0, dn = has_down() ? 1 : 0;
+    const int64_t i0 = std::min(own0 + up, own1), i1 = std::max(i0, own1 - dn);
+    r[0] = r[1] = r[2] = r[3] = 0;
+    if (part == 0) {
+      r[0] = own0, r[1] = own1;
+    } else if (part == 1) {
+      r[0] = i0, r[1] = i1;
+    } else {
+      r[0] = own0, r[1] = i0;  // top boundary row (if any)
+      r[2] = std::max(i1, i0), r[3] = own1;
+      if (r[1] >= r[2]) r[1] = r[3], r[2] = r[3] = 0;  // adjacent: one range
+    }
   }
 
-  int update(cudaStream_t s) {
+  int associate(bool with_update, int part, cudaStream_t s) {
+    SPX_CUDA(cudaSetDevice(device));
+    int64_t r[4];
+    rows_of(part, r);
+    for (int i = 0; i < 4; i += 2) {
+      if (r[i + 1] <= r[i]) continue;
+      const int rc = launch_cell(lab, cxy[cur], clab[cur], rec, labels, acc, nullptr, hl, g.width,
+                                 g.s, nrl, g.ns_c, xy_weight, 1, with_update, s, r[i], r[i + 1],
+                                 rl0);
+      if (rc) return rc;
+    }
+    return SPX_OK;
+  }
+
+  // part 0: the whole update; 1: interior clusters (before the neighbours'
+  // partial sums arrive); 2: boundary clusters, then the exact fallback over
+  // every flagged cluster of this iteration (needs the label halos).
+  int update(int part, cudaStream_t s) {
     SPX_CUDA(cudaSetDevice(device));
     const int nxt = cur ^ 1;
-    int rc = launch_reduce_cells(acc, lab, labels, cxy[cur], clab[cur], cxy[nxt], clab[nxt], counts,
-                                 rec, nullptr, worklist, worklist + K, hl, g.width, g.s, nrl, g.ns_c,
-                                 g.tile_len, 1, s, own0, own1, rl0);
+    int64_t r[4];
+    rows_of(part, r);
+    int rc;
+    auto reduce = [&](int64_t a, int64_t b, int mode) {
+      return launch_reduce_cells(acc, lab, labels, cxy[cur], clab[cur], cxy[nxt], clab[nxt],
+                                 counts, rec, nullptr, worklist, worklist + K, hl, g.width, g.s,
+                                 nrl, g.ns_c, g.tile_len, 1, s, a, b, rl0, mode);
+    };
+    if (part == 0) {
+      rc = reduce(own0, own1, kReduceAndExact);
+    } else if (part == 1) {
+      rc = reduce(r[0], r[1], kReduceAppendFirst);  // zeroes the count even if empty
+    } else if (r[1] > r[0] && r[3] > r[2]) {
+      rc = reduce(r[0], r[1], kReduceAppend);
+      if (!rc) rc = reduce(r[2], r[3], kReduceAppendLast);
+    } else if (r[1] > r[0] || r[3] > r[2]) {
+      rc = r[1] > r[0] ? reduce(r[0], r[1], kReduceAppendLast) : reduce(r[2], r[3], kReduceAppendLast);
+    } else {  // no neighbours: the interior part reduced every own cluster
+      rc = reduce(own0, own1, kExactOnly);
+    }
     if (rc) return rc;
-    // halo centres of the old buffer are stale in the new one until received
-    cur = nxt;
+    if (part != 1) cur = nxt;  // halo centres of the new buffer arrive by exchange
+    return SPX_OK;
+  }
+
+  // |new - old| of the own clusters' centres (x, y per cluster) after an
+  // update, for the early-stop shift over all clusters (engine.py:196).
+  int shift_local(double* out, cudaStream_t s) {
+    SPX_CUDA(cudaSetDevice(device));
+    const int64_t c = g.ns_c, no = (own1 - own0) * c;
+    k_absdiff<<<(unsigned)ceil_div(std::max<int64_t>(2 * no, 1), 256), 256, 0, s>>>(
+        cxy[cur] + own0 * c * 2, cxy[cur ^ 1] + own0 * c * 2, out, 2 * no);
+    SPX_LAUNCH_CHECK("k_absdiff");
     return SPX_OK;
   }
 
@@ -299,10 +363,6 @@ int32_t spx_strip_create(const spx_settings* st, int64_t row_lo, int64_t row_hi,
     set_error("row strips need the fused cell path (4 <= S <= 255, ceil(3S / tile_len) <= 64)");
     return SPX_ERR_INVALID_SETTINGS;
   }
-  if (st->early_stop >= 0.0) {
-    set_error("row strips do not support early stop");
-    return SPX_ERR_INVALID_SETTINGS;
-  }
   spx_strip* s = new spx_strip();
   int rc = s->s.init(*st, row_lo, row_hi, device);
   if (rc) {
@@ -334,12 +394,34 @@ int32_t spx_strip_begin(spx_strip* s, const uint8_t* rgb_window, void* stream) {
   return s->s.begin(rgb_window, as_stream(stream));
 }
 int32_t spx_strip_associate(spx_strip* s, int32_t with_update, void* stream) {
-  return s->s.associate(with_update != 0, as_stream(stream));
+  return s->s.associate(with_update != 0, 0, as_stream(stream));
 }
-int32_t spx_strip_update(spx_strip* s, void* stream) { return s->s.update(as_stream(stream)); }
+
+int32_t spx_strip_update(spx_strip* s, void* stream) { return s->s.update(0, as_stream(stream)); }
+
+int32_t spx_strip_associate_part(spx_strip* s, int32_t with_update, int32_t part, void* stream) {
+  if (part < 0 || part > 2) {
+    spx::set_error("strip part must be 0 (all), 1 (interior) or 2 (boundary)");
+    return SPX_ERR_VALUE;
+  }
+  return s->s.associate(with_update != 0, part, as_stream(stream));
+}
+
+int32_t spx_strip_update_part(spx_strip* s, int32_t part, void* stream) {
+  if (part < 0 || part > 2) {
+    spx::set_error("strip part must be 0 (all), 1 (interior) or 2 (boundary)");
+    return SPX_ERR_VALUE;
+  }
+  return s->s.update(part, as_stream(stream));
+}
+
+int32_t spx_strip_shift_local(spx_strip* s, double* out, void* stream) {
+  return s->s.shift_local(out, as_stream(stream));
+}
 int32_t spx_strip_pack_centres(spx_strip* s, double* up, double* down, void* stream) {
   return s->s.pack_centres(up, down, as_stream(stream));
 }
+
 int32_t spx_strip_unpack_centres(spx_strip* s, const double* from_up, const double* from_down,
                                  void* stream) {
   return s->s.unpack_centres(from_up, from_down, as_stream(stream));

@@ -25,6 +25,7 @@ from .errors import InvalidSettingsError
 from .sharding import strip_plan
 
 ACC_BYTES = 48  # sizeof(ClusterAcc)
+ALL, INTERIOR, BOUNDARY = 0, 1, 2
 
 
 def _p(t):
@@ -80,15 +81,26 @@ class StripEngine:
         down = bufs[1][i] if self.has_down else None
         return _p(up), _p(down)
 
-    # kernel steps
+    # kernel steps; part: 0 all own rows, 1 interior, 2 boundary (spx.h)
     def begin(self, rgb_window):
         self._call("spx_strip_begin", _p(rgb_window))
 
-    def associate(self, with_update):
-        self._call("spx_strip_associate", int(with_update))
+    def associate(self, with_update, part=ALL):
+        self._call("spx_strip_associate_part", int(with_update), int(part))
 
-    def update(self):
-        self._call("spx_strip_update")
+    def update(self, part=ALL):
+        self._call("spx_strip_update_part", int(part))
+
+    @property
+    def own_clusters(self):
+        return (self.row_hi - self.row_lo) * self.grid.ns_c
+
+    def shift_local(self):
+        """|new - old| of the own centres after an update (x, y per cluster)."""
+        out = self.torch.empty((self.own_clusters * 2,), dtype=self.torch.float64,
+                               device=self.device)
+        self._call("spx_strip_shift_local", _p(out))
+        return out
 
     def pack(self, what):
         self._call(f"spx_strip_pack_{what}", *self._pair(getattr(self, what), True))
@@ -109,47 +121,70 @@ class StripEngine:
         return labels, cxy, clab, counts
 
 
+def pairwise_sum(x):
+    """numpy's pairwise sum of a contiguous float64 device vector (spx_pairwise_sum),
+    returned as a 1-element device tensor."""
+    import torch
+    out = torch.empty((1,), dtype=torch.float64, device=x.device)
+    lib = _lib.load()
+    _lib.check(lib.spx_pairwise_sum(_p(x), x.numel(), _p(out),
+                                    ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)),
+               "pairwise_sum")
+    return out
+
+
 class LocalComm:
-    """Neighbour exchange between strips held by one process (device copies)."""
+    """Neighbour exchange between strips held by one process (device copies).
+
+    start() packs every strip's send buffers; finish() copies them to the
+    neighbours' receive buffers and unpacks (the same schedule as DistComm,
+    executed in order)."""
 
     def __init__(self, strips):
         self.strips = strips
 
+    def start(self, whats):
+        for what in whats:
+            for st in self.strips:
+                st.pack(what)
+        return whats
+
+    def finish(self, whats):
+        for what in whats:
+            for i, st in enumerate(self.strips):
+                bufs = getattr(st, what)
+                if st.has_up:  # from the upper strip's "down" send buffer
+                    bufs[0][1].copy_(getattr(self.strips[i - 1], what)[1][0])
+                if st.has_down:
+                    bufs[1][1].copy_(getattr(self.strips[i + 1], what)[0][0])
+            for st in self.strips:
+                st.unpack(what)
+
     def exchange(self, what):
-        for st in self.strips:
-            st.pack(what)
-        for i, st in enumerate(self.strips):
-            bufs = getattr(st, what)
-            if st.has_up:  # from the upper strip's "down" send buffer
-                bufs[0][1].copy_(getattr(self.strips[i - 1], what)[1][0])
-            if st.has_down:
-                bufs[1][1].copy_(getattr(self.strips[i + 1], what)[0][0])
-        for st in self.strips:
-            st.unpack(what)
+        self.finish(self.start([what]))
+
+    def shift(self):
+        """The whole image's centre shift (device scalar): the strips' own
+        |delta| arrays concatenated in cluster order, pairwise-summed."""
+        import torch
+        return pairwise_sum(torch.cat([st.shift_local() for st in self.strips]))
 
 
 class DistComm:
     """Neighbour exchange between ranks with torch.distributed send/recv.
 
     Buffers are [[send_up, recv_up], [send_down, recv_down]].  With NCCL the
-    device buffers go over NVLink directly; with gloo (CPU transport, used for
-    functional tests) device buffers are staged through host memory.
+    device buffers go over NVLink directly, and start() returns without
+    waiting: the transfer runs on NCCL's stream while this rank's stream
+    computes, and finish() makes the stream wait for it (Work.wait()) before
+    unpacking.  With gloo (CPU transport, functional tests) device buffers
+    are staged through host memory and the exchange completes in start().
     """
 
-    def __init__(self, rank, world, group=None):
-        self.rank, self.world, self.group = rank, world, group
+    def __init__(self, rank, world, strip, group=None):
+        self.rank, self.world, self.strip, self.group = rank, world, strip, group
 
-    def exchange_buffers(self, bufs):
-        import torch.distributed as dist
-        if bufs[0][0].is_cuda and dist.get_backend(self.group) == "gloo":
-            host = [[b.cpu() for b in pair] for pair in bufs]
-            self._exchange(host)
-            for pair, hpair in zip(bufs, host):
-                pair[1].copy_(hpair[1])
-            return
-        self._exchange(bufs)
-
-    def _exchange(self, bufs):
+    def _ops(self, bufs):
         import torch.distributed as dist
         ops = []
         if self.rank > 0:
@@ -158,36 +193,103 @@ class DistComm:
         if self.rank < self.world - 1:
             ops.append(dist.P2POp(dist.isend, bufs[1][0], self.rank + 1, self.group))
             ops.append(dist.P2POp(dist.irecv, bufs[1][1], self.rank + 1, self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        return ops
+
+    def _gloo(self):
+        import torch.distributed as dist
+        return dist.get_backend(self.group) == "gloo"
+
+    def start(self, whats):
+        import torch.distributed as dist
+        st = self.strip
+        for what in whats:
+            st.pack(what)
+        works, staged = [], []
+        for what in whats:
+            bufs = getattr(st, what)
+            if bufs[0][0].is_cuda and self._gloo():
+                host = [[b.cpu() for b in pair] for pair in bufs]
+                ops = self._ops(host)
+                if ops:
+                    for w in dist.batch_isend_irecv(ops):
+                        w.wait()
+                for pair, hpair in zip(bufs, host):
+                    pair[1].copy_(hpair[1])
+                continue
+            ops = self._ops(bufs)
+            if ops:
+                works.extend(dist.batch_isend_irecv(ops))
+        return whats, works
+
+    def finish(self, handle):
+        whats, works = handle
+        for w in works:
+            w.wait()  # NCCL: the current stream waits; the host does not
+        for what in whats:
+            self.strip.unpack(what)
 
     def exchange(self, strip, what):
-        strip.pack(what)
-        self.exchange_buffers(getattr(strip, what))
-        strip.unpack(what)
+        self.finish(self.start([what]))
+
+    def shift(self):
+        """The whole image's centre shift: every rank's own |delta| gathered in
+        rank (= cluster) order, then the same pairwise sum on every rank."""
+        import torch
+        import torch.distributed as dist
+        local = self.strip.shift_local()
+        g = self.strip.grid
+        sizes = [2 * (p.cell_row_hi - p.cell_row_lo) * g.ns_c
+                 for p in strip_plan(self.strip.settings.img_height, g.s, g.ns_r, self.world)]
+        m = max(sizes)
+        pad = torch.zeros((m,), dtype=torch.float64, device=local.device)
+        pad[:local.numel()] = local
+        if self._gloo():
+            parts = [torch.empty((m,), dtype=torch.float64) for _ in range(self.world)]
+            dist.all_gather(parts, pad.cpu(), group=self.group)
+            parts = [t.to(local.device) for t in parts]
+        else:
+            parts = [torch.empty_like(pad) for _ in range(self.world)]
+            dist.all_gather(parts, pad, group=self.group)
+        full = torch.cat([t[:n] for t, n in zip(parts, sizes)])
+        return pairwise_sum(full)
 
 
-def _run(strips, xchg):
-    """The per-strip step sequence (identical for local and distributed runs)."""
+def _run(strips, comm):
+    """The per-strip step sequence (identical for local and distributed runs).
+
+    Each exchange overlaps the compute that does not need it: the centres
+    travel while the interior rows associate, the partial sums and label
+    halos while the interior clusters update.  With early stop, the shift of
+    every update (all clusters, numpy's pairwise order) decides on the host
+    whether the next association is the last (engine.py:196-200)."""
     st = strips[0].settings
-    xchg("centres")
+    thr = st.early_stop_threshold
+    h = comm.start(["centres"])
     for _ in range(st.no_iters):
         for s in strips:
-            s.associate(True)
-        xchg("sums")
-        xchg("labels")
+            s.associate(True, INTERIOR)
+        comm.finish(h)
         for s in strips:
-            s.update()
-        xchg("centres")
+            s.associate(True, BOUNDARY)
+        h = comm.start(["sums", "labels"])
+        for s in strips:
+            s.update(INTERIOR)
+        comm.finish(h)
+        for s in strips:
+            s.update(BOUNDARY)
+        stop = thr is not None and float(comm.shift().item()) < thr
+        h = comm.start(["centres"])
+        if stop:
+            break
     for s in strips:
-        s.associate(False)
-    xchg("labels")
+        s.associate(False, INTERIOR)
+    comm.finish(h)
+    for s in strips:
+        s.associate(False, BOUNDARY)
+    comm.finish(comm.start(["labels"]))
 
 
 def check_strip_settings(settings):
-    if settings.early_stop_threshold is not None:
-        raise InvalidSettingsError("row strips do not support early stop")
     if settings.do_enforce_connectivity and settings.connectivity_mode.value == "strict":
         raise InvalidSettingsError("row strips support weak or no connectivity")
 
@@ -207,8 +309,7 @@ def segment_strips_local(settings, rgb, n_strips, device=0):
     d_rgb = torch.from_numpy(np.ascontiguousarray(rgb, dtype=np.uint8)).to(strips[0].device)
     for s in strips:
         s.begin(d_rgb[s.y0:s.y0 + s.hl].contiguous())
-    comm = LocalComm(strips)
-    _run(strips, comm.exchange)
+    _run(strips, LocalComm(strips))
     outs = [s.finish() for s in strips]
     torch.cuda.synchronize(strips[0].device)
     labels = torch.cat([o[0] for o in outs]).cpu().numpy()
@@ -230,8 +331,7 @@ def segment_strip_rank(settings, rgb_window, rank, world, device, group=None):
     p = strip_plan(settings.img_height, grid.s, grid.ns_r, world)[rank]
     strip = StripEngine(settings, p.cell_row_lo, p.cell_row_hi, device)
     strip.begin(rgb_window)
-    comm = DistComm(rank, world, group)
-    _run([strip], lambda what: comm.exchange(strip, what))
+    _run([strip], DistComm(rank, world, strip, group))
     return strip.finish()
 
 
@@ -245,4 +345,4 @@ def strip_window(settings, rank, world):
 
 
 __all__ = ["StripEngine", "LocalComm", "DistComm", "segment_strips_local", "segment_strip_rank",
-           "strip_window", "default_min_size"]
+           "strip_window", "pairwise_sum", "default_min_size"]

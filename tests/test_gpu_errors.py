@@ -114,10 +114,11 @@ def test_c_abi_engine_create_reports_invalid_settings():
 
 
 def test_strip_engine_rejects_unsupported_modes():
+    # strict connectivity is a whole-image CCL: not available in row strips;
+    # early stop is (the gathered shift, tests/test_gpu_pipeline.py)
     from paper_1509_04232_b200.strips import check_strip_settings
-    with pytest.raises(spx.InvalidSettingsError):
-        check_strip_settings(spx.Settings(img_width=64, img_height=64, spixel_size=8,
-                                          early_stop_threshold=1.0))
+    check_strip_settings(spx.Settings(img_width=64, img_height=64, spixel_size=8,
+                                      early_stop_threshold=1.0))
     with pytest.raises(spx.InvalidSettingsError):
         check_strip_settings(spx.Settings(img_width=64, img_height=64, spixel_size=8,
                                           connectivity_mode=spx.ConnectivityMode.STRICT))

@@ -434,6 +434,14 @@ def test_cell_path_batch_gray_heavy_frames():
     (200, 160, dict(spixel_size=16), 5),
     (250, 96, dict(spixel_size=8, tile_len=5, enable_perturbation=True), 4),
     (130, 64, dict(spixel_size=12, do_enforce_connectivity=False, no_iters=3), 3),
+    # early stop (the gathered shift decides on every strip at once); the
+    # thresholds stop the noise / smooth frames at different passes
+    (200, 160, dict(spixel_size=16, no_iters=9, early_stop_threshold=400.0), 3),
+    (240, 200, dict(spixel_size=12, no_iters=12, early_stop_threshold=150.0), 4),
+    # odd width (padded planes), S > 32, boundary-only strips (1-2 own rows)
+    (231, 157, dict(spixel_size=9, no_iters=4), 5),
+    (300, 150, dict(spixel_size=40, no_iters=3), 3),
+    (96, 80, dict(spixel_size=8, no_iters=3), 6),
 ])
 def test_row_strips_equal_whole_image(h, w, kw, n):
     """C5 decomposition: strips with halo centres / partial-sum / label exchange
@@ -584,8 +592,9 @@ class TestStream:
             assert r.spixel_map.centers_lab.tobytes() == clab.tobytes()
 
 
-@pytest.mark.parametrize("ranks", [2, 3])
-def test_row_strips_distributed_processes(ranks):
+@pytest.mark.parametrize("ranks,extra", [(2, []), (3, []),
+                                         (3, ["--early-stop", "1000", "--iters", "10"])])
+def test_row_strips_distributed_processes(ranks, extra):
     """One process per strip (torchrun), halos and partial sums exchanged
     through DistComm (gloo, staged through host memory; the ranks share this
     GPU): the gathered strips equal the whole-image engine bit for bit."""
@@ -601,7 +610,8 @@ def test_row_strips_distributed_processes(ranks):
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={ranks}", "--master-addr", "127.0.0.1",
                         "--master-port", str(port), os.path.join(root, "tools", "strips_dist.py"),
-                        "--size", "512", "--check"], env=env, capture_output=True, text=True,
+                        "--size", "512", "--check", *extra], env=env, capture_output=True,
+                       text=True,
                        timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "bit-identical to the whole-image engine: True" in r.stdout

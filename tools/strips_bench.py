@@ -61,8 +61,7 @@ def main():
         t0 = time.perf_counter()
         for s, wdw in zip(strips, windows):
             s.begin(wdw)
-        comm = LocalComm(strips)
-        _run(strips, comm.exchange)
+        _run(strips, LocalComm(strips))
         outs = [s.finish() for s in strips]
         torch.cuda.synchronize()
         host_s = time.perf_counter() - t0
