@@ -429,6 +429,197 @@ def run_ours(args):
     return 0
 
 
+C5_N, C5_S = 16384, 16
+METRIC_C5 = "images/s and Mpix/s, 16384x16384 S=16 5 iters, row strips (1/2/4/8 B200)"
+
+
+def c5_settings():
+    import paper_1509_04232_b200 as spx
+    return spx.Settings(img_width=C5_N, img_height=C5_N, spixel_size=C5_S, no_iters=ITERS)
+
+
+def c5_image():
+    return np.random.default_rng(0).integers(0, 256, (C5_N, C5_N, 3), dtype=np.uint8)
+
+
+def c5_config(world):
+    return {"workload": "C5: 16384x16384 RGB (268 Mpx), S=16 (1024x1024 grid, 1,048,576 "
+                        "clusters), m=10, 5 iters, LAB, weak connectivity",
+            "parallelism": f"row strips x{world}: halo centres, boundary-cluster partial sums "
+                           f"and S label rows exchanged with the vertical neighbours per "
+                           f"iteration (NCCL send/recv over NVLink)",
+            "global_batch": 1, "l2": "inputs > L2: 805 MB RGB + 3.2 GB Lab per image"}
+
+
+def run_reference_c5(args):
+    """Reference arm for C5: the reference SegEngine (all host cores) on a
+    bounded band of the image per step, scaled to images/s."""
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return 0
+    sp = reference_package()
+    if sp is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    cores = os.cpu_count() or 1
+    rows = args.ref_rows
+    band = c5_image()[:rows]
+    st = sp.Settings(img_width=C5_N, img_height=rows, spixel_size=C5_S, no_iters=ITERS)
+    eng = sp.SegEngine(st, backend="par", workers=cores)
+    img = sp.ImageRGB(band)
+    for _ in range(args.warmup):
+        eng.perform_segmentation(img)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        eng.perform_segmentation(img)
+        times.append(time.perf_counter() - t0)
+    per_image = statistics.mean(times) * C5_N / rows
+    value = 1.0 / per_image
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC_C5, "value": value, "unit": "images/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * per_image, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": c5_config(world),
+        "mpix_per_s": value * C5_N * C5_N / 1e6,
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "reference",
+                         "sample": f"bounded sample: a {C5_N}x{rows} band of the image per step "
+                                   f"(x{args.steps}), reference SegEngine backend=par "
+                                   f"workers={cores}, scaled by {C5_N}/{rows}"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}))
+    return 0
+
+
+def run_ours_c5(args):
+    """C5: one 16384^2 image per step, row strips over the ranks (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1509_04232_b200.sharding import strip_plan
+    from paper_1509_04232_b200.strips import DistComm, LocalComm, StripEngine, _run, strip_window
+
+    world, rank, local = dist_setup()
+    backend = os.environ.get("SPX_BENCH_BACKEND", "nccl")
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    st = c5_settings()
+    import paper_1509_04232_b200 as spx
+    g = spx.compute_grid(st)
+    plan = strip_plan(C5_N, g.s, g.ns_r, world)[rank]
+    y0, y1 = strip_window(st, rank, world)
+    host = c5_image()
+    window_host = torch.from_numpy(np.ascontiguousarray(host[y0:y1])).pin_memory()
+    del host
+    window = window_host.to(dev)
+    strip = StripEngine(st, plan.cell_row_lo, plan.cell_row_hi, dev)
+    comm = DistComm(rank, world, strip) if world > 1 else LocalComm([strip])
+    stream = torch.cuda.current_stream(dev)
+
+    def step(win):
+        strip.begin(win)
+        _run([strip], comm)
+        return strip.finish()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        step(window)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(window)
+        e1.record(stream)
+        clk._sample()
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    red_dev = dev if backend == "nccl" else "cpu"
+    if world > 1:
+        t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = args.steps / (ms / 1e3)
+    # end to end: the rank's RGB window uploaded from pinned host memory and
+    # its own rows / clusters' results read back, every step
+    n_own = strip.own_clusters
+    outs_host = [torch.empty((plan.y_hi - plan.y_lo, C5_N), dtype=torch.int32).pin_memory(),
+                 torch.empty((n_own, 2), dtype=torch.float64).pin_memory(),
+                 torch.empty((n_own, 3), dtype=torch.float64).pin_memory(),
+                 torch.empty((n_own,), dtype=torch.int64).pin_memory()]
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        window.copy_(window_host, non_blocking=True)
+        res = step(window)
+        for hb, d in zip(outs_host, res):
+            hb.copy_(d, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=red_dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = window_host.numel() * world
+    d2h = sum(t.numel() * t.element_size() for t in outs_host) * world
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        n_px = C5_N * C5_N
+        frame_bytes = algorithmic_bytes(n_px, g.num_clusters, ITERS)
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            sp = reference_package()
+            if sp is not None:
+                rows = args.ref_rows
+                band = np.random.default_rng(0).integers(0, 256, (C5_N, C5_N, 3),
+                                                         dtype=np.uint8)[:rows]
+                cores = os.cpu_count() or 1
+                rst = sp.Settings(img_width=C5_N, img_height=rows, spixel_size=C5_S,
+                                  no_iters=ITERS)
+                reng = sp.SegEngine(rst, backend="par", workers=cores)
+                t0 = time.perf_counter()
+                reng.perform_segmentation(sp.ImageRGB(band))
+                per_image = (time.perf_counter() - t0) * C5_N / rows
+                cpu = {"value": 1.0 / per_image, "unit": "images/s", "cores": cores,
+                       "kind": "reference",
+                       "sample": f"a {C5_N}x{rows} band, reference SegEngine par x{cores}, "
+                                 f"scaled by {C5_N}/{rows}"}
+        line = {
+            "metric": METRIC_C5, "value": value, "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": c5_config(world),
+            "mpix_per_s": value * n_px / 1e6,
+            "frame_roofline": {"bytes_per_image": frame_bytes,
+                               "achieved_gbs": value * frame_bytes / 1e9 / world,
+                               "frac": value * frame_bytes / 1e9 / world / peak,
+                               "peak": peak, "peak_kind": peak_kind,
+                               "note": "SURVEY §8(d) bytes of the whole image / time, per GPU"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": args.steps / (e2e_ms / 1e3), "unit": "images/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "per rank: RGB window H2D (pinned), strip engine, own results D2H"},
+            "gpu_launches": None, "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -440,6 +631,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-frames", type=int, default=400)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="c1", choices=["c1", "c5"],
+                    help="c1: the BASELINE headline (default); c5: 16384^2 row strips")
+    ap.add_argument("--ref-rows", type=int, default=1024,
+                    help="c5 reference arm / cpu_baseline: rows of the bounded band")
     args = ap.parse_args()
     if args.gpus < 1:
         ap.error("--gpus must be >= 1")
@@ -449,6 +644,8 @@ def main():
     if world != args.gpus:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
         return 2
+    if args.workload == "c5":
+        return run_reference_c5(args) if args.impl == "reference" else run_ours_c5(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

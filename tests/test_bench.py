@@ -54,3 +54,12 @@ def test_bench_gpus_2_launches_two_ranks():
     assert line["config"]["global_batch"] == 16
     assert line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["gpu_launches"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_c5_row_strips_two_ranks():
+    # C5 (16384^2) as two row strips, ranks sharing the GPU over gloo
+    line = _run(["--workload", "c5", "--gpus", "2", "--steps", "1", "--warmup", "3", "--no-cpu"],
+                {"SPX_BENCH_BACKEND": "gloo"}, timeout=900)
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
