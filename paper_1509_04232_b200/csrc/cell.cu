@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
   auto run_len = [&](int c4, int x) { return AL ? 4 : min(4, min(S - c4, p.w - x)); };
   auto load_run = [&](bool ok, int y, int x, int nv, float4& Lx, float4& Ax, float4& Bx) {
     if (!ok) return;
+    SPX_DCHECK(y >= 0 && y < p.h && x >= 0 && nv >= 1 && x + nv <= p.w);
     const float* q = fimg + (long long)y * p.w + x;
     if (AL) {
       Lx = __ldg(reinterpret_cast<const float4*>(q));
@@ -366,7 +367,12 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
       }
       int lab4[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) lab4[i] = cand_k[t[i]] + p.row_off * p.ns_c;  // GLOBAL ids
+      for (int i = 0; i < 4; ++i) {
+        SPX_DCHECK(t[i] >= 0 && t[i] < 9);
+        SPX_DCHECK(i >= nv || (cand_k[t[i]] >= 0 && cand_k[t[i]] < K));
+        lab4[i] = cand_k[t[i]] + p.row_off * p.ns_c;  // GLOBAL ids
+      }
+      SPX_DCHECK(y < p.h && x + nv <= p.w && pix + nv <= (long long)p.frames * hw);
       if (ACC) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -410,6 +416,7 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
               sacc = dadd(dadd(sacc, v.x), v.y);
             }
             // an empty (or out-of-grid) slot sums to +0.0: nothing to add
+            SPX_DCHECK(sacc == 0.0 || (cand_k[col / 3] >= 0 && cand_k[col / 3] < K));
             if (sacc != 0.0) atomicAdd(&fa[cand_k[col / 3]].s[col % 3], sacc);
           } else {
             const ulonglong2* src =
@@ -441,6 +448,7 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
               }
             }
             if (cnt) {
+              SPX_DCHECK(cand_k[col - 27] >= 0 && cand_k[col - 27] < K && flg <= cnt);
               ClusterAcc* o = fa + cand_k[col - 27];
               atomicAdd(&o->sx, sxr + cnt * (unsigned long long)x_cell);
               atomicAdd(&o->sy, syr + cnt * (unsigned long long)y_glob0);
@@ -750,6 +758,8 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
     const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
     const int ya0 = max(ry0, 0);
     const int ww = wx1 - wx0, wrows = ry1 - ya0;
+    SPX_DCHECK(gk >= 0 && (long long)gk < cap && ww > 0 && ww <= 3 * p.s && wrows > 0 &&
+               wrows <= 3 * p.s && p.n_bl <= kExMaxStrips);
     // the window's labels: staged (row stride ww) or in place (row stride w)
     const int32_t* const win = staged ? win_s : lb + (long long)ya0 * p.w + wx0;
     const int wst = staged ? ww : p.w;
@@ -760,12 +770,14 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
 #pragma unroll 1
       for (int i = threadIdx.x; i < wrows * q4; i += blockDim.x) {
         const int rr = i / q4, cq = i - rr * q4;
+        SPX_DCHECK(rr * ww + 4 * cq + 4 <= 9 * p.s * p.s);
         cp_async16(win_s + rr * ww + 4 * cq, lb + (long long)(ya0 + rr) * p.w + wx0 + 4 * cq);
       }
     } else {
 #pragma unroll 1
       for (int i = threadIdx.x; i < wrows * ww; i += blockDim.x) {
         const int rr = i / ww, cc = i - rr * ww;
+        SPX_DCHECK(i < 9 * p.s * p.s);
         cp_async4(win_s + i, lb + (long long)(ya0 + rr) * p.w + wx0 + cc);
       }
     }
@@ -790,6 +802,7 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
         const bool own = row < rc;
         const int c0 = own ? min(sg * seg, ww) : 0, c1 = own ? min(c0 + seg, ww) : 0;
         const int y = yc + row;
+        SPX_DCHECK(!own || (y >= ya0 && y < ya0 + wrows && c0 >= 0 && c1 <= ww));
         const int32_t* wrow = win + (long long)(y - ya0) * wst;
         // Members of this lane's segment as bit masks of <= 96 columns; a
         // longer segment (S > 32) is walked in sub-chunks of 96 columns,
@@ -852,6 +865,7 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
                   const int k = 32 * wd + __ffs(mw) - 1;
                   mw &= mw - 1;
                   if (o >= base && o < base + kExCap) {
+                    SPX_DCHECK(a0 + k < ww && o - base >= 0);
                     cp_async4(cw + (o - base), g0 + k);
                     cp_async4(cw + kExCap + (o - base), g0 + p.plane + k);
                     cp_async4(cw + 2 * kExCap + (o - base), g0 + 2 * p.plane + k);
@@ -937,6 +951,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_exact_wide(ReduceParams p) 
     const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
     const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
     const int nseg = (wx1 - wx0 + 255) >> 8;
+    SPX_DCHECK(gk >= 0 && gk < p.frames * K && p.n_bl <= kExMaxStrips && wx1 > wx0);
 #pragma unroll 1
     for (int i = threadIdx.x; i < p.n_bl * 6; i += blockDim.x) (&strips[0][0])[i] = 0.0;
     __syncthreads();

@@ -389,15 +389,38 @@ int launch_weak2(const int32_t* src, int32_t* dst, int64_t h, int64_t w, int fra
 // scratch: parent, size, nxt (n each) and first (frames * nlab + kStrictExtra),
 // all int32;
 // src and dst must not overlap (dst holds the component list meanwhile).
+static int launch_strict_chunk(const int32_t* src, int32_t* dst, int64_t h, int64_t w,
+                               int frames, int64_t nlab, int64_t min_size, int32_t* parent,
+                               int32_t* size, int32_t* nxt, int32_t* first, cudaStream_t st);
+
+// Frames are independent: a batch whose pixel indices would overflow int32
+// runs in chunks of whole frames (same buffers, offset by the chunk).
 int launch_strict(const int32_t* src, int32_t* dst, int64_t h, int64_t w, int frames,
                   int64_t nlab, int64_t min_size, int32_t* parent, int32_t* size, int32_t* nxt,
                   int32_t* first, cudaStream_t st) {
-  int64_t hw = h * w, n = hw * frames;
-  if (n == 0) return SPX_OK;
-  if (n >= INT32_MAX) {
-    set_error("strict_fill: %lld pixels exceed the int32 component index", (long long)n);
+  const int64_t hw = h * w;
+  if (hw == 0 || frames <= 0) return SPX_OK;
+  if (hw >= INT32_MAX) {
+    set_error("strict_fill: %lld pixels per frame exceed the int32 component index",
+              (long long)hw);
     return SPX_ERR_VALUE;
   }
+  const int fc = (int)std::min<int64_t>(frames, (INT32_MAX - 1) / hw);
+  for (int f0 = 0; f0 < frames; f0 += fc) {
+    const int nf = std::min(fc, frames - f0);
+    const int64_t o = (int64_t)f0 * hw;
+    const int rc = launch_strict_chunk(src + o, dst + o, h, w, nf, nlab, min_size, parent + o,
+                                       size + o, nxt + o, first, st);
+    if (rc) return rc;
+  }
+  return SPX_OK;
+}
+
+static int launch_strict_chunk(const int32_t* src, int32_t* dst, int64_t h, int64_t w,
+                               int frames, int64_t nlab, int64_t min_size, int32_t* parent,
+                               int32_t* size, int32_t* nxt, int32_t* first, cudaStream_t st) {
+  int64_t hw = h * w, n = hw * frames;
+  if (n == 0) return SPX_OK;
   if (h > 65535 || frames > 65535) {
     set_error("strict_fill: at most 65535 rows and 65535 frames per launch");
     return SPX_ERR_VALUE;

@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
         convert_px<SPACE>(lut, fc, c[3 * i], c[3 * i + 1], c[3 * i + 2], o[3 * i], o[3 * i + 1],
                           o[3 * i + 2]);
       if (PLANAR) {
+        SPX_DCHECK(pr + 4 <= pst && pf < p1 / hw);
         float* base = out + pf * 3 * pst + pr;
         *reinterpret_cast<float4*>(base) =
             make_float4(with_flag(o[0], o[1], o[2], tau), with_flag(o[3], o[4], o[5], tau),
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
         float o0, o1, o2;
         convert_px<SPACE>(lut, fc, rgb[p * 3], rgb[p * 3 + 1], rgb[p * 3 + 2], o0, o1, o2);
         if (PLANAR) {
+          SPX_DCHECK(pr + (p - q) < hw && pf < p1 / hw);
           float* base = out + pf * 3 * pst + pr + (p - q);
           base[0] = with_flag(o0, o1, o2, tau);
           base[pst] = o1;
