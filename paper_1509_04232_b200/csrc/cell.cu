@@ -125,6 +125,12 @@ constexpr int kGroupsPerWarp = 4;  // max consecutive cell groups walked by one 
 #ifndef SPX_MINB
 #define SPX_MINB 4  // resident blocks per SM the register budget is sized for
 #endif
+#ifndef SPX_MINB_FIN
+#define SPX_MINB_FIN SPX_MINB  // the same for the final (no-accumulation) pass
+#endif
+#ifndef SPX_PAIRMIN
+#define SPX_PAIRMIN 1  // top-2 keys merged two candidates at a time (cellbench: -0.8% / -1.6%)
+#endif
 // (rounded up to 16 bytes: the accumulators behind it take 16-byte accesses)
 __host__ __device__ constexpr size_t cand_bytes(int lpc) {
   return ((size_t)(32 / lpc) * 9 * 24 + 15) & ~(size_t)15;
@@ -135,8 +141,22 @@ __host__ __device__ constexpr size_t cand_bytes(int lpc) {
 // column of its cell, each lane starts at a rotated 16-byte offset so the
 // lanes' reads spread over the banks.
 constexpr size_t kAccBytes = 9 * 3 * 32 * sizeof(double) + 9 * 32 * sizeof(uint64_t);
+// Aligned runs of the final pass are staged by cp.async into a per-lane
+// double buffer in shared memory instead of a register prefetch (cellbench,
+// 256 C1 frames: 0.469 -> 0.455 ms); the accumulating pass keeps the
+// register prefetch (its shared memory already holds the accumulators, and
+// staging measured no better there).
+#ifndef SPX_CPA
+#define SPX_CPA 1
+#endif
+#ifndef SPX_CPA_ACC
+#define SPX_CPA_ACC 0
+#endif
+__host__ __device__ constexpr bool cpa_on(bool acc) { return acc ? SPX_CPA_ACC : SPX_CPA; }
+// cp.async run staging: [2 buffers][3 channels][32 lanes] float4
+constexpr size_t kStageBytes = 2 * 3 * 32 * 16;
 __host__ __device__ constexpr size_t warp_smem(int lpc, bool acc) {
-  return cand_bytes(lpc) + (acc ? kAccBytes : 0);
+  return cand_bytes(lpc) + (acc ? kAccBytes : 0) + (cpa_on(acc) ? kStageBytes : 0);
 }
 
 // Work unit: a group of CPW = 32 / LPC cells of one frame; a warp walks
@@ -151,7 +171,7 @@ __host__ __device__ constexpr size_t warp_smem(int lpc, bool acc) {
 // are loaded and stored one by one and the pixels past the cell (or image)
 // edge are masked out of the labels, the certificate and the sums.
 template <bool ACC, int LPC, bool AL>
-__global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
+__global__ void __launch_bounds__(128, ACC ? SPX_MINB : SPX_MINB_FIN) k_cell(CellParams p) {
   constexpr int CPW = 32 / LPC;
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -172,6 +192,8 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
   double* accd = reinterpret_cast<double*>(wbase + cand_bytes(LPC));
   unsigned long long* acci =
       reinterpret_cast<unsigned long long*>(wbase + cand_bytes(LPC) + 9 * 3 * 32 * sizeof(double));
+  constexpr bool CPA = AL && cpa_on(ACC);
+  float4* stage = reinterpret_cast<float4*>(wbase + cand_bytes(LPC) + (ACC ? kAccBytes : 0));
 
   const long long hw = (long long)p.h * p.w, pl = p.plane;
   const float* fimg = p.img + (long long)f * 3 * pl;
@@ -185,6 +207,16 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
   };
   // valid pixels of the run starting at cell column c4, image column x
   auto run_len = [&](int c4, int x) { return AL ? 4 : min(4, min(S - c4, p.w - x)); };
+  // CPA: the run's three float4 are copied into this lane's stage buffer
+  auto stage_run = [&](bool ok, int y, int x, int buf) {
+    if (!ok) return;
+    const float* q = fimg + (long long)y * p.w + x;
+    float4* d = stage + buf * 96 + lane;
+    const unsigned sd = (unsigned)__cvta_generic_to_shared(d);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sd), "l"(q));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sd + 512), "l"(q + pl));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sd + 1024), "l"(q + 2 * pl));
+  };
   auto load_run = [&](bool ok, int y, int x, int nv, float4& Lx, float4& Ax, float4& Bx) {
     if (!ok) return;
     SPX_DCHECK(y >= 0 && y < p.h && x >= 0 && nv >= 1 && x + nv <= p.w);
@@ -222,7 +254,13 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
     bool ok_n = active && ll < p.runs && y_cell + row0 < p.h && x_cell + c40 < p.w;
     int row_n = row0, c4_n = c40;
     float4 Ln = make_float4(0.f, 0.f, 0.f, 0.f), An = Ln, Bn = Ln;
-    load_run(ok_n, y_cell + row0, x_cell + c40, run_len(c40, x_cell + c40), Ln, An, Bn);
+    int buf = 0;
+    if (CPA) {
+      stage_run(ok_n, y_cell + row0, x_cell + c40, 0);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    } else {
+      load_run(ok_n, y_cell + row0, x_cell + c40, run_len(c40, x_cell + c40), Ln, An, Bn);
+    }
 
     // ---- stage the 9 candidates (the cell's lanes, 9 / LPC each) --------------
     float mc = 0.f, mxy = 0.f, okf = 1.f;
@@ -273,12 +311,29 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
     for (int j = ll; j < p.runs; j += LPC) {
       const int row = row_n, c4 = c4_n;
       const bool ok = ok_n;
-      const float4 Lv = Ln, Av = An, Bv = Bn;
+      float4 Lv = Ln, Av = An, Bv = Bn;
       // prefetch the lane's next run of this cell (software pipelining)
       if (j + LPC < p.runs) {
         run_pos(j + LPC, row_n, c4_n);
         ok_n = active && y_cell + row_n < p.h && x_cell + c4_n < p.w;
-        load_run(ok_n, y_cell + row_n, x_cell + c4_n, run_len(c4_n, x_cell + c4_n), Ln, An, Bn);
+        if (CPA)
+          stage_run(ok_n, y_cell + row_n, x_cell + c4_n, buf ^ 1);
+        else
+          load_run(ok_n, y_cell + row_n, x_cell + c4_n, run_len(c4_n, x_cell + c4_n), Ln, An, Bn);
+      }
+      if (CPA) {
+        // this run's copies (the group before the one just issued) are done;
+        // the buffer the next run is copied into was read by the previous
+        // iteration, whose values are consumed by now
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        const float4* sb = stage + buf * 96 + lane;
+        if (ok) {
+          Lv = sb[0];
+          Av = sb[32];
+          Bv = sb[64];
+        }
+        buf ^= 1;
       }
       if (!ok) continue;
       const int y = y_cell + row, x = x_cell + c4;
@@ -301,6 +356,8 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
       const float yr = (float)row;
       unsigned k1[4] = {0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu};
       unsigned k2[4] = {0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu, 0x7F7FFFFFu};
+      unsigned kp[4];  // SPX_PAIRMIN: the first key of a candidate pair
+      (void)kp;
       const float w32 = p.w32;
 #pragma unroll
       for (int t = 0; t < 9; ++t) {
@@ -332,8 +389,23 @@ __global__ void __launch_bounds__(128, SPX_MINB) k_cell(CellParams p) {
           // D = sqrt(q) + w * sqrt(r) (MUFU.SQRT; error bound in DESIGN.md)
           const float d = __fmaf_rn(w32, sqa(R[i]), sqa(Q[i]));
           const unsigned key = (__float_as_uint(d) & ~15u) | (unsigned)t;
+#if SPX_PAIRMIN
+          // candidate 0 seeds the best key; later candidates merge in pairs:
+          // the two smallest of {k1 <= k2} u {lo <= hi} are min(k1, lo) and
+          // min(max(k1, lo), k2, hi) -- 5 min/max per 2 candidates, not 6
+          if (t == 0) {
+            k1[i] = key;
+          } else if (t & 1) {
+            kp[i] = key;
+          } else {
+            const unsigned lo = min(kp[i], key), hi = max(kp[i], key);
+            k2[i] = min(min(k2[i], hi), max(k1[i], lo));
+            k1[i] = min(k1[i], lo);
+          }
+#else
           k2[i] = min(k2[i], max(k1[i], key));
           k1[i] = min(k1[i], key);
+#endif
         }
       }
       // certificate for the 4 pixels; uncertain ones (rare) take the exact path

@@ -262,13 +262,42 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
     pf = g / gpf;
     pr = (g - pf * gpf) << 2;
   }
+  // source pixel index (HWC, flat) of a group's first pixel, its end, and
+  // whether the group takes the 12-byte vector load
+  auto group = [&](int64_t gg, int64_t f_, int64_t r_, int64_t& q_, int64_t& qe_) {
+    q_ = PLANAR ? f_ * hw + r_ : gg << 2;
+    qe_ = PLANAR ? f_ * hw + hw : p1;
+    return vec && q_ >= p0 && q_ + 4 <= qe_ && (!PLANAR || ((q_ * 3) & 3) == 0);
+  };
+  // the next group's 12 bytes are loaded one iteration ahead (software
+  // pipelining: the loads' latency overlaps this group's binary64 work)
+  int64_t nq, nqe;
+  bool nvec = g < g1 && group(g, pf, pr, nq, nqe);
+  uint32_t n0 = 0, n1 = 0, n2 = 0;
+  if (nvec) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(rgb + nq * 3);
+    n0 = __ldg(src), n1 = __ldg(src + 1), n2 = __ldg(src + 2);
+  }
   for (; g < g1; g += stride) {
-    // source pixel index (HWC, flat) of the group's first pixel, and its end
-    const int64_t q = PLANAR ? pf * hw + pr : g << 2;
-    const int64_t qe = PLANAR ? pf * hw + hw : p1;
-    if (vec && q >= p0 && q + 4 <= qe && (!PLANAR || ((q * 3) & 3) == 0)) {
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(rgb + q * 3);
-      uint32_t w0 = __ldg(src), w1 = __ldg(src + 1), w2 = __ldg(src + 2);
+    const int64_t q = nq, qe = nqe;
+    const bool isvec = nvec;
+    const uint32_t w0 = n0, w1 = n1, w2 = n2;
+    {  // prefetch group g + stride (frame / offset advanced as below)
+      int64_t f2 = pf, r2 = pr;
+      if (PLANAR) {
+        r2 += stride << 2;
+        while (r2 >= gpf << 2) {
+          r2 -= gpf << 2;
+          ++f2;
+        }
+      }
+      nvec = g + stride < g1 && group(g + stride, f2, r2, nq, nqe);
+      if (nvec) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(rgb + nq * 3);
+        n0 = __ldg(src), n1 = __ldg(src + 1), n2 = __ldg(src + 2);
+      }
+    }
+    if (isvec) {
       uint8_t c[12];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
