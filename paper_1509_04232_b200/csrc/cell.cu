@@ -578,6 +578,7 @@ struct ReduceParams {
   int h, w, s, ns_r, ns_c, frames, n_bl, tile_len;
   long long plane;         // planar Lab channel stride (plane_of(h * w))
   bool win_staged;         // k_exact_clusters stages the label window in smem
+  float tau_strip;         // k_exact_wide: certified range of one strip's members
   int kr0, kr1;            // cluster rows reduced (local grid)
   int row_off;             // global cell row of local row 0
 };
@@ -997,14 +998,22 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
 }
 
 // Exact recomputation for large cells (S > 32), where most clusters are
-// flagged (the certified range 2^k <= |v| < 128 narrows as 9 S^2 grows) and
-// a strip holds thousands of members.  One block of kWideWarps warps per
-// cluster, warp w folding strips w, w + kWideWarps, ...; a strip is walked
-// in row-major units of (row, 256 columns): the unit's labels and Lab
-// values are loaded coalesced (8 per lane, the next unit's loads in flight
-// while this one is folded), members found by ballot, and lanes 0..2 fold
-// channel 0..2 of each member in order, the values arriving by shuffle.
+// flagged (the certified range 2^k <= |v| < 128 narrows as 9 S^2 grows).
+// One block of kWideWarps warps per cluster, warp w taking strips w,
+// w + kWideWarps, ... (an independent reference fold each,
+// _core.pyx:233-243).  A strip has at most tile_len * 3S members, so a much
+// wider range is certified per strip: if every member value of a channel is
+// 0 or tau_strip <= |v| < 128 (tau_strip = 2^k with tile_len * 3S <=
+// 2^(23+k)), every partial sum of that channel is exact and the strip's
+// fold equals any-order sum -- lanes accumulate their members in binary64
+// and the warp adds the lane sums.  Only channels with an uncertified member
+// (rare) are refolded sequentially: row-major units of 256 columns, labels
+// and values loaded coalesced, members found by ballot, lanes 0..2 folding
+// in order with the values arriving by shuffle.
 constexpr int kWideWarps = 8;
+// kWideCh: 32-column chunks per unit (8, 12 or 16 by window width, so a
+// window row of up to 512 columns is one unit)
+template <int kWideCh>
 __global__ void __launch_bounds__(kWideWarps * 32) k_exact_wide(ReduceParams p) {
   __shared__ double strips[kExMaxStrips][6];
   __shared__ double qv[6];
@@ -1012,6 +1021,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_exact_wide(ReduceParams p) 
   const int K = p.ns_r * p.ns_c;
   const long long hw = (long long)p.h * p.w;
   const int n = *p.worklist_n;
+  const unsigned tau_bits = __float_as_uint(p.tau_strip);
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
     const int gk = p.worklist[item];
     const int ff = gk / K, fk = gk - ff * K;
@@ -1022,7 +1032,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_exact_wide(ReduceParams p) 
     const int gid = fk + p.row_off * p.ns_c;
     const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
     const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
-    const int nseg = (wx1 - wx0 + 255) >> 8;
+    const int nseg = (wx1 - wx0 + 32 * kWideCh - 1) / (32 * kWideCh);
     SPX_DCHECK(gk >= 0 && gk < p.frames * K && p.n_bl <= kExMaxStrips && wx1 > wx0);
 #pragma unroll 1
     for (int i = threadIdx.x; i < p.n_bl * 6; i += blockDim.x) (&strips[0][0])[i] = 0.0;
@@ -1033,56 +1043,59 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_exact_wide(ReduceParams p) 
       const int yz = min(ry0 + (j + 1) * p.tile_len, ry1);
       if (ya >= yz) continue;  // warp-uniform
       const int units = (yz - ya) * nseg;
-      double acc = 0.0;
+      auto unit_xy = [&](int u, int& y, int& x0) {
+        y = ya + u / nseg;
+        x0 = wx0 + (u % nseg) * 32 * kWideCh + lane;
+      };
+      // ---- pass 1: lane sums of the members (exact if certified) ---------
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      unsigned bad = 0;  // channels with an uncertified member (bits 0..2)
       unsigned long long lx = 0, ly = 0, lc = 0;
-      int lb_n[8];
-      float l_n[8], a_n[8], b_n[8];
-      auto load = [&](int u) {
-        const int y = ya + u / nseg, x0 = wx0 + (u % nseg) * 256 + lane;
+      int lb_n[kWideCh];
+      auto load_labels = [&](int u) {
+        int y, x0;
+        unit_xy(u, y, x0);
         const long long row = (long long)y * p.w;
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
+        for (int ch = 0; ch < kWideCh; ++ch) {
           const int x = x0 + 32 * ch;
-          const bool v = x < wx1;
-          lb_n[ch] = v ? __ldg(lb + row + x) : -1;
-          l_n[ch] = v ? __ldg(im + row + x) : 0.f;
-          a_n[ch] = v ? __ldg(im + p.plane + row + x) : 0.f;
-          b_n[ch] = v ? __ldg(im + 2 * p.plane + row + x) : 0.f;
+          lb_n[ch] = x < wx1 ? __ldg(lb + row + x) : -1;
         }
       };
-      load(0);
+      auto cert = [&](float v) {  // 0, or tau_strip <= |v| < 128
+        const unsigned a = __float_as_uint(v) & 0x7FFFFFFFu;
+        return a == 0u || (a >= tau_bits && a < 0x43000000u);
+      };
+      load_labels(0);
 #pragma unroll 1
       for (int u = 0; u < units; ++u) {
-        int lbv[8];
-        float lv[8], av[8], bv[8];
+        int lbv[kWideCh];
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          lbv[ch] = lb_n[ch];
-          lv[ch] = l_n[ch];
-          av[ch] = a_n[ch];
-          bv[ch] = b_n[ch];
-        }
-        if (u + 1 < units) load(u + 1);
-        const int y = ya + u / nseg, x0 = wx0 + (u % nseg) * 256 + lane;
+        for (int ch = 0; ch < kWideCh; ++ch) lbv[ch] = lb_n[ch];
+        if (u + 1 < units) load_labels(u + 1);  // the next unit's labels in flight
+        int y, x0;
+        unit_xy(u, y, x0);
+        const long long row = (long long)y * p.w;
         const unsigned long long yg = (unsigned long long)(y + p.row_off * p.s);
+        float lv[kWideCh], av[kWideCh], bv[kWideCh];
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
+        for (int ch = 0; ch < kWideCh; ++ch) {  // member values only (one read per pixel)
           const bool hit = lbv[ch] == gid;
-          unsigned m = __ballot_sync(0xFFFFFFFFu, hit);
-          if (hit) {
+          const long long o = row + x0 + 32 * ch;
+          lv[ch] = hit ? fabsf(__ldg(im + o)) : 0.f;  // channel 0: |L| (flag bit)
+          av[ch] = hit ? __ldg(im + p.plane + o) : 0.f;
+          bv[ch] = hit ? __ldg(im + 2 * p.plane + o) : 0.f;
+        }
+#pragma unroll
+        for (int ch = 0; ch < kWideCh; ++ch) {
+          if (lbv[ch] == gid) {
+            s0 = dadd(s0, (double)lv[ch]);
+            s1 = dadd(s1, (double)av[ch]);
+            s2 = dadd(s2, (double)bv[ch]);
+            bad |= (cert(lv[ch]) ? 0u : 1u) | (cert(av[ch]) ? 0u : 2u) | (cert(bv[ch]) ? 0u : 4u);
             lx += (unsigned long long)(x0 + 32 * ch);
             ly += yg;
             ++lc;
-          }
-          while (m) {  // warp-uniform: members in column order
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            const float v0 = __shfl_sync(0xFFFFFFFFu, lv[ch], b);
-            const float v1 = __shfl_sync(0xFFFFFFFFu, av[ch], b);
-            const float v2 = __shfl_sync(0xFFFFFFFFu, bv[ch], b);
-            // channel 0 carries the certified-sum flag in its sign bit
-            const float v = lane == 0 ? fabsf(v0) : (lane == 1 ? v1 : v2);
-            if (lane < 3) acc = dadd(acc, (double)v);
           }
         }
       }
@@ -1091,6 +1104,43 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_exact_wide(ReduceParams p) 
         lx += __shfl_xor_sync(0xFFFFFFFFu, lx, o);
         ly += __shfl_xor_sync(0xFFFFFFFFu, ly, o);
         lc += __shfl_xor_sync(0xFFFFFFFFu, lc, o);
+        s0 = dadd(s0, __shfl_xor_sync(0xFFFFFFFFu, s0, o));
+        s1 = dadd(s1, __shfl_xor_sync(0xFFFFFFFFu, s1, o));
+        s2 = dadd(s2, __shfl_xor_sync(0xFFFFFFFFu, s2, o));
+        bad |= __shfl_xor_sync(0xFFFFFFFFu, bad, o);
+      }
+      // ---- pass 2 (uncertified channels): the reference's ordered fold ----
+      double acc = lane == 0 ? s0 : (lane == 1 ? s1 : s2);
+      if (bad) {  // warp-uniform
+        const bool mine = lane < 3 && (bad >> lane & 1u);
+        if (mine) acc = 0.0;
+#pragma unroll 1
+        for (int u = 0; u < units; ++u) {
+          int y, x0;
+          unit_xy(u, y, x0);
+          const long long row = (long long)y * p.w;
+#pragma unroll 1
+          for (int ch = 0; ch < kWideCh; ++ch) {
+            const int x = x0 + 32 * ch;
+            const bool hit = x < wx1 && __ldg(lb + row + x) == gid;
+            unsigned m = __ballot_sync(0xFFFFFFFFu, hit);
+            float v0 = 0.f, v1 = 0.f, v2 = 0.f;
+            if (hit) {
+              v0 = fabsf(__ldg(im + row + x));
+              v1 = __ldg(im + p.plane + row + x);
+              v2 = __ldg(im + 2 * p.plane + row + x);
+            }
+            while (m) {  // warp-uniform: members in column order
+              const int b = __ffs(m) - 1;
+              m &= m - 1;
+              const float w0 = __shfl_sync(0xFFFFFFFFu, v0, b);
+              const float w1 = __shfl_sync(0xFFFFFFFFu, v1, b);
+              const float w2 = __shfl_sync(0xFFFFFFFFu, v2, b);
+              const float v = lane == 0 ? w0 : (lane == 1 ? w1 : w2);
+              if (mine) acc = dadd(acc, (double)v);
+            }
+          }
+        }
       }
       if (lane < 3) strips[j][lane] = acc;
       if (lane == 0) {
@@ -1104,8 +1154,6 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_exact_wide(ReduceParams p) 
     __syncthreads();  // strips are reused by the next item
   }
 }
-
-
 
 }  // namespace
 
@@ -1273,6 +1321,11 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   p.frames = frames;
   p.plane = plane_of(h * w);
   p.win_staged = exact_win_staged(s);
+  {  // a strip holds <= tile_len * 3S members: tau = 2^k, tile_len*3S <= 2^(23+k)
+    int k = -23;
+    while ((double)tile_len * 3.0 * (double)s > std::ldexp(1.0, 23 + k)) ++k;
+    p.tau_strip = (float)std::ldexp(1.0, k);
+  }
   p.n_bl = (int)ceil_div(3 * s, tile_len);
   p.tile_len = (int)tile_len;
   if (kr1 < 0) kr1 = ns_r;
@@ -1296,7 +1349,13 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
     // large cells: most clusters are flagged, one block per cluster
     const long long wb = std::max<long long>(
         1, std::min<long long>((long long)num_sms() * 8, nk * frames));
-    k_exact_wide<<<(unsigned)wb, kWideWarps * 32, 0, st>>>(p);
+    const int64_t ww = std::min<int64_t>(3 * s, w);
+    if (ww <= 256)
+      k_exact_wide<8><<<(unsigned)wb, kWideWarps * 32, 0, st>>>(p);
+    else if (ww <= 384)
+      k_exact_wide<12><<<(unsigned)wb, kWideWarps * 32, 0, st>>>(p);
+    else
+      k_exact_wide<16><<<(unsigned)wb, kWideWarps * 32, 0, st>>>(p);
     SPX_LAUNCH_CHECK("k_exact_wide");
     return SPX_OK;
   }
