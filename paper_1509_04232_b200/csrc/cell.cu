@@ -1,27 +1,33 @@
 // cell.cu -- the engine's fused association + centre-update path.
 //
 // Work unit: one grid cell (S x S pixels).  All pixels of a cell share the
-// same 9 candidate centres, so a warp (or half-warp for S = 8) loads them once
-// into registers and streams the cell's pixels in runs of 4 (three 128-bit
-// loads of HWC Lab per run).  Distances are evaluated two pixels at a time
-// with Blackwell's packed FFMA2/FADD2/FMUL2, square roots on MUFU.RSQ, and
-// the same rigorous fp32 -> binary64 argmin certificate as assoc.cu (uncertain
-// pixels are re-evaluated with the reference's exact binary64 order).
+// same 9 candidate centres, so the cell's LPC lanes (4, 8, 16 or 32 by S)
+// stage the 9 fp32 candidate records in shared memory and stream the cell's
+// pixels in runs of 4 (one 128-bit load per planar Lab channel; the final
+// pass stages its runs with cp.async).  Distances are evaluated two pixels
+// at a time with Blackwell's packed FFMA2/FADD2/FMUL2 (the candidate as a
+// broadcast scalar operand), square roots with MUFU (sqrt.approx.ftz), and a
+// rigorous fp32 -> binary64 argmin certificate: pixels whose best and
+// second-best keys are closer than the error bound are re-evaluated with the
+// reference's exact binary64 order.
 //
-// With ACC the kernel also produces the centre-update partial sums for every
-// (cell, candidate slot): the run's slot nibbles and Lab values are staged in
-// shared memory and 9 (or 27) "owner" lanes fold them per slot in binary64
-// (colour) and int32 (x, y, count).  The reduce kernel adds the 9 partials of
-// each cluster in a fixed order.
+// With ACC the kernel also produces the centre update: each lane adds its
+// pixels' colour (binary64) and packed x / y / count / flag counters
+// (integer) into lane-private per-slot accumulators in shared memory; at the
+// end of a cell the LPC lane entries of each slot are summed and added to
+// the cluster's ClusterAcc with global atomics (f64 atomicAdd for colour).
 //
-// Exactness of the sums: the reference folds the
-// colour sums left-to-right in binary64 (_core.pyx:233-243).  If every member
-// value v of a cluster is 0 or has 2^-tau_exp <= |v| < 128, every partial sum
-// of any subset of the cluster is an exact binary64 number (members are
-// multiples of ulp(2^tau) and |sum| < count * 128 <= 2^53 ulp), so the
-// reference's fold, its strip tree, and our fixed-order sum all equal the
-// exact sum.  Pixels outside that range set a flag bit; the reduce kernel
-// recomputes flagged clusters with the reference's exact strip fold.
+// Determinism / exactness of the sums: the
+// reference folds each strip's colour values left to right in binary64 and
+// combines strips with a pairwise tree (_core.pyx:233-311).  If every member
+// value v of a cluster is 0 or has 2^k <= |v| < 128 with 9 S^2 <= 2^(23+k),
+// every partial sum of any subset of the cluster is an exact binary64 number,
+// so the reference's fold, its tree and ANY order of our lane sums and
+// atomics give the same (exact) result -- the atomics' order cannot matter.
+// Pixels outside that range carry a flag (sign bit of Lab channel 0, set by
+// the engine's convert); a cluster with a flagged member is queued and
+// recomputed by k_exact_clusters (S <= 32) / k_exact_wide (S > 32) with the
+// reference's strip folds and tree.  k_reduce_cells divides the exact sums.
 #include <algorithm>
 #include <atomic>
 #include <cmath>

@@ -92,7 +92,7 @@ struct Engine {
   // is a child Engine (own buffers, worklist, side stream, events) created on
   // first use; frames are independent, so the results are bitwise the same
   // as the unsplit call (tests/test_gpu_engine.py).  Measured on C1, 256
-  // frames (tools/lanes_probe.py): 1 lane 4.59 ms, 2: 4.56, 3: 4.40, 4: 4.32,
+  // frames (tools/probe.py lanes): 1 lane 4.59 ms, 2: 4.56, 3: 4.40, 4: 4.32,
   // 5: 4.67, 6: 4.48, 8: 4.44.  Staggering the lanes (lane i starting after
   // lane i-1's convert) measured 1% slower at 4 lanes, and stream priorities
   // by lane (either order) 7% slower: the gain needs the lanes to co-run.
@@ -110,7 +110,7 @@ struct Engine {
   int lanes_for(int64_t batch) const {
     if (batch < 2 || (lanes_req == 0 && lanes_off)) return 1;
     int64_t l = lanes_req;
-    if (l == 0) {  // auto (tools/lanes_probe.py; eager VGA calls: 32 frames ->
+    if (l == 0) {  // auto (tools/probe.py lanes; eager VGA calls: 32 frames ->
                    // 3 lanes +37%, 64 -> 3 lanes +23%, 128 -> 4 lanes +13%,
                    // 256 -> 4 lanes +6%; 3 lanes remain for eager calls < 24 Mpx)
       // graph-replayed calls (<= kGraphMaxBatch frames) split too: the

@@ -274,14 +274,22 @@ class SegEngine:
         _lib.check(self._lib.spx_engine_wait(self._h), "wait")
         self._pending.clear()
 
-    def last_timing(self):
-        """Per-stage device times (seconds) of the last call, batch-wide."""
-        t = _lib.SpxTiming()
+    def last_timing(self, max_updates=None):
+        """Per-stage device times (seconds) of the last call, batch-wide
+        (`max_updates`: keep only that many update passes and one more
+        association, the passes a given frame ran)."""
+        t = self.__dict__.get("_timing_buf")
+        if t is None:
+            t = self._timing_buf = _lib.SpxTiming()
         _lib.check(self._lib.spx_engine_timing(self._h, ctypes.byref(t)), "timing")
         ms = 1e-3
+        na, nu = t.n_associate, t.n_update
+        if max_updates is not None:
+            nu = min(nu, max_updates)
+            na = min(na, max_updates + 1)
         return StageTiming(convert=t.convert * ms, init=t.init * ms, perturb=t.perturb * ms,
-                           associate=tuple(t.associate[i] * ms for i in range(t.n_associate)),
-                           update=tuple(t.update[i] * ms for i in range(t.n_update)),
+                           associate=tuple(v * ms for v in t.associate[:na]),
+                           update=tuple(v * ms for v in t.update[:nu]),
                            connectivity=t.connectivity * ms, total=t.total * ms)
 
     def last_launches(self):
@@ -355,14 +363,12 @@ class SegEngine:
         pin = self._pinned_input(1)
         np.copyto(pin[0], img.data)
         outs = self._pinned_outputs(1)
-        p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
-        _lib.check(self._lib.spx_engine_segment_host(self._h, p(pin), 1, *(p(a) for a in outs)),
-                   "segment")
+        rc = self._lib.spx_engine_segment_host(self._h, pin.ctypes.data, 1,
+                                               *(a.ctypes.data for a in outs))
+        if rc:
+            _lib.check(rc, "segment")
         labels, cxy, clab, counts, passes = outs
-        n_up = int(passes[0])
-        tm = self.last_timing()
-        tm = StageTiming(tm.convert, tm.init, tm.perturb, tm.associate[:n_up + 1],
-                         tm.update[:n_up], tm.connectivity, tm.total)
+        tm = self.last_timing(max_updates=int(passes[0]))
         return SegResult(labels=LabelMap._trusted(labels[0]),
                          spixel_map=SuperpixelMap(self.grid, cxy[0], clab[0], counts[0]),
                          timing=tm)
