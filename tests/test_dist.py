@@ -81,10 +81,28 @@ def _strip_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    bufs = [[torch.full((5,), 100.0 * rank + 1), torch.zeros(5)],
-            [torch.full((5,), 100.0 * rank + 2), torch.zeros(5)]]
-    DistComm(rank, world).exchange_buffers(bufs)
-    q.put((rank, float(bufs[0][1][0]), float(bufs[1][1][0])))
+
+    class FakeStrip:  # the exchange only needs the buffers and pack / unpack
+        def __init__(self):
+            self.centres = [[torch.full((5,), 100.0 * rank + 1), torch.zeros(5)],
+                            [torch.full((5,), 100.0 * rank + 2), torch.zeros(5)]]
+            self.labels = [[torch.full((3,), 10.0 * rank + 3), torch.zeros(3)],
+                           [torch.full((3,), 10.0 * rank + 4), torch.zeros(3)]]
+            self.packed, self.unpacked = [], []
+
+        def pack(self, what):
+            self.packed.append(what)
+
+        def unpack(self, what):
+            self.unpacked.append(what)
+
+    st = FakeStrip()
+    comm = DistComm(rank, world, st)
+    h = comm.start(["centres", "labels"])  # both exchanges in flight at once
+    comm.finish(h)
+    assert st.packed == ["centres", "labels"] and st.unpacked == ["centres", "labels"]
+    q.put((rank, float(st.centres[0][1][0]), float(st.centres[1][1][0]),
+           float(st.labels[0][1][0]), float(st.labels[1][1][0])))
     dist.destroy_process_group()
 
 
@@ -100,7 +118,9 @@ def test_strip_neighbour_exchange(world):
         p.join(120)
         assert p.exitcode == 0
     res = sorted(q.get(timeout=10) for _ in range(world))
-    for rank, from_up, from_down in res:
+    for rank, from_up, from_down, lab_up, lab_down in res:
         # from_up = the upper rank's "send down" (100*(r-1)+2); from_down = lower's "send up"
         assert from_up == (100.0 * (rank - 1) + 2 if rank > 0 else 0.0)
         assert from_down == (100.0 * (rank + 1) + 1 if rank < world - 1 else 0.0)
+        assert lab_up == (10.0 * (rank - 1) + 4 if rank > 0 else 0.0)
+        assert lab_down == (10.0 * (rank + 1) + 3 if rank < world - 1 else 0.0)
