@@ -354,9 +354,13 @@ struct Engine {
   // Stage-timing event record.  During capture the external flag turns it
   // into an event-record node of the graph (each replay records the event);
   // otherwise it is an ordinary record.
+  // Captured graphs hold no event nodes (SPX_GRAPH_EVENTS=1 restores the
+  // start / end nodes): a replay's total comes from ordinary records on the
+  // caller's stream around cudaGraphLaunch.
   void stage_mark(cudaEvent_t e, cudaStream_t s) {
     if (capturing) {
-      if (e != ev[EV_START] && e != ev[EV_END]) return;
+      static const bool nodes = getenv("SPX_GRAPH_EVENTS") != nullptr;
+      if (!nodes || (e != ev[EV_START] && e != ev[EV_END])) return;
       cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
     } else {
       cudaEventRecord(e, s);
@@ -480,7 +484,10 @@ struct Engine {
       g->n_update = n_update;
       g->launches = launches;
     }
+    static const bool nodes = getenv("SPX_GRAPH_EVENTS") != nullptr;
+    if (!nodes) SPX_CUDA(cudaEventRecord(ev[EV_START], s));
     SPX_CUDA(cudaGraphLaunch(g->exec, s));
+    if (!nodes) SPX_CUDA(cudaEventRecord(ev[EV_END], s));
     n_assoc = g->n_assoc;
     n_update = g->n_update;
     launches = g->launches;
@@ -575,6 +582,22 @@ struct Engine {
       }
     }
     stage_mark(ev[EV_CONN0], s);
+    // Final centres: frame f ends in buffer passes[f] & 1 (ping-pong,
+    // engine.py:197; without early stop every frame ran no_iters passes).
+    // The same launch writes the per-frame pass counts.  It only needs the
+    // finished update passes, so on the cell path it runs on the side stream
+    // beside the connectivity pass (joined before the end event).
+    cudaStream_t sg = use_cell ? s_side : s;
+    if (use_cell) {
+      SPX_CUDA(cudaEventRecord(ev_fork, s));
+      SPX_CUDA(cudaStreamWaitEvent(s_side, ev_fork, 0));
+    }
+    k_gather_centres<<<(unsigned)ceil_div(K * B, 256), 256, 0, sg>>>(
+        cxy[0], clab[0], cxy[1], clab[1], early ? passes : nullptr, early ? -1 : (int)st.no_iters,
+        K, B, out_xy, out_lab, out_passes);
+    SPX_LAUNCH_CHECK("k_gather_centres");
+    ++launches;
+    if (use_cell) SPX_CUDA(cudaEventRecord(ev_join, s_side));
     if (st.connectivity == 1) {
       if ((rc = launch_weak2(labels, out_labels, st.height, st.width, B, s, 0, -1))) return rc;
       ++launches;
@@ -589,15 +612,8 @@ struct Engine {
       SPX_CUDA(cudaMemcpyAsync(out_labels, labels, (size_t)B * hw * sizeof(int32_t),
                                cudaMemcpyDeviceToDevice, s));
     }
+    if (use_cell) SPX_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
     stage_mark(ev[EV_END], s);
-    // Final centres: frame f ends in buffer passes[f] & 1 (ping-pong,
-    // engine.py:197; without early stop every frame ran no_iters passes).
-    // The same launch writes the per-frame pass counts.
-    k_gather_centres<<<(unsigned)ceil_div(K * B, 256), 256, 0, s>>>(
-        cxy[0], clab[0], cxy[1], clab[1], early ? passes : nullptr, early ? -1 : (int)st.no_iters,
-        K, B, out_xy, out_lab, out_passes);
-    SPX_LAUNCH_CHECK("k_gather_centres");
-    ++launches;
     return SPX_OK;
   }
 
@@ -803,12 +819,14 @@ struct Engine {
         SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_h2d[sl], 0));
         if (seq >= kSlots) SPX_CUDA(cudaStreamWaitEvent(s_comp, ev_d2h[sl], 0));
       }
-      if (c == 0) SPX_CUDA(cudaEventRecord(sr.a, s_comp));
+      // (a synchronous one-stream call needs no events: the host waits for
+      // it before any later submission can reuse the slot)
+      if (c == 0 && !one_stream) SPX_CUDA(cudaEventRecord(sr.a, s_comp));
       mark(s_comp);
       if ((rc = segment(h_rgb[sl], nb, d_lab, d_xy, d_cl, d_cnt, d_pass, s_comp))) return rc;
       mark(s_comp);
-      if (c == nchunks - 1) SPX_CUDA(cudaEventRecord(sr.b, s_comp));
-      SPX_CUDA(cudaEventRecord(ev_comp[sl], s_comp));
+      if (c == nchunks - 1 && !one_stream) SPX_CUDA(cudaEventRecord(sr.b, s_comp));
+      if (!one_stream) SPX_CUDA(cudaEventRecord(ev_comp[sl], s_comp));
       if (!one_stream) SPX_CUDA(cudaStreamWaitEvent(s_d2h, ev_comp[sl], 0));
       mark(q_d2h);
       if (host_block) {
@@ -831,10 +849,12 @@ struct Engine {
                                    q_d2h));
       }
       mark(q_d2h);
-      SPX_CUDA(cudaEventRecord(ev_d2h[sl], q_d2h));
+      if (!one_stream) SPX_CUDA(cudaEventRecord(ev_d2h[sl], q_d2h));
     }
-    sr.ticket = seq;
-    ++n_subs;
+    if (!one_stream) {
+      sr.ticket = seq;
+      ++n_subs;
+    }
     last_sync = one_stream;
     return SPX_OK;
   }
