@@ -44,13 +44,14 @@ def frame(rng, kind, h, w):
 
 
 def case(rng):
-    h, w = int(rng.integers(6, 420)), int(rng.integers(6, 560))
-    if rng.random() < 0.7:  # mostly shapes the fused path takes (h*w % 4 == 0)
-        w += (-w) % 4 if rng.random() < 0.5 else 0
-        if (h * w) % 4:
-            h += 4 - (h * w) % 4 if (h * w) % 2 == 0 else 0
+    big = rng.random() < 0.15  # large cells (S > 32: k_exact_wide, 16/32 lanes per cell)
+    h, w = int(rng.integers(6, 900 if big else 420)), int(rng.integers(6, 900 if big else 560))
+    if rng.random() < 0.5:  # half the shapes 128-bit aligned (W % 4 == 0), half anything
+        w += (-w) % 4
     kw = {}
-    if rng.random() < 0.5:
+    if big:
+        kw["spixel_size"] = int(rng.integers(33, 161))
+    elif rng.random() < 0.5:
         kw["spixel_size"] = int(rng.integers(2, 41))
     else:
         kw["num_superpixels"] = int(rng.integers(1, max(2, h * w // 16)))
@@ -72,7 +73,7 @@ def case(rng):
     except spx.SuperpixError:
         return None
     kinds = ["noise", "gray", "smooth", "dark", "flat", "stripes"]
-    b = int(rng.integers(1, 6))
+    b = int(rng.integers(1, 3 if big else 6))
     frames = np.stack([frame(rng, kinds[int(rng.integers(0, len(kinds)))], h, w) for _ in range(b)])
     return st, frames
 
@@ -80,6 +81,7 @@ def case(rng):
 def check(st, frames):
     g = spx.compute_grid(st)
     eng = spx.SegEngine(st, max_batch=frames.shape[0])
+    check.fused += eng.fused_path
     labels, cxy, clab, counts, passes = eng.segment_host(frames)
     conn = 0 if not st.do_enforce_connectivity else (
         2 if st.connectivity_mode is spx.ConnectivityMode.STRICT else 1)
@@ -96,6 +98,9 @@ def check(st, frames):
         if not ok:
             bad.append((i, int((labels[i] != ol).sum())))
     return bad
+
+
+check.fused = 0
 
 
 def main():
@@ -116,8 +121,8 @@ def main():
         if bad:
             fails += 1
             print(f"MISMATCH {st} frames {frames.shape} bad {bad}", flush=True)
-    print(f"fuzz: {n} cases, {frames_total} frames, {fails} failing cases "
-          f"({time.time() - t0:.0f} s)", flush=True)
+    print(f"fuzz: {n} cases ({check.fused} on the fused cell path), {frames_total} frames, "
+          f"{fails} failing cases ({time.time() - t0:.0f} s)", flush=True)
     sys.exit(1 if fails else 0)
 
 
