@@ -124,3 +124,64 @@ def test_strip_neighbour_exchange(world):
         assert from_down == (100.0 * (rank + 1) + 1 if rank < world - 1 else 0.0)
         assert lab_up == (10.0 * (rank - 1) + 4 if rank > 0 else 0.0)
         assert lab_down == (10.0 * (rank + 1) + 3 if rank < world - 1 else 0.0)
+
+
+def test_strip_schedule_overlaps_and_stops_early():
+    """strips._run issues each exchange before the compute that does not need
+    it and waits for it only before the compute that does; with early stop it
+    ends after the first update whose shift is below the threshold, with one
+    last association (engine.py:196-200).  Fake strips / comm record the
+    order (no GPU)."""
+    from paper_1509_04232_b200 import Settings
+    from paper_1509_04232_b200.strips import BOUNDARY, INTERIOR, _run
+
+    log = []
+
+    class FakeStrip:
+        def __init__(self, settings):
+            self.settings = settings
+
+        def associate(self, with_update, part):
+            log.append(("assoc", with_update, "interior" if part == INTERIOR else "boundary"))
+
+        def update(self, part):
+            log.append(("update", "interior" if part == INTERIOR else "boundary"))
+
+    class FakeComm:
+        def __init__(self, shifts):
+            self.shifts = list(shifts)
+
+        def start(self, whats):
+            log.append(("start", tuple(whats)))
+            return tuple(whats)
+
+        def finish(self, h):
+            log.append(("finish", h))
+
+        def shift(self):
+            class T:
+                def __init__(self, v):
+                    self.v = v
+
+                def item(self):
+                    return self.v
+            log.append(("shift",))
+            return T(self.shifts.pop(0))
+
+    st = Settings(img_width=64, img_height=64, spixel_size=8, no_iters=3)
+    _run([FakeStrip(st)], FakeComm([]))
+    one_iter = [("assoc", True, "interior"), ("finish", ("centres",)),
+                ("assoc", True, "boundary"), ("start", ("sums", "labels")),
+                ("update", "interior"), ("finish", ("sums", "labels")),
+                ("update", "boundary"), ("start", ("centres",))]
+    tail = [("assoc", False, "interior"), ("finish", ("centres",)),
+            ("assoc", False, "boundary"), ("start", ("labels",)), ("finish", ("labels",))]
+    assert log == [("start", ("centres",))] + one_iter * 3 + tail
+
+    log.clear()
+    st = Settings(img_width=64, img_height=64, spixel_size=8, no_iters=9,
+                  early_stop_threshold=5.0)
+    _run([FakeStrip(st)], FakeComm([9.0, 7.0, 4.0, 1.0]))
+    with_shift = one_iter[:7] + [("shift",)] + one_iter[7:]
+    # passes 1, 2 continue; pass 3's shift 4.0 < 5.0: its association is the last
+    assert log == [("start", ("centres",))] + with_shift * 3 + tail
