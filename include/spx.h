@@ -222,9 +222,11 @@ SPX_API int32_t spx_engine_timing(spx_engine *eng, spx_timing *out);
  *   labels   S * W int32        (pack after associate, unpack before update/finish)
  * Sequence: begin, xchg centres, { associate(1), xchg sums+labels, update,
  * xchg centres } x no_iters, associate(0), xchg labels, finish.
- * Results equal the single-GPU engine bit for bit.  Weak or no connectivity,
- * fused-cell geometry (4 <= S <= 255); early stop through
- * spx_strip_shift_local + spx_pairwise_sum over the gathered shifts. */
+ * Results equal the single-GPU engine bit for bit.  Fused-cell geometry
+ * (4 <= S <= 255); early stop through spx_strip_shift_local +
+ * spx_pairwise_sum over the gathered shifts.  With strict connectivity
+ * (a whole-image scan-order pass) finish returns the raw labels and the
+ * caller runs spx_strict_fill over the gathered image. */
 typedef struct spx_strip spx_strip;
 SPX_API int32_t spx_strip_create(const spx_settings *st, int64_t row_lo, int64_t row_hi,
                                  int32_t device, spx_strip **out);

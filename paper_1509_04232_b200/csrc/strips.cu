@@ -313,7 +313,8 @@ struct Strip {
     return SPX_OK;
   }
 
-  // weak connectivity on own rows; labels carry global cluster ids
+  // weak connectivity on own rows (strict: none here); labels carry global
+  // cluster ids
   int finish(int32_t* out_labels, double* out_xy, double* out_lab, int64_t* out_counts,
              cudaStream_t s) {
     SPX_CUDA(cudaSetDevice(device));
@@ -323,10 +324,10 @@ struct Strip {
     if (g.connectivity == 1) {
       if ((rc = launch_weak2(labels, out, hl, w, 1, s, oy0, oy1))) return rc;
       src = out;
-    } else if (g.connectivity != 0) {
-      set_error("row strips support weak or no connectivity (strict is sequential)");
-      return SPX_ERR_INVALID_SETTINGS;
     }
+    // connectivity 2 (strict): the raw labels; strict connectivity is a
+    // whole-image scan-order pass, which the caller runs over the gathered
+    // strips (strips.py)
     const int64_t n = (oy1 - oy0) * w;  // labels already carry global ids
     SPX_CUDA(cudaMemcpyAsync(out_labels, src + oy0 * w, n * 4, cudaMemcpyDeviceToDevice, s));
     const int64_t c = g.ns_c, no = (own1 - own0) * c;

@@ -231,6 +231,38 @@ class DistComm:
     def exchange(self, strip, what):
         self.finish(self.start([what]))
 
+    def strict_labels(self, own):
+        """Strict connectivity for row strips: the ranks' raw own-row labels
+        are gathered on rank 0, which runs the whole-image pass, and each rank
+        gets its rows back (gather + scatter of 4 B/px)."""
+        import torch
+        import torch.distributed as dist
+        st = self.strip.settings
+        g = self.strip.grid
+        plan = strip_plan(st.img_height, g.s, g.ns_r, self.world)
+        rows = [p.y_hi - p.y_lo for p in plan]
+        m = max(rows) * st.img_width
+        gloo = self._gloo()
+        dev = own.device
+        pad = torch.zeros((m,), dtype=torch.int32, device=dev)
+        pad[:own.numel()] = own.reshape(-1)
+        src = pad.cpu() if gloo else pad
+        parts = [torch.empty_like(src) for _ in range(self.world)] if self.rank == 0 else None
+        dist.gather(src, parts, dst=0, group=self.group)
+        chunks = None
+        if self.rank == 0:
+            full = torch.cat([t[:r * st.img_width] for t, r in zip(parts, rows)]).to(dev)
+            res = strict_whole_image(st, full.reshape(st.img_height, st.img_width)).reshape(-1)
+            chunks, o = [], 0
+            for r in rows:
+                c = torch.zeros((m,), dtype=torch.int32, device=dev)
+                c[:r * st.img_width] = res[o:o + r * st.img_width]
+                o += r * st.img_width
+                chunks.append(c.cpu() if gloo else c)
+        mine = torch.empty_like(src)
+        dist.scatter(mine, chunks, src=0, group=self.group)
+        return mine.to(dev)[:own.numel()].reshape(own.shape)
+
     def shift(self):
         """The whole image's centre shift: every rank's own |delta| gathered in
         rank (= cluster) order, then the same pairwise sum on every rank."""
@@ -290,8 +322,29 @@ def _run(strips, comm):
 
 
 def check_strip_settings(settings):
-    if settings.do_enforce_connectivity and settings.connectivity_mode.value == "strict":
-        raise InvalidSettingsError("row strips support weak or no connectivity")
+    """Row strips take every setting the fused engine takes (S in [4, 255],
+    ceil(3S / tile_len) <= 64); the native strip create reports the rest."""
+    slic_core.compute_grid(settings)
+
+
+def _strict(settings):
+    return settings.do_enforce_connectivity and settings.connectivity_mode.value == "strict"
+
+
+def strict_whole_image(settings, labels):
+    """Strict connectivity (_core.pyx:359-461) over a whole image's raw labels
+    (a device int32 tensor [H][W]): the scan-order component pass is global,
+    so row strips gather their raw labels and run it once (spx_strict_fill)."""
+    import torch
+    g = slic_core.compute_grid(settings)
+    min_size = settings.min_size if settings.min_size is not None else default_min_size(g.s)
+    out = torch.empty_like(labels)
+    lib = _lib.load()
+    _lib.check(lib.spx_strict_fill(_p(labels), _p(out), labels.shape[0], labels.shape[1],
+                                   int(min_size), ctypes.c_void_p(
+                                       torch.cuda.current_stream(labels.device).cuda_stream)),
+               "strict_fill")
+    return out
 
 
 def segment_strips_local(settings, rgb, n_strips, device=0):
@@ -311,8 +364,11 @@ def segment_strips_local(settings, rgb, n_strips, device=0):
         s.begin(d_rgb[s.y0:s.y0 + s.hl].contiguous())
     _run(strips, LocalComm(strips))
     outs = [s.finish() for s in strips]
+    lab = torch.cat([o[0] for o in outs])
+    if _strict(settings):
+        lab = strict_whole_image(settings, lab)
     torch.cuda.synchronize(strips[0].device)
-    labels = torch.cat([o[0] for o in outs]).cpu().numpy()
+    labels = lab.cpu().numpy()
     cxy = torch.cat([o[1] for o in outs]).cpu().numpy()
     clab = torch.cat([o[2] for o in outs]).cpu().numpy()
     counts = torch.cat([o[3] for o in outs]).cpu().numpy()
@@ -331,8 +387,12 @@ def segment_strip_rank(settings, rgb_window, rank, world, device, group=None):
     p = strip_plan(settings.img_height, grid.s, grid.ns_r, world)[rank]
     strip = StripEngine(settings, p.cell_row_lo, p.cell_row_hi, device)
     strip.begin(rgb_window)
-    _run([strip], DistComm(rank, world, strip, group))
-    return strip.finish()
+    comm = DistComm(rank, world, strip, group)
+    _run([strip], comm)
+    out = strip.finish()
+    if _strict(settings):
+        out = (comm.strict_labels(out[0]),) + tuple(out[1:])
+    return out
 
 
 def strip_window(settings, rank, world):

@@ -114,11 +114,12 @@ def test_c_abi_engine_create_reports_invalid_settings():
 
 
 def test_strip_engine_rejects_unsupported_modes():
-    # strict connectivity is a whole-image CCL: not available in row strips;
-    # early stop is (the gathered shift, tests/test_gpu_pipeline.py)
-    from paper_1509_04232_b200.strips import check_strip_settings
+    # row strips take early stop and strict connectivity (the strict pass runs
+    # over the gathered image); geometry outside the fused path is rejected
+    from paper_1509_04232_b200.strips import StripEngine, check_strip_settings
     check_strip_settings(spx.Settings(img_width=64, img_height=64, spixel_size=8,
                                       early_stop_threshold=1.0))
+    check_strip_settings(spx.Settings(img_width=64, img_height=64, spixel_size=8,
+                                      connectivity_mode=spx.ConnectivityMode.STRICT))
     with pytest.raises(spx.InvalidSettingsError):
-        check_strip_settings(spx.Settings(img_width=64, img_height=64, spixel_size=8,
-                                          connectivity_mode=spx.ConnectivityMode.STRICT))
+        StripEngine(spx.Settings(img_width=64, img_height=64, spixel_size=3), 0, 5)

@@ -169,7 +169,7 @@ def _oracle_pipeline(rgb, st):
         2 if st.connectivity_mode is spx.ConnectivityMode.STRICT else 1)
     return oracle.segment(rgb, g.s, g.ns_r, g.ns_c, st.compactness, no_iters=st.no_iters,
                           space=st.color_space.value, perturb=st.enable_perturbation,
-                          connectivity=conn, tile_len=st.tile_len,
+                          connectivity=conn, min_size=st.min_size, tile_len=st.tile_len,
                           early_stop=st.early_stop_threshold)
 
 
@@ -442,6 +442,10 @@ def test_cell_path_batch_gray_heavy_frames():
     (231, 157, dict(spixel_size=9, no_iters=4), 5),
     (300, 150, dict(spixel_size=40, no_iters=3), 3),
     (96, 80, dict(spixel_size=8, no_iters=3), 6),
+    # strict connectivity: the scan-order pass over the gathered strips
+    (200, 160, dict(spixel_size=16, connectivity_mode=spx.ConnectivityMode.STRICT), 3),
+    (150, 96, dict(spixel_size=8, min_size=20, no_iters=4,
+                   connectivity_mode=spx.ConnectivityMode.STRICT), 5),
 ])
 def test_row_strips_equal_whole_image(h, w, kw, n):
     """C5 decomposition: strips with halo centres / partial-sum / label exchange
@@ -593,7 +597,8 @@ class TestStream:
 
 
 @pytest.mark.parametrize("ranks,extra", [(2, []), (3, []),
-                                         (3, ["--early-stop", "1000", "--iters", "10"])])
+                                         (3, ["--early-stop", "1000", "--iters", "10"]),
+                                         (3, ["--strict"])])
 def test_row_strips_distributed_processes(ranks, extra):
     """One process per strip (torchrun), halos and partial sums exchanged
     through DistComm (gloo, staged through host memory; the ranks share this

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--early-stop", type=float, default=None)
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--strict", action="store_true")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -37,7 +38,9 @@ def main():
     dist.init_process_group(backend)
     n = a.size
     st = spx.Settings(img_width=n, img_height=n, spixel_size=a.s, no_iters=a.iters,
-                      early_stop_threshold=a.early_stop)
+                      early_stop_threshold=a.early_stop,
+                      connectivity_mode=(spx.ConnectivityMode.STRICT if a.strict
+                                         else spx.ConnectivityMode.WEAK))
     rgb = np.random.default_rng(7).integers(0, 256, (n, n, 3), dtype=np.uint8)
     y0, y1 = strip_window(st, rank, world)
     window = torch.from_numpy(np.ascontiguousarray(rgb[y0:y1])).cuda(dev)
