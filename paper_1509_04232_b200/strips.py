@@ -204,7 +204,7 @@ class DistComm:
         st = self.strip
         for what in whats:
             st.pack(what)
-        works, staged = [], []
+        works = []
         for what in whats:
             bufs = getattr(st, what)
             if bufs[0][0].is_cuda and self._gloo():
