@@ -19,6 +19,10 @@ Cases:
   C4                 3840x2160, S=8, 10 iters
   C5                 16384x16384, S=16, 5 iters (~1 min on 8 cores)
   T1_<w>x<h>_k<K>    PAPER.md:135-139 image sizes at 1000 / 2000 superpixels
+  M_<name>           the Settings surface: strict connectivity (default and
+                     explicit min_size), perturbation, XYZ / RGB, early stop,
+                     no connectivity, unaligned S, compactness / iterations,
+                     tile_len, 720p, S > 32, and everything at once
 """
 
 import argparse
@@ -46,6 +50,26 @@ CASES = (
     + [(f"T1_{w}x{h}_k{k}", w, h, dict(num_superpixels=k), 0) for w, h in TABLE1
        for k in (1000, 2000)]
     + [("C5", 16384, 16384, dict(spixel_size=16), 0)]
+    # the Settings surface at VGA / 720p / C2 sizes (every option the
+    # reference's SegEngine takes, one at a time and combined)
+    + [(f"M_{name}", w, h, kw, seed) for name, w, h, kw, seed in (
+        ("strict", 640, 480, dict(num_superpixels=1200, connectivity_mode="strict"), 3),
+        ("strict_min50", 640, 480, dict(num_superpixels=1200, connectivity_mode="strict",
+                                        min_size=50), 4),
+        ("perturb", 640, 480, dict(num_superpixels=1200, enable_perturbation=True), 5),
+        ("xyz", 640, 480, dict(num_superpixels=1200, color_space="xyz"), 6),
+        ("rgb", 640, 480, dict(num_superpixels=1200, color_space="rgb", compactness=0.1), 7),
+        ("early", 640, 480, dict(num_superpixels=1200, no_iters=20, early_stop_threshold=200.0), 8),
+        ("noconn", 640, 480, dict(num_superpixels=1200, do_enforce_connectivity=False), 9),
+        ("k1000_s18", 640, 480, dict(num_superpixels=1000), 10),
+        ("m40_i12", 640, 480, dict(num_superpixels=600, compactness=40.0, no_iters=12), 11),
+        ("tile5", 640, 480, dict(spixel_size=12, tile_len=5), 12),
+        ("720p", 1280, 720, dict(num_superpixels=3600), 13),
+        ("c2_s35", 1280, 960, dict(num_superpixels=1000), 14),
+        ("all", 1001, 777, dict(num_superpixels=2500, compactness=15.0, no_iters=7,
+                                enable_perturbation=True, connectivity_mode="strict",
+                                min_size=30, tile_len=8, early_stop_threshold=80.0), 15),
+    )]
 )
 
 
@@ -64,7 +88,12 @@ def main():
         if args.only and name not in args.only:
             continue
         t0 = time.time()
-        st = sp.Settings(img_width=w, img_height=h, **kw)
+        kw2 = dict(kw)
+        if "connectivity_mode" in kw2:
+            kw2["connectivity_mode"] = sp.ConnectivityMode.parse(kw2["connectivity_mode"])
+        if "color_space" in kw2:
+            kw2["color_space"] = sp.ColorSpace.parse(kw2["color_space"])
+        st = sp.Settings(img_width=w, img_height=h, **kw2)
         img = np.random.default_rng(seed).integers(0, 256, (h, w, 3), dtype=np.uint8)
         res = sp.SegEngine(st, backend="par", workers=os.cpu_count()).perform_segmentation(
             sp.ImageRGB(img))
@@ -74,6 +103,7 @@ def main():
             "cxy": sha(res.spixel_map.centers_xy),
             "clab": sha(res.spixel_map.centers_lab),
             "counts": sha(res.spixel_map.num_pixels),
+            "passes": [len(res.timing.associate), len(res.timing.update)],
             "num_pixels_total": int(res.spixel_map.num_pixels.sum()),
             "ref_seconds": round(res.timing.total, 2),
             "ref_workers": os.cpu_count(),

@@ -10,7 +10,11 @@ compare sha256 of labels, centres and counts:
 * C4: 3840x2160, S = 8, 10 iterations;
 * C5: 16384x16384 (268 Mpx, 1,048,576 clusters) through SegEngine and as 8
   row strips with the halo / partial-sum / label exchange;
-* the five PAPER.md Table 1 image sizes at 1000 and 2000 superpixels.
+* the five PAPER.md Table 1 image sizes at 1000 and 2000 superpixels;
+* the Settings surface (``large_M_*``): strict connectivity, perturbation,
+  XYZ / RGB, early stop, no connectivity, unaligned S, tile_len, 720p,
+  S > 32 and all options together -- per frame through
+  perform_segmentation and inside a mixed batch through segment_device.
 """
 
 import hashlib
@@ -102,3 +106,28 @@ def test_paper_table1_sizes(golden_meta, size, k):
     res = eng.perform_segmentation(spx.ImageRGB(frame(m)))
     assert_matches(m, res.labels.data, res.spixel_map.centers_xy, res.spixel_map.centers_lab,
                    res.spixel_map.num_pixels, f"{size} K={k}")
+
+
+MATRIX = ["strict", "strict_min50", "perturb", "xyz", "rgb", "early", "noconn", "k1000_s18",
+          "m40_i12", "tile5", "720p", "c2_s35", "all"]
+
+
+@pytest.mark.parametrize("name", MATRIX)
+def test_settings_matrix(golden_meta, name):
+    import torch
+    m = golden_meta["hashes"][f"large_M_{name}"]
+    st = settings(m)
+    img = frame(m)
+    res = spx.SegEngine(st).perform_segmentation(spx.ImageRGB(img))
+    assert_matches(m, res.labels.data, res.spixel_map.centers_xy, res.spixel_map.centers_lab,
+                   res.spixel_map.num_pixels, f"{name} perform_segmentation")
+    assert len(res.timing.update) == m["passes"][1], name
+    # the same frame in the middle of a batch of unrelated frames
+    other = np.random.default_rng(m["seed"] + 1000).integers(0, 256, img.shape, dtype=np.uint8)
+    batch = torch.from_numpy(np.stack([other, img, other[::-1].copy()])).cuda()
+    eng = spx.SegEngine(st, max_batch=3)
+    labels, cxy, clab, counts, passes = eng.segment_device(batch)
+    torch.cuda.synchronize()
+    assert_matches(m, labels[1].cpu().numpy(), cxy[1].cpu().numpy(), clab[1].cpu().numpy(),
+                   counts[1].cpu().numpy(), f"{name} batch")
+    assert int(passes[1]) == m["passes"][1]

@@ -185,6 +185,34 @@ def test_large_frame_hashes(golden_meta, case):
     assert sha(cxy) == m["cxy"] and sha(clab) == m["clab"] and sha(counts) == m["counts"]
 
 
+def _oracle_kwargs(kw):
+    conn = 0 if kw.get("do_enforce_connectivity") is False else \
+        {"weak": 1, "strict": 2}[kw.get("connectivity_mode", "weak")]
+    return dict(no_iters=kw.get("no_iters", 5),
+                space={"rgb": 0, "xyz": 1, "lab": 2}[kw.get("color_space", "lab")],
+                perturb=kw.get("enable_perturbation", False), connectivity=conn,
+                min_size=kw.get("min_size"), tile_len=kw.get("tile_len", 16),
+                early_stop=kw.get("early_stop_threshold"))
+
+
+def test_settings_matrix_hashes(golden_meta):
+    """Every Settings option at VGA / 720p / C2 sizes (``large_M_*``, made by
+    the reference SegEngine in tests/golden/make_golden_large.py)."""
+    cases = {k: v for k, v in golden_meta["hashes"].items() if k.startswith("large_M_")}
+    assert len(cases) >= 13
+    for name, m in cases.items():
+        kw = m["settings"]
+        rgb = np.random.default_rng(m["seed"]).integers(0, 256, (m["h"], m["w"], 3),
+                                                         dtype=np.uint8)
+        s, ns_r, ns_c = _grid(m["w"], m["h"], kw)
+        labels, cxy, clab, counts, passes = oracle.segment(
+            rgb, s, ns_r, ns_c, kw.get("compactness", 10.0), **_oracle_kwargs(kw))
+        assert sha(labels) == m["labels"], name
+        assert sha(cxy) == m["cxy"] and sha(clab) == m["clab"], name
+        assert sha(counts) == m["counts"], name
+        assert passes == m["passes"][1], name
+
+
 def test_center_shift_matches_numpy():
     rng = np.random.default_rng(5)
     for k in (1, 3, 4, 7, 60, 64, 65, 200, 1200, 8160, 50000):
