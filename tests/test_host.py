@@ -34,6 +34,15 @@ class TestSettings:
         with pytest.raises(spx.InvalidSettingsError):
             spx.Settings(img_width=0, img_height=8, num_superpixels=4)
 
+    def test_enum_fields_take_names(self):
+        st = spx.Settings(img_width=8, img_height=8, num_superpixels=4, color_space="xyz",
+                          connectivity_mode="Weak")
+        assert st.color_space is spx.ColorSpace.XYZ
+        assert st.connectivity_mode is spx.ConnectivityMode.WEAK
+        for kw in ({"color_space": "hsv"}, {"connectivity_mode": "loose"}):
+            with pytest.raises(spx.InvalidSettingsError):
+                spx.Settings(img_width=8, img_height=8, num_superpixels=4, **kw)
+
     def test_errors_are_valueerrors(self):
         assert issubclass(spx.InvalidSettingsError, ValueError)
         assert issubclass(spx.DimensionMismatchError, spx.SuperpixError)
