@@ -131,3 +131,12 @@ def test_settings_matrix(golden_meta, name):
     assert_matches(m, labels[1].cpu().numpy(), cxy[1].cpu().numpy(), clab[1].cpu().numpy(),
                    counts[1].cpu().numpy(), f"{name} batch")
     assert int(passes[1]) == m["passes"][1]
+
+
+@pytest.mark.parametrize("name", MATRIX)
+def test_settings_matrix_row_strips(golden_meta, name):
+    # the same cases as 3 row strips (halo / partial sums / labels exchanged)
+    from paper_1509_04232_b200.strips import segment_strips_local
+    m = golden_meta["hashes"][f"large_M_{name}"]
+    labels, cxy, clab, counts = segment_strips_local(settings(m), frame(m), 3)
+    assert_matches(m, labels, cxy, clab, counts, f"{name} 3 strips")
