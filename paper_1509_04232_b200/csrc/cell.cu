@@ -733,12 +733,12 @@ __global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
 //  (2) the 3S x 3S window of labels is staged into shared memory with one
 //      round of cp.async (16-byte copies when aligned);
 //  (3) each warp takes row strips (strip j = rows [ry0 + j*tile_len, ...),
-//      an independent reference fold from 0.0, _core.pyx:233-243).  Lanes own
-//      (row, column-segment) pieces of the strip in row-major order: each
-//      counts its members, a warp scan gives every member its row-major
-//      position, members' L / a / b are copied with cp.async into a compact
-//      array (kExCap values per round; one round in practice), and lanes
-//      0..2 fold the three channels in order;
+//      an independent reference fold from 0.0, _core.pyx:233-243) and walks
+//      the strip in row-major order, 4 x 32 window positions per step: a
+//      ballot finds the members and their row-major ranks, the members'
+//      L / a / b are copied with cp.async into a compact array, and lanes
+//      0..2 fold the three channels in order once the array is half full and
+//      at the end of the strip (one fold per strip in practice);
 //  (4) lanes 0..5 of warp 0 run the pairwise strip tree (_core.pyx:300-311)
 //      for one component each and lanes 0..4 divide one component each.
 // Pipeline labels never spill, so the window holds every member.
@@ -797,7 +797,7 @@ __device__ __forceinline__ void finish_cluster(const ReduceParams& p, double (*s
   if (lane < 5) {
     double q;
     if (cnt > 0.0) {
-      q = ddiv(strips[0][lane], cnt);
+      q = ddiv_ilp(strips[0][lane], cnt);
     } else {  // empty: keep the previous centre
       q = lane < 3 ? p.prev_lab[3LL * gk + lane] : p.prev_xy[2LL * gk + (lane - 3)];
     }
@@ -864,130 +864,104 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
     for (int i = threadIdx.x; i < p.n_bl * 6; i += blockDim.x) (&strips[0][0])[i] = 0.0;
     cp_async_wait_all();
     __syncthreads();
-    // (3) strips
+    // (3) strips: row-major walk of the strip's window rectangle, 4 x 32
+    // positions per step (position i = row i / ww, column i % ww); a ballot
+    // per 32 positions gives the members their row-major ranks
+    const int dq = 32 / ww, dr = 32 - dq * ww;
+    const unsigned lt_mask = (1u << lane) - 1u;
 #pragma unroll 1
     for (int j = warp; j < p.n_bl; j += kExWarps) {
       const int ya = max(ry0 + j * p.tile_len, 0);
       const int yz = min(ry0 + (j + 1) * p.tile_len, ry1);
       if (ya >= yz) continue;  // warp-uniform
+      const int n_rect = (yz - ya) * ww;
       double acc = 0.0;                           // lanes 0..2: channel fold
       unsigned long long lx = 0, ly = 0, lc = 0;  // lane sums of x, global y, count
-#pragma unroll 1
-      for (int yc = ya; yc < yz; yc += 32) {  // chunks of <= 32 rows
-        const int rc = min(32, yz - yc);
-        const int g = 32 / rc;                 // segments per row
-        const int seg = (ww + g - 1) / g;
-        const int row = lane / g, sg = lane - row * g;
-        const bool own = row < rc;
-        const int c0 = own ? min(sg * seg, ww) : 0, c1 = own ? min(c0 + seg, ww) : 0;
-        const int y = yc + row;
-        SPX_DCHECK(!own || (y >= ya0 && y < ya0 + wrows && c0 >= 0 && c1 <= ww));
-        const int32_t* wrow = win + (long long)(y - ya0) * wst;
-        // Members of this lane's segment as bit masks of <= 96 columns; a
-        // longer segment (S > 32) is walked in sub-chunks of 96 columns,
-        // re-scanned when its members are copied.  Each row starts its walk
-        // at a different column: with the staged window's 16 (mod 32)-word
-        // row stride, lanes of different rows would otherwise hit the same
-        // shared-memory banks.
-        const int len = c1 - c0;
-        const int nsub = (len + 95) / 96;
-        auto scan = [&](int a0, int a1, unsigned& m0, unsigned& m1, unsigned& m2) -> unsigned {
-          m0 = m1 = m2 = 0;
-          unsigned sxx = 0;
-          const int sl = a1 - a0;
-          const int rot = sl ? row % sl : 0;
-          auto part = [&](int k0, int k1) {
+      int rr = lane / ww, cc = lane - (lane / ww) * ww;  // this lane's position
+      int o = 0;                                  // members copied, not yet folded
+      // lanes 0..2 fold the copied members of one channel each, in order;
+      // channel 0 carries the certified-sum flag in its sign bit: |L|
+      auto fold = [&]() {
+        cp_async_wait_all();
+        __syncwarp();
+        if (lane < 3) {
+          const float* src = cw + lane * kExCap;
+          const bool l0 = lane == 0;
+          int i = 0;
 #pragma unroll 4
-            for (int k = k0; k < k1; ++k) {
-              const bool hit = wrow[a0 + k] == gid;
-              sxx += hit ? (unsigned)(wx0 + a0 + k) : 0u;
-              if (k < 32) m0 |= (unsigned)hit << k;
-              else if (k < 64) m1 |= (unsigned)hit << (k - 32);
-              else m2 |= (unsigned)hit << (k - 64);
+          for (; i + 4 <= o; i += 4) {
+            float v0 = src[i], v1 = src[i + 1], v2 = src[i + 2], v3 = src[i + 3];
+            if (l0) {
+              v0 = fabsf(v0);
+              v1 = fabsf(v1);
+              v2 = fabsf(v2);
+              v3 = fabsf(v3);
             }
-          };
-          part(rot, sl);
-          part(0, rot);
-          return sxx;
-        };
-        unsigned m0 = 0, m1 = 0, m2 = 0;
-        int cnt = 0;
-        for (int sb = 0; sb < nsub; ++sb) {
-          const int a0 = c0 + 96 * sb, a1 = min(a0 + 96, c1);
-          lx += scan(a0, a1, m0, m1, m2);
-          cnt += __popc(m0) + __popc(m1) + __popc(m2);
-        }
-        lc += (unsigned)cnt;
-        ly += (unsigned long long)cnt * (unsigned long long)(y + p.row_off * p.s);
-        // exclusive scan of the counts in lane (= row-major) order
-        int off = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xFFFFFFFFu, off, o);
-          if (lane >= o) off += t;
-        }
-        const int total = __shfl_sync(0xFFFFFFFFu, off, 31);
-        off -= cnt;
-#pragma unroll 1
-        for (int base = 0; base < total; base += kExCap) {
-          if (cnt && off < base + kExCap && off + cnt > base) {
-            int o = off;
-            for (int sb = 0; sb < nsub && o < base + kExCap; ++sb) {
-              const int a0 = c0 + 96 * sb, a1 = min(a0 + 96, c1);
-              if (nsub > 1) scan(a0, a1, m0, m1, m2);  // one sub-chunk: masks kept
-              const float* g0 = im + (long long)y * p.w + wx0 + a0;
-#pragma unroll
-              for (int wd = 0; wd < 3; ++wd) {
-                unsigned mw = wd == 0 ? m0 : (wd == 1 ? m1 : m2);
-#pragma unroll 1
-                while (mw) {
-                  const int k = 32 * wd + __ffs(mw) - 1;
-                  mw &= mw - 1;
-                  if (o >= base && o < base + kExCap) {
-                    SPX_DCHECK(a0 + k < ww && o - base >= 0);
-                    cp_async4(cw + (o - base), g0 + k);
-                    cp_async4(cw + kExCap + (o - base), g0 + p.plane + k);
-                    cp_async4(cw + 2 * kExCap + (o - base), g0 + 2 * p.plane + k);
-                  }
-                  ++o;
-                }
-              }
-            }
+            acc = dadd(acc, (double)v0);
+            acc = dadd(acc, (double)v1);
+            acc = dadd(acc, (double)v2);
+            acc = dadd(acc, (double)v3);
           }
-          cp_async_wait_all();
-          __syncwarp();
-          if (lane < 3) {
-            // row-major order; channel 0 carries the certified-sum flag in
-            // its sign bit: |L|
-            const float* src = cw + lane * kExCap;
-            const int m = min(kExCap, total - base);
-            const bool l0 = lane == 0;
-            int i = 0;
-#pragma unroll 4
-            for (; i + 4 <= m; i += 4) {
-              float v0 = src[i], v1 = src[i + 1], v2 = src[i + 2], v3 = src[i + 3];
-              if (l0) {
-                v0 = fabsf(v0);
-                v1 = fabsf(v1);
-                v2 = fabsf(v2);
-                v3 = fabsf(v3);
-              }
-              acc = dadd(acc, (double)v0);
-              acc = dadd(acc, (double)v1);
-              acc = dadd(acc, (double)v2);
-              acc = dadd(acc, (double)v3);
-            }
 #pragma unroll 1
-            for (; i < m; ++i) acc = dadd(acc, (double)(l0 ? fabsf(src[i]) : src[i]));
+          for (; i < o; ++i) acc = dadd(acc, (double)(l0 ? fabsf(src[i]) : src[i]));
+        }
+        __syncwarp();
+        o = 0;
+      };
+#pragma unroll 1
+      for (int base = 0; base < n_rect; base += 128) {
+        if (o > kExCap - 128) fold();  // room for this step's members
+        int ry[4], cx[4];
+        bool hit[4];
+        unsigned msk[4];
+        ry[0] = rr;
+        cx[0] = cc;
+#pragma unroll
+        for (int u = 1; u < 4; ++u) {
+          ry[u] = ry[u - 1] + dq;
+          cx[u] = cx[u - 1] + dr;
+          if (cx[u] >= ww) {
+            cx[u] -= ww;
+            ++ry[u];
           }
-          __syncwarp();
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool in = base + 32 * u + lane < n_rect;
+          SPX_DCHECK(!in || (ya + ry[u] < ya0 + wrows && cx[u] >= 0 && cx[u] < ww));
+          hit[u] = in && win[(long long)(ya - ya0 + ry[u]) * wst + cx[u]] == gid;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) msk[u] = __ballot_sync(0xFFFFFFFFu, hit[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (hit[u]) {
+            const int q = o + __popc(msk[u] & lt_mask);
+            SPX_DCHECK(q < kExCap);
+            const int y = ya + ry[u];
+            const float* g0 = im + (long long)y * p.w + wx0 + cx[u];
+            cp_async4(cw + q, g0);
+            cp_async4(cw + kExCap + q, g0 + p.plane);
+            cp_async4(cw + 2 * kExCap + q, g0 + 2 * p.plane);
+            lx += (unsigned long long)(wx0 + cx[u]);
+            ly += (unsigned long long)(y + p.row_off * p.s);
+            lc += 1;
+          }
+          o += __popc(msk[u]);
+        }
+        rr = ry[3] + dq;
+        cc = cx[3] + dr;
+        if (cc >= ww) {
+          cc -= ww;
+          ++rr;
         }
       }
+      if (o) fold();
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        lx += __shfl_xor_sync(0xFFFFFFFFu, lx, o);
-        ly += __shfl_xor_sync(0xFFFFFFFFu, ly, o);
-        lc += __shfl_xor_sync(0xFFFFFFFFu, lc, o);
+      for (int sh = 16; sh; sh >>= 1) {
+        lx += __shfl_xor_sync(0xFFFFFFFFu, lx, sh);
+        ly += __shfl_xor_sync(0xFFFFFFFFu, ly, sh);
+        lc += __shfl_xor_sync(0xFFFFFFFFu, lc, sh);
       }
       if (lane < 3) strips[j][lane] = acc;
       if (lane == 0) {
