@@ -32,6 +32,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "spx_internal.cuh"
 
@@ -1135,6 +1136,352 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_exact_wide(ReduceParams p) 
   }
 }
 
+// ---- wide cells (S > 32): per-(cluster, strip) sums ------------------------
+//
+// With large cells nearly every cluster has a member outside the certified
+// range 2^k <= |v| < 128 (9 S^2 <= 2^(23+k): S = 118 needs |v| >= 2^-6), so
+// the cluster-level certificate of k_cell fails everywhere and the exact
+// fallback re-reads each cluster's 3S x 3S window -- every pixel nine times.
+// The reference's strips are the natural unit instead: a strip holds at most
+// tile_len * 3S members, so its own certified range is far wider (S = 118:
+// |v| >= 2^-10; 0.7% of strip channels fail on random frames).  Wide mode:
+//  (A) k_strip_acc reads every pixel once (its label and Lab) and adds it to
+//      its cluster's strip: one warp per cell walks the cell row by row
+//      into lane-private per-slot accumulators (as k_cell) and, whenever the
+//      rows of a slot row's clusters cross a strip boundary, sums the slot
+//      columns and adds them to the (cluster, strip) entry with atomics --
+//      exact in any order for a certified channel.  A channel with an
+//      uncertified member marks the entry; the first mark enqueues it.
+//  (B) k_strip_refold folds each marked channel again in the reference's
+//      row-major order (_core.pyx:233-243) over the strip's window rows.
+//  (C) k_reduce_strips runs the pairwise strip tree and the divisions
+//      (_core.pyx:300-320) per cluster and clears the entries.
+struct WideParams {
+  const float* img;        // planar Lab [F][3][plane]
+  const int32_t* labels;   // [F][H][W]
+  StripAcc* sacc;          // [F][K][n_bl]
+  const int32_t* done;
+  long long* wl;           // (gk << 8) | strip, entries with an uncertified channel
+  int32_t* wl_n;
+  int h, w, s, ns_r, ns_c, frames, n_bl, tile_len;
+  long long plane;
+  unsigned tau_bits;               // tau_strip
+  unsigned long long ns_c_magic;   // ceil(2^64 / ns_c): k / ns_c = umul64hi(k, magic)
+};
+
+constexpr int kWideAccBytes = 9 * 3 * 32 * 8 + 9 * 32 * 8 + 9 * 32;  // colour, ints, bad bits
+constexpr int kWideWarpSmem = (kWideAccBytes + 15) & ~15;
+
+template <int kPx>  // pixels per lane and cell row: ceil(S / 32)
+__global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f = blockIdx.y;
+  if (p.done && p.done[f] == 1) return;  // whole block: one frame
+  const int K = p.ns_r * p.ns_c;
+  const int cell = blockIdx.x * 4 + warp;
+  if (cell >= K) return;  // whole warp
+  unsigned char* wb = smem + warp * kWideWarpSmem;
+  double* accd = reinterpret_cast<double*>(wb);                                  // [9][3][32]
+  unsigned long long* acci = reinterpret_cast<unsigned long long*>(wb + 6912);   // [9][32]
+  unsigned char* badb = wb + 6912 + 2304;                                        // [9][32]
+  for (int i = lane; i < kWideAccBytes / 16; i += 32)
+    reinterpret_cast<float4*>(wb)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int S = p.s;
+  const int cr = cell / p.ns_c, cc = cell - cr * p.ns_c;
+  const int x_cell = cc * S, y_cell = cr * S;
+  const int rows = min(S, p.h - y_cell), cols = min(S, p.w - x_cell);
+  SPX_DCHECK(rows > 0 && cols > 0 && cols <= 32 * kPx);
+  const long long hw = (long long)p.h * p.w;
+  const float* fimg = p.img + (long long)f * 3 * p.plane;
+  const int32_t* flab = p.labels + (long long)f * hw;
+  StripAcc* fsa = p.sacc + (long long)f * K * p.n_bl;
+  const unsigned tau = p.tau_bits;
+  const bool small_grid = p.ns_c < 3;
+  const int kbase = (cr - 1) * p.ns_c + (cc - 1);  // id of slot (0, 0)
+  auto bad_bit = [&](float v, unsigned bit) {  // not 0 and outside [tau_strip, 128)
+    const unsigned a = __float_as_uint(v) & 0x7FFFFFFFu;
+    return (a - 1u < tau - 1u || a >= 0x43000000u) ? bit : 0u;
+  };
+  // a lane's pixels of a cell row: columns lane, lane + 32, ... (coalesced
+  // 4-byte loads)
+  int lb[kPx];
+  float L[kPx], A[kPx], B[kPx];
+  auto load_row = [&](int yl) {
+    const long long o = (long long)(y_cell + yl) * p.w + x_cell + lane;
+#pragma unroll
+    for (int u = 0; u < kPx; ++u) {
+      const bool in = lane + 32 * u < cols;
+      lb[u] = in ? flab[o + 32 * u] : 0;
+      L[u] = in ? __ldg(fimg + o + 32 * u) : 0.f;
+      A[u] = in ? __ldg(fimg + p.plane + o + 32 * u) : 0.f;
+      B[u] = in ? __ldg(fimg + 2 * p.plane + o + 32 * u) : 0.f;
+    }
+  };
+  // next strip boundary (last row of a strip) of each slot row dr: rows yl
+  // with yl + 1 + (2 - dr) S a multiple of tile_len
+  int nb[3];
+#pragma unroll
+  for (int dr = 0; dr < 3; ++dr) {
+    const int m = ((2 - dr) * S + 1) % p.tile_len;
+    nb[dr] = m ? p.tile_len - m : 0;
+  }
+  load_row(0);
+  __syncwarp();
+#pragma unroll 1
+  for (int yl = 0; yl < rows; ++yl) {
+    int clb[kPx];
+    float cL[kPx], cA[kPx], cB[kPx];
+#pragma unroll
+    for (int u = 0; u < kPx; ++u) {
+      clb[u] = lb[u];
+      cL[u] = L[u];
+      cA[u] = A[u];
+      cB[u] = B[u];
+    }
+    if (yl + 1 < rows) load_row(yl + 1);  // the next row's loads in flight
+    const unsigned long long pk_row = 1ull | ((unsigned long long)yl << 43);
+    // a lane's pixels of one slot are summed in registers first
+    int tc = -1;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    unsigned long long ci = 0;
+    unsigned cb = 0;
+    auto put = [&]() {
+      double* d = accd + tc * 96 + lane;
+      d[0] = dadd(d[0], c0);
+      d[32] = dadd(d[32], c1);
+      d[64] = dadd(d[64], c2);
+      acci[tc * 32 + lane] += ci;
+      badb[tc * 32 + lane] |= (unsigned char)cb;
+    };
+#pragma unroll
+    for (int u = 0; u < kPx; ++u) {
+      const int xr = lane + 32 * u;  // cell-relative column
+      if (xr >= cols) break;
+      int t;  // slot (dr, dc), row-major
+      if (small_grid) {
+        const unsigned k = (unsigned)clb[u];
+        const int kr = p.ns_c_magic ? (int)__umul64hi((unsigned long long)k, p.ns_c_magic)
+                                    : (int)k;
+        const int kc = (int)k - kr * p.ns_c;
+        t = (kr - cr + 1) * 3 + (kc - cc + 1);
+      } else {  // ns_c >= 3: the offset from slot 0's id names the slot
+        const int dk = clb[u] - kbase;
+        const int dr = (dk >= p.ns_c) + (dk >= 2 * p.ns_c);
+        t = dr * 3 + (dk - dr * p.ns_c);
+      }
+      SPX_DCHECK(t >= 0 && t < 9);
+      const float l = fabsf(cL[u]);  // channel 0 carries the cluster-level flag: |L|
+      const unsigned bb = bad_bit(l, 1u) | bad_bit(cA[u], 2u) | bad_bit(cB[u], 4u);
+      const unsigned long long pk = pk_row + ((unsigned long long)xr << 22);
+      if (t != tc) {
+        if (tc >= 0) put();
+        tc = t;
+        c0 = (double)l;
+        c1 = (double)cA[u];
+        c2 = (double)cB[u];
+        ci = pk;
+        cb = bb;
+      } else {
+        c0 = dadd(c0, (double)l);
+        c1 = dadd(c1, (double)cA[u]);
+        c2 = dadd(c2, (double)cB[u]);
+        ci += pk;
+        cb |= bb;
+      }
+    }
+    if (tc >= 0) put();
+    // Slot row dr holds clusters of cluster row cr - 1 + dr, whose windows
+    // start at row (cr + dr - 2) S: their strips end where
+    // yl + 1 + (2 - dr) S is a multiple of tile_len (or at the cell's end).
+#pragma unroll
+    for (int dr = 0; dr < 3; ++dr) {
+      const int rel = yl + (2 - dr) * S;  // row yl from the window top
+      if (yl == nb[dr]) nb[dr] += p.tile_len;
+      else if (yl + 1 < rows) continue;  // warp-uniform
+      const int kr = cr - 1 + dr;
+      if (kr < 0 || kr >= p.ns_r) continue;
+      const int j = rel / p.tile_len;
+      SPX_DCHECK(j >= 0 && j < p.n_bl);
+      __syncwarp();
+      // the slot row's three slots: each lane takes its own entries, the
+      // warp reduces them (any order: exact for certified channels; marked
+      // ones are refolded by k_strip_refold), lane 0 adds them to the entry
+#pragma unroll 1
+      for (int dc = 0; dc < 3; ++dc) {
+        const int kc = cc - 1 + dc, t = dr * 3 + dc;
+        if (kc < 0 || kc >= p.ns_c) continue;  // warp-uniform (no members)
+        const unsigned long long v = acci[t * 32 + lane];
+        const unsigned cnt = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(v & 2047ull));
+        if (cnt == 0u) continue;  // nothing added since the last flush (entries zero)
+        const unsigned sxr = __reduce_add_sync(0xFFFFFFFFu, (unsigned)((v >> 22) & 0x1FFFFFull));
+        const unsigned syr = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(v >> 43));
+        const unsigned bad = __reduce_or_sync(0xFFFFFFFFu, (unsigned)badb[t * 32 + lane]);
+        double* d = accd + t * 96 + lane;
+        double s0 = d[0], s1 = d[32], s2 = d[64];
+        d[0] = 0.0;
+        d[32] = 0.0;
+        d[64] = 0.0;
+        acci[t * 32 + lane] = 0ull;
+        badb[t * 32 + lane] = 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          s0 = dadd(s0, __shfl_xor_sync(0xFFFFFFFFu, s0, o));
+          s1 = dadd(s1, __shfl_xor_sync(0xFFFFFFFFu, s1, o));
+          s2 = dadd(s2, __shfl_xor_sync(0xFFFFFFFFu, s2, o));
+        }
+        if (lane == 0) {
+          StripAcc* e = fsa + ((long long)kr * p.ns_c + kc) * p.n_bl + j;
+          if (s0 != 0.0) atomicAdd(&e->s[0], s0);
+          if (s1 != 0.0) atomicAdd(&e->s[1], s1);
+          if (s2 != 0.0) atomicAdd(&e->s[2], s2);
+          atomicAdd(&e->sx, (unsigned long long)sxr + (unsigned long long)cnt * x_cell);
+          atomicAdd(&e->sy, (unsigned long long)syr + (unsigned long long)cnt * y_cell);
+          atomicAdd(&e->cnt, cnt);
+          if (bad && atomicOr(&e->bad, bad) == 0u)
+            p.wl[atomicAdd(p.wl_n, 1)] =
+                (((long long)f * K + (long long)kr * p.ns_c + kc) << 8) | j;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// (B) one warp per marked (cluster, strip): the marked channels folded in
+// the reference's order over the strip's window rows (_core.pyx:233-243):
+// 32 columns at a time, members ranked by ballot and compacted into shared
+// memory, lanes 0..2 folding them in order.
+constexpr int kRefoldCap = 512;  // compacted members per warp and fold round
+__global__ void __launch_bounds__(128) k_strip_refold(WideParams p) {
+  __shared__ float cvals[4][3][kRefoldCap];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* const cw = &cvals[warp][0][0];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int n = *p.wl_n;
+  const int K = p.ns_r * p.ns_c;
+  const long long hw = (long long)p.h * p.w;
+  for (int item = blockIdx.x * 4 + warp; item < n; item += gridDim.x * 4) {
+    const long long it = p.wl[item];
+    const long long gk = it >> 8;
+    const int j = (int)(it & 255);
+    const int ff = (int)(gk / K), fk = (int)(gk - (long long)ff * K);
+    StripAcc* e = p.sacc + gk * p.n_bl + j;
+    const unsigned bad = e->bad;
+    SPX_DCHECK(bad != 0u && bad < 8u && j < p.n_bl);
+    const float* im = p.img + (long long)ff * 3 * p.plane;
+    const int32_t* lb = p.labels + (long long)ff * hw;
+    const int r = fk / p.ns_c, c = fk - r * p.ns_c;
+    const int wx0 = max((c - 1) * p.s, 0), wx1 = min((c + 2) * p.s, p.w);
+    const int ry0 = (r - 1) * p.s, ry1 = min((r + 2) * p.s, p.h);
+    const int ya = max(ry0 + j * p.tile_len, 0), yz = min(ry0 + (j + 1) * p.tile_len, ry1);
+    const bool mine = lane < 3 && (bad >> lane & 1u);
+    double acc = 0.0;
+    int o = 0;  // members compacted, not yet folded
+    // lanes 0..2 fold their (marked) channel over the compacted members
+    auto fold = [&]() {
+      __syncwarp();
+      if (mine) {
+        const float* src = cw + lane * kRefoldCap;
+        int i = 0;
+#pragma unroll 1
+        for (; i + 4 <= o; i += 4) {
+          const float v0 = src[i], v1 = src[i + 1], v2 = src[i + 2], v3 = src[i + 3];
+          acc = dadd(acc, (double)v0);
+          acc = dadd(acc, (double)v1);
+          acc = dadd(acc, (double)v2);
+          acc = dadd(acc, (double)v3);
+        }
+#pragma unroll 1
+        for (; i < o; ++i) acc = dadd(acc, (double)src[i]);
+      }
+      __syncwarp();
+      o = 0;
+    };
+    // units of 32 columns in row-major order; groups of 4 units are loaded
+    // one group ahead (labels and values together); members get their
+    // row-major ranks from ballots and are compacted into shared memory
+    const int chunks = (wx1 - wx0 + 31) >> 5;
+    const int units = (yz - ya) * chunks;
+    int g_lb[4];
+    float g_v0[4], g_v1[4], g_v2[4];
+    auto load4 = [&](int u0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int u = u0 + q;
+        const int ry = u / chunks, ch = u - ry * chunks;
+        const int x = wx0 + 32 * ch + lane;
+        const bool in = u < units && x < wx1;
+        const long long off = (long long)(ya + ry) * p.w + x;
+        g_lb[q] = in ? __ldg(lb + off) : -1;
+        g_v0[q] = in ? __ldg(im + off) : 0.f;
+        g_v1[q] = in ? __ldg(im + p.plane + off) : 0.f;
+        g_v2[q] = in ? __ldg(im + 2 * p.plane + off) : 0.f;
+      }
+    };
+    load4(0);
+#pragma unroll 1
+    for (int u0 = 0; u0 < units; u0 += 4) {
+      int c_lb[4];
+      float c_v0[4], c_v1[4], c_v2[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        c_lb[q] = g_lb[q];
+        c_v0[q] = g_v0[q];
+        c_v1[q] = g_v1[q];
+        c_v2[q] = g_v2[q];
+      }
+      if (u0 + 4 < units) load4(u0 + 4);
+      if (o > kRefoldCap - 128) fold();  // room for this group's members
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool hit = c_lb[q] == fk;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, hit);
+        if (hit) {
+          const int pos = o + __popc(m & lt_mask);
+          cw[pos] = fabsf(c_v0[q]);  // channel 0: |L| (cluster-level flag bit)
+          cw[kRefoldCap + pos] = c_v1[q];
+          cw[2 * kRefoldCap + pos] = c_v2[q];
+        }
+        o += __popc(m);
+      }
+    }
+    if (o) fold();
+    if (mine) e->s[lane] = acc;
+  }
+}
+
+// (C) one warp per cluster: the strip entries into shared memory (cleared
+// in global memory for the next pass), then the strip tree, the divisions
+// and the stores of finish_cluster.
+__global__ void __launch_bounds__(128) k_reduce_strips(ReduceParams p, StripAcc* sacc,
+                                                       int32_t* wl_n) {
+  __shared__ double strips[4][kExMaxStrips][6];
+  __shared__ double qv[4][6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = p.ns_r * p.ns_c;
+  const int f = blockIdx.y;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *wl_n = 0;  // B has read it
+  if (p.done && p.done[f]) return;
+  const int k = blockIdx.x * 4 + warp;
+  if (k >= K) return;  // whole warp
+  const long long gk = (long long)f * K + k;
+  StripAcc* e = sacc + gk * p.n_bl;
+  for (int j = lane; j < p.n_bl; j += 32) {
+    const StripAcc v = e[j];
+    strips[warp][j][0] = v.s[0];
+    strips[warp][j][1] = v.s[1];
+    strips[warp][j][2] = v.s[2];
+    strips[warp][j][3] = (double)v.sx;
+    strips[warp][j][4] = (double)v.sy;
+    strips[warp][j][5] = (double)v.cnt;
+    e[j] = StripAcc{{0.0, 0.0, 0.0}, 0ull, 0ull, 0u, 0u};
+  }
+  __syncwarp();
+  const int r = k / p.ns_c, c = k - r * p.ns_c;
+  finish_cluster(p, strips[warp], qv[warp], (int)gk, r, c, lane);
+}
+
 }  // namespace
 
 // ---- launchers ----------------------------------------------------------------
@@ -1267,6 +1614,99 @@ int launch_records(const double* cxy, const double* clab, CRec* rec, int64_t ns_
                                                         (int)(ns_r * ns_c), n, (int)k0, (int)k1,
                                                         (int)row_off);
   SPX_LAUNCH_CHECK("k_records");
+  return SPX_OK;
+}
+
+// Wide mode for S > 32 (SPX_WIDE=0 keeps the per-cluster certificate and
+// k_exact_wide, for comparison).
+bool wide_mode(int64_t s, int64_t ns_r, int64_t ns_c) {
+  static const bool on = !getenv("SPX_WIDE") || atoi(getenv("SPX_WIDE")) != 0;
+  return on && s > 32 && ns_r * ns_c < ((int64_t)1 << 31);
+}
+
+static unsigned strip_tau_bits(int64_t s, int64_t tile_len) {
+  // a strip holds <= tile_len * 3S members: tau = 2^k with tile_len * 3S <= 2^(23+k)
+  int k = -23;
+  while ((double)tile_len * 3.0 * (double)s > std::ldexp(1.0, 23 + k)) ++k;
+  const float tau = (float)std::ldexp(1.0, k);
+  unsigned bits;
+  std::memcpy(&bits, &tau, sizeof bits);
+  return bits;
+}
+
+int launch_wide_update(const float* img, const int32_t* labels, StripAcc* sacc, long long* wl,
+                       int32_t* wl_n, const double* prev_xy, const double* prev_lab,
+                       double* out_xy, double* out_lab, int64_t* counts, CRec* rec,
+                       const int32_t* done, int64_t h, int64_t w, int64_t s, int64_t ns_r,
+                       int64_t ns_c, int64_t tile_len, int frames, cudaStream_t st) {
+  const int64_t K = ns_r * ns_c;
+  if (K <= 0 || frames <= 0) return SPX_OK;
+  if (frames > 65535) {
+    set_error("wide update: at most 65535 frames per launch");
+    return SPX_ERR_VALUE;
+  }
+  const int64_t n_bl = ceil_div(3 * s, tile_len);
+  if (s > kCellMaxS || n_bl > kExMaxStrips) {
+    set_error("wide update: S %lld / %lld strips out of range", (long long)s, (long long)n_bl);
+    return SPX_ERR_VALUE;
+  }
+  WideParams wp;
+  wp.img = img;
+  wp.labels = labels;
+  wp.sacc = sacc;
+  wp.done = done;
+  wp.wl = wl;
+  wp.wl_n = wl_n;
+  wp.h = (int)h;
+  wp.w = (int)w;
+  wp.s = (int)s;
+  wp.ns_r = (int)ns_r;
+  wp.ns_c = (int)ns_c;
+  wp.frames = frames;
+  wp.n_bl = (int)n_bl;
+  wp.tile_len = (int)tile_len;
+  wp.plane = plane_of(h * w);
+  wp.tau_bits = strip_tau_bits(s, tile_len);
+  // ceil(2^64 / ns_c); ns_c = 1 divides by itself (magic 0 marks it)
+  wp.ns_c_magic = ns_c == 1 ? 0ull : ~0ull / (unsigned long long)ns_c + 1ull;
+  const dim3 grid((unsigned)ceil_div(K, 4), (unsigned)frames);
+  const size_t smem = 4 * kWideWarpSmem;
+  switch ((int)ceil_div(s, 32)) {  // S in (32, 255]
+    case 2: k_strip_acc<2><<<grid, 128, smem, st>>>(wp); break;
+    case 3: k_strip_acc<3><<<grid, 128, smem, st>>>(wp); break;
+    case 4: k_strip_acc<4><<<grid, 128, smem, st>>>(wp); break;
+    case 5: k_strip_acc<5><<<grid, 128, smem, st>>>(wp); break;
+    case 6: k_strip_acc<6><<<grid, 128, smem, st>>>(wp); break;
+    case 7: k_strip_acc<7><<<grid, 128, smem, st>>>(wp); break;
+    default: k_strip_acc<8><<<grid, 128, smem, st>>>(wp); break;
+  }
+  SPX_LAUNCH_CHECK("k_strip_acc");
+  k_strip_refold<<<(unsigned)std::max(1, num_sms() * 8), 128, 0, st>>>(wp);
+  SPX_LAUNCH_CHECK("k_strip_refold");
+  ReduceParams p{};
+  p.img = img;
+  p.labels = labels;
+  p.prev_xy = prev_xy;
+  p.prev_lab = prev_lab;
+  p.out_xy = out_xy;
+  p.out_lab = out_lab;
+  p.counts = counts;
+  p.rec = rec;
+  p.done = done;
+  p.h = (int)h;
+  p.w = (int)w;
+  p.s = (int)s;
+  p.ns_r = (int)ns_r;
+  p.ns_c = (int)ns_c;
+  p.frames = frames;
+  p.plane = plane_of(h * w);
+  p.n_bl = (int)n_bl;
+  p.tile_len = (int)tile_len;
+  p.kr0 = 0;
+  p.kr1 = (int)ns_r;
+  p.row_off = 0;
+  k_reduce_strips<<<grid, 128, 0, st>>>(p, sacc, wl_n);
+  SPX_LAUNCH_CHECK("k_reduce_strips");
   return SPX_OK;
 }
 

@@ -80,6 +80,10 @@ struct Engine {
   cudaStream_t s_side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool use_cell = false;
+  bool wide = false;               // S > 32: per-(cluster, strip) sums (cell.cu)
+  StripAcc* sacc = nullptr;
+  long long* wwl = nullptr;
+  int32_t* wwl_n = nullptr;
   cudaEvent_t ev[EV_FIXED] = {};
   std::vector<cudaEvent_t> ev_assoc, ev_update;  // start/end pairs
   int n_assoc = 0, n_update = 0;
@@ -223,7 +227,8 @@ struct Engine {
     for (void* p : {(void*)lab, (void*)labels, (void*)scratch, (void*)cxy[0], (void*)cxy[1],
                     (void*)clab[0], (void*)clab[1], (void*)slab, (void*)done, (void*)passes,
                     (void*)cc_parent, (void*)cc_size, (void*)cc_nxt, (void*)cc_first,
-                    (void*)rec, (void*)acc, (void*)worklist})
+                    (void*)rec, (void*)acc, (void*)worklist, (void*)sacc, (void*)wwl,
+                    (void*)wwl_n})
       if (p) cudaFree(p);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -270,6 +275,15 @@ struct Engine {
       SPX_CUDA(cudaStreamCreateWithFlags(&s_side, cudaStreamNonBlocking));
       SPX_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       SPX_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+      wide = wide_mode(st.s, st.ns_r, st.ns_c);
+      if (wide) {
+        const size_t n = B * K * n_bl;
+        SPX_CUDA(cudaMalloc(&sacc, n * sizeof(StripAcc)));
+        SPX_CUDA(cudaMemset(sacc, 0, n * sizeof(StripAcc)));
+        SPX_CUDA(cudaMalloc(&wwl, n * sizeof(long long)));
+        SPX_CUDA(cudaMalloc(&wwl_n, sizeof(int32_t)));
+        SPX_CUDA(cudaMemset(wwl_n, 0, sizeof(int32_t)));
+      }
     } else {
       SPX_CUDA(cudaMalloc(&slab, B * K * n_bl * 6 * sizeof(double)));
     }
@@ -303,9 +317,11 @@ struct Engine {
   int associate(int cur, int frames, const int32_t* dn, bool with_update, int pass,
                 cudaStream_t s) {
     stage_mark(pass_event(ev_assoc, 2 * n_assoc), s);
+    // (wide mode: association only; the update reads the labels itself)
     int rc = use_cell ? launch_cell(lab, cxy[cur], clab[cur], rec, labels, acc, dn, st.height,
                                     st.width, st.s, st.ns_r, st.ns_c, xy_weight, frames,
-                                    with_update, s, 0, -1, 0, worklist, wl_n + (pass & 1))
+                                    with_update && !wide, s, 0, -1, 0, worklist,
+                                    wl_n + (pass & 1))
                       : launch_assoc(lab, cxy[cur], clab[cur], labels, dn, st.height, st.width,
                                      st.s, st.ns_r, st.ns_c, xy_weight, 0, st.height, frames, K, s);
     stage_mark(pass_event(ev_assoc, 2 * n_assoc + 1), s);
@@ -537,7 +553,13 @@ struct Engine {
     if ((rc = associate(cur, B, dn, true, 0, s))) return rc;
     for (int it = 0; it < st.no_iters; ++it) {
       stage_mark(pass_event(ev_update, 2 * n_update), s);
-      if (use_cell) {
+      if (use_cell && wide) {
+        if ((rc = launch_wide_update(lab, labels, sacc, wwl, wwl_n, cxy[cur], clab[cur],
+                                     cxy[nxt], clab[nxt], out_counts, rec, dn, st.height,
+                                     st.width, st.s, st.ns_r, st.ns_c, st.tile_len, B, s)))
+          return rc;
+        launches += 3;
+      } else if (use_cell) {
         // fork: the exact fallback (pass `it`'s worklist) on the side stream,
         // the reduce (which also zeroes the next pass's count) here; join
         SPX_CUDA(cudaEventRecord(ev_fork, s));
