@@ -1167,6 +1167,7 @@ struct WideParams {
   long long plane;
   unsigned tau_bits;               // tau_strip
   unsigned long long ns_c_magic;   // ceil(2^64 / ns_c): k / ns_c = umul64hi(k, magic)
+  int bands, band_rows;            // k_strip_acc: warps per cell, rows per warp
 };
 
 constexpr int kWideAccBytes = 9 * 3 * 32 * 8 + 9 * 32 * 8 + 9 * 32;  // colour, ints, bad bits
@@ -1179,7 +1180,8 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
   const int f = blockIdx.y;
   if (p.done && p.done[f] == 1) return;  // whole block: one frame
   const int K = p.ns_r * p.ns_c;
-  const int cell = blockIdx.x * 4 + warp;
+  const int wid = blockIdx.x * 4 + warp;
+  const int cell = wid / p.bands, band = wid - cell * p.bands;
   if (cell >= K) return;  // whole warp
   unsigned char* wb = smem + warp * kWideWarpSmem;
   double* accd = reinterpret_cast<double*>(wb);                                  // [9][3][32]
@@ -1190,8 +1192,11 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
   const int S = p.s;
   const int cr = cell / p.ns_c, cc = cell - cr * p.ns_c;
   const int x_cell = cc * S, y_cell = cr * S;
-  const int rows = min(S, p.h - y_cell), cols = min(S, p.w - x_cell);
-  SPX_DCHECK(rows > 0 && cols > 0 && cols <= 32 * kPx);
+  const int cols = min(S, p.w - x_cell);
+  // this warp's band of the cell's rows (small launches split cells)
+  const int yl0 = band * p.band_rows, rows = min(min(S, p.h - y_cell), yl0 + p.band_rows);
+  if (yl0 >= rows) return;  // whole warp
+  SPX_DCHECK(cols > 0 && cols <= 32 * kPx);
   const long long hw = (long long)p.h * p.w;
   const float* fimg = p.img + (long long)f * 3 * p.plane;
   const int32_t* flab = p.labels + (long long)f * hw;
@@ -1224,12 +1229,13 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
 #pragma unroll
   for (int dr = 0; dr < 3; ++dr) {
     const int m = ((2 - dr) * S + 1) % p.tile_len;
-    nb[dr] = m ? p.tile_len - m : 0;
+    const int b0 = m ? p.tile_len - m : 0;  // first boundary row of the cell
+    nb[dr] = yl0 <= b0 ? b0 : b0 + (yl0 - b0 + p.tile_len - 1) / p.tile_len * p.tile_len;
   }
-  load_row(0);
+  load_row(yl0);
   __syncwarp();
 #pragma unroll 1
-  for (int yl = 0; yl < rows; ++yl) {
+  for (int yl = yl0; yl < rows; ++yl) {
     int clb[kPx];
     float cL[kPx], cA[kPx], cB[kPx];
 #pragma unroll
@@ -1353,6 +1359,10 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
 // 32 columns at a time, members ranked by ballot and compacted into shared
 // memory, lanes 0..2 folding them in order.
 constexpr int kRefoldCap = 512;  // compacted members per warp and fold round
+#ifndef SPX_REFOLD_G
+#define SPX_REFOLD_G 8
+#endif
+constexpr int kRefoldG = SPX_REFOLD_G;  // units of 32 columns loaded per group
 __global__ void __launch_bounds__(128) k_strip_refold(WideParams p) {
   __shared__ float cvals[4][3][kRefoldCap];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1398,16 +1408,16 @@ __global__ void __launch_bounds__(128) k_strip_refold(WideParams p) {
       __syncwarp();
       o = 0;
     };
-    // units of 32 columns in row-major order; groups of 4 units are loaded
+    // units of 32 columns in row-major order; groups of kRefoldG units are loaded
     // one group ahead (labels and values together); members get their
     // row-major ranks from ballots and are compacted into shared memory
     const int chunks = (wx1 - wx0 + 31) >> 5;
     const int units = (yz - ya) * chunks;
-    int g_lb[4];
-    float g_v0[4], g_v1[4], g_v2[4];
+    int g_lb[kRefoldG];
+    float g_v0[kRefoldG], g_v1[kRefoldG], g_v2[kRefoldG];
     auto load4 = [&](int u0) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kRefoldG; ++q) {
         const int u = u0 + q;
         const int ry = u / chunks, ch = u - ry * chunks;
         const int x = wx0 + 32 * ch + lane;
@@ -1421,20 +1431,20 @@ __global__ void __launch_bounds__(128) k_strip_refold(WideParams p) {
     };
     load4(0);
 #pragma unroll 1
-    for (int u0 = 0; u0 < units; u0 += 4) {
-      int c_lb[4];
-      float c_v0[4], c_v1[4], c_v2[4];
+    for (int u0 = 0; u0 < units; u0 += kRefoldG) {
+      int c_lb[kRefoldG];
+      float c_v0[kRefoldG], c_v1[kRefoldG], c_v2[kRefoldG];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kRefoldG; ++q) {
         c_lb[q] = g_lb[q];
         c_v0[q] = g_v0[q];
         c_v1[q] = g_v1[q];
         c_v2[q] = g_v2[q];
       }
-      if (u0 + 4 < units) load4(u0 + 4);
-      if (o > kRefoldCap - 128) fold();  // room for this group's members
+      if (u0 + kRefoldG < units) load4(u0 + kRefoldG);
+      if (o > kRefoldCap - 32 * kRefoldG) fold();  // room for this group's members
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kRefoldG; ++q) {
         const bool hit = c_lb[q] == fk;
         const unsigned m = __ballot_sync(0xFFFFFFFFu, hit);
         if (hit) {
@@ -1669,7 +1679,16 @@ int launch_wide_update(const float* img, const int32_t* labels, StripAcc* sacc, 
   wp.tau_bits = strip_tau_bits(s, tile_len);
   // ceil(2^64 / ns_c); ns_c = 1 divides by itself (magic 0 marks it)
   wp.ns_c_magic = ns_c == 1 ? 0ull : ~0ull / (unsigned long long)ns_c + 1ull;
-  const dim3 grid((unsigned)ceil_div(K, 4), (unsigned)frames);
+  // small launches split each cell into row bands (one warp each) so that
+  // about 16 warps per SM are in flight
+  {
+    const long long cells = K * (long long)frames;
+    const long long want = (long long)num_sms() * 16;
+    int bands = (int)std::min<long long>(std::max<long long>(1, ceil_div(want, cells)), ceil_div(s, 8));
+    wp.band_rows = (int)ceil_div(s, bands);
+    wp.bands = (int)ceil_div(s, wp.band_rows);
+  }
+  const dim3 grid((unsigned)ceil_div(K * (long long)wp.bands, 4), (unsigned)frames);
   const size_t smem = 4 * kWideWarpSmem;
   switch ((int)ceil_div(s, 32)) {  // S in (32, 255]
     case 2: k_strip_acc<2><<<grid, 128, smem, st>>>(wp); break;
@@ -1705,7 +1724,7 @@ int launch_wide_update(const float* img, const int32_t* labels, StripAcc* sacc, 
   p.kr0 = 0;
   p.kr1 = (int)ns_r;
   p.row_off = 0;
-  k_reduce_strips<<<grid, 128, 0, st>>>(p, sacc, wl_n);
+  k_reduce_strips<<<dim3((unsigned)ceil_div(K, 4), (unsigned)frames), 128, 0, st>>>(p, sacc, wl_n);
   SPX_LAUNCH_CHECK("k_reduce_strips");
   return SPX_OK;
 }

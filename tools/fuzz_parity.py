@@ -44,7 +44,7 @@ def frame(rng, kind, h, w):
 
 
 def case(rng):
-    big = rng.random() < 0.15  # large cells (S > 32: k_exact_wide, 16/32 lanes per cell)
+    big = rng.random() < 0.15  # large cells (S > 32: strip sums, 16/32 lanes per cell)
     h, w = int(rng.integers(6, 900 if big else 420)), int(rng.integers(6, 900 if big else 560))
     if rng.random() < 0.5:  # half the shapes 128-bit aligned (W % 4 == 0), half anything
         w += (-w) % 4
