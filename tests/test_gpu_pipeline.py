@@ -235,6 +235,43 @@ def test_cell_path_large_cells_and_odd_frames(s, h, w):
             assert np.array_equal(res.spixel_map.num_pixels, counts), (s, name, tile)
 
 
+@pytest.mark.parametrize("kw", [
+    dict(spixel_size=40),
+    dict(spixel_size=48, early_stop_threshold=40.0, no_iters=9),
+    dict(spixel_size=36, enable_perturbation=True, tile_len=7),
+    dict(spixel_size=70, connectivity_mode=spx.ConnectivityMode.STRICT, tile_len=30),
+    dict(spixel_size=33, color_space=spx.ColorSpace.XYZ, compactness=3.0),
+])
+def test_wide_mode_batches_graphs_and_lanes(kw):
+    # S > 32 (per-(cluster, strip) sums): a mixed batch through the graph
+    # replay (calls 3 and 4) and through concurrent lanes, every frame equal
+    # to the oracle; early stop, perturbation, strict connectivity, odd tile
+    # lengths and XYZ included
+    import torch
+    h, w = 181, 243
+    st = spx.Settings(img_width=w, img_height=h, **kw)
+    imgs = _images(h, w, 5)
+    frames = np.stack([imgs[k] for k in ("noise", "gray", "smooth", "dark")] + [imgs["noise"][::-1].copy()])
+    ref = [_oracle_pipeline(f, st) for f in frames]
+    eng = spx.SegEngine(st, max_batch=len(frames))
+    assert eng.fused_path
+    d = torch.from_numpy(frames).cuda()
+    for call in range(4):
+        labels, cxy, clab, counts, passes = (x.cpu().numpy() for x in eng.segment_device(d))
+        for i, (ol, ox, oc, on, op) in enumerate(ref):
+            assert np.array_equal(labels[i], ol), (kw, call, i)
+            assert cxy[i].tobytes() == ox.tobytes() and clab[i].tobytes() == oc.tobytes(), (kw, call, i)
+            assert np.array_equal(counts[i], on) and int(passes[i]) == op, (kw, call, i)
+    big = torch.from_numpy(np.concatenate([frames] * 4)).cuda()  # 20 frames: lanes
+    eng2 = spx.SegEngine(st, max_batch=20)
+    eng2.set_lanes(3)
+    labels, cxy, clab, counts, _ = (x.cpu().numpy() for x in eng2.segment_device(big))
+    for i in range(20):
+        ol, ox, oc, on, _ = ref[i % 5]
+        assert np.array_equal(labels[i], ol) and np.array_equal(counts[i], on), (kw, i)
+        assert cxy[i].tobytes() == ox.tobytes() and clab[i].tobytes() == oc.tobytes(), (kw, i)
+
+
 def test_odd_frame_batches_and_strips():
     # a batch of frames with h*w odd (frame f's pixels start at an unaligned
     # RGB offset for odd f) and a row-strip split of such a frame
