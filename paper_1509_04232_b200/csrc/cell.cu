@@ -1173,7 +1173,9 @@ struct WideParams {
 constexpr int kWideAccBytes = 9 * 3 * 32 * 8 + 9 * 32 * 8 + 9 * 32;  // colour, ints, bad bits
 constexpr int kWideWarpSmem = (kWideAccBytes + 15) & ~15;
 
-template <int kPx>  // pixels per lane and cell row: ceil(S / 32)
+// kPx: pixels per lane and cell row, ceil(S / 32); SG: fewer than 3 cluster
+// columns (slots from a division instead of the id offset)
+template <int kPx, bool SG>
 __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1202,7 +1204,9 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
   const int32_t* flab = p.labels + (long long)f * hw;
   StripAcc* fsa = p.sacc + (long long)f * K * p.n_bl;
   const unsigned tau = p.tau_bits;
-  const bool small_grid = p.ns_c < 3;
+  const bool small_grid = SG;
+  const long long pl = p.plane;
+  const int ns_c = p.ns_c;
   const int kbase = (cr - 1) * p.ns_c + (cc - 1);  // id of slot (0, 0)
   auto bad_bit = [&](float v, unsigned bit) {  // not 0 and outside [tau_strip, 128)
     const unsigned a = __float_as_uint(v) & 0x7FFFFFFFu;
@@ -1212,15 +1216,19 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
   // 4-byte loads)
   int lb[kPx];
   float L[kPx], A[kPx], B[kPx];
+  const int32_t* const lcell = flab + (long long)y_cell * p.w + x_cell + lane;
+  const float* const icell = fimg + (long long)y_cell * p.w + x_cell + lane;
   auto load_row = [&](int yl) {
-    const long long o = (long long)(y_cell + yl) * p.w + x_cell + lane;
+    const long long o = (long long)yl * p.w;
+    const int32_t* lr = lcell + o;
+    const float* ir = icell + o;
 #pragma unroll
     for (int u = 0; u < kPx; ++u) {
       const bool in = lane + 32 * u < cols;
-      lb[u] = in ? flab[o + 32 * u] : 0;
-      L[u] = in ? __ldg(fimg + o + 32 * u) : 0.f;
-      A[u] = in ? __ldg(fimg + p.plane + o + 32 * u) : 0.f;
-      B[u] = in ? __ldg(fimg + 2 * p.plane + o + 32 * u) : 0.f;
+      lb[u] = in ? lr[32 * u] : 0;
+      L[u] = in ? __ldg(ir + 32 * u) : 0.f;
+      A[u] = in ? __ldg(ir + pl + 32 * u) : 0.f;
+      B[u] = in ? __ldg(ir + 2 * pl + 32 * u) : 0.f;
     }
   };
   // next strip boundary (last row of a strip) of each slot row dr: rows yl
@@ -1273,8 +1281,8 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
         t = (kr - cr + 1) * 3 + (kc - cc + 1);
       } else {  // ns_c >= 3: the offset from slot 0's id names the slot
         const int dk = clb[u] - kbase;
-        const int dr = (dk >= p.ns_c) + (dk >= 2 * p.ns_c);
-        t = dr * 3 + (dk - dr * p.ns_c);
+        const int dr = (dk >= ns_c) + (dk >= 2 * ns_c);
+        t = dr * 3 + (dk - dr * ns_c);
       }
       SPX_DCHECK(t >= 0 && t < 9);
       const float l = fabsf(cL[u]);  // channel 0 carries the cluster-level flag: |L|
@@ -1690,15 +1698,20 @@ int launch_wide_update(const float* img, const int32_t* labels, StripAcc* sacc, 
   }
   const dim3 grid((unsigned)ceil_div(K * (long long)wp.bands, 4), (unsigned)frames);
   const size_t smem = 4 * kWideWarpSmem;
+  const bool sg = ns_c < 3;
+#define SPX_STRIP_ACC(PX)                                        \
+  (sg ? k_strip_acc<PX, true><<<grid, 128, smem, st>>>(wp)       \
+      : k_strip_acc<PX, false><<<grid, 128, smem, st>>>(wp))
   switch ((int)ceil_div(s, 32)) {  // S in (32, 255]
-    case 2: k_strip_acc<2><<<grid, 128, smem, st>>>(wp); break;
-    case 3: k_strip_acc<3><<<grid, 128, smem, st>>>(wp); break;
-    case 4: k_strip_acc<4><<<grid, 128, smem, st>>>(wp); break;
-    case 5: k_strip_acc<5><<<grid, 128, smem, st>>>(wp); break;
-    case 6: k_strip_acc<6><<<grid, 128, smem, st>>>(wp); break;
-    case 7: k_strip_acc<7><<<grid, 128, smem, st>>>(wp); break;
-    default: k_strip_acc<8><<<grid, 128, smem, st>>>(wp); break;
+    case 2: SPX_STRIP_ACC(2); break;
+    case 3: SPX_STRIP_ACC(3); break;
+    case 4: SPX_STRIP_ACC(4); break;
+    case 5: SPX_STRIP_ACC(5); break;
+    case 6: SPX_STRIP_ACC(6); break;
+    case 7: SPX_STRIP_ACC(7); break;
+    default: SPX_STRIP_ACC(8); break;
   }
+#undef SPX_STRIP_ACC
   SPX_LAUNCH_CHECK("k_strip_acc");
   k_strip_refold<<<(unsigned)std::max(1, num_sms() * 8), 128, 0, st>>>(wp);
   SPX_LAUNCH_CHECK("k_strip_refold");
