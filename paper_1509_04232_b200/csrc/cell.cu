@@ -662,18 +662,17 @@ constexpr int kRedT = 128;
 constexpr int kRedPer = SPX_REDPER;  // clusters per thread: their loads are in flight together
 constexpr int kRedN = kRedT * kRedPer;
 
-__global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
+__device__ __forceinline__ void reduce_cells_body(const ReduceParams& p, int bx, int f) {
   __shared__ __align__(16) double s_xy[kRedN * 2];
   __shared__ __align__(16) double s_lab[kRedN * 3];
   __shared__ __align__(16) long long s_cnt[kRedN];
   __shared__ __align__(16) CRec s_rec[kRedN];
   __shared__ bool s_fl[kRedN];  // flagged: k_exact_clusters owns its outputs
-  if (p.wl_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *p.wl_reset = 0;
+  if (p.wl_reset && bx == 0 && f == 0 && threadIdx.x == 0) *p.wl_reset = 0;
   const int K = p.ns_r * p.ns_c;
   const int nk = (p.kr1 - p.kr0) * p.ns_c;
-  const int f = blockIdx.y;
   if (p.done && p.done[f]) return;  // whole block: one frame
-  const int j0 = blockIdx.x * kRedN;
+  const int j0 = bx * kRedN;
   const int n = min(kRedN, nk - j0);
   const long long gk0 = (long long)f * K + p.kr0 * p.ns_c + j0;
   const int t = threadIdx.x;
@@ -725,6 +724,10 @@ __global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
     for (int i = t; i < 2 * n; i += kRedT)
       if (!s_fl[i >> 1]) gr[i] = sr[i];
   }
+}
+
+__global__ void __launch_bounds__(kRedT) k_reduce_cells(ReduceParams p) {
+  reduce_cells_body(p, blockIdx.x, blockIdx.y);
 }
 
 // Exact recomputation of flagged clusters (certificate failed).  One block
@@ -808,7 +811,9 @@ __device__ __forceinline__ void finish_cluster(const ReduceParams& p, double (*s
   if (lane == 0) write_centre(p, gk, r, c, cnt, qv);
 }
 
-__global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p) {
+// Items first, first + stride, ... of the worklist; blocks of >= kExWarps
+// warps (warps beyond kExWarps only help stage the window).
+__device__ __forceinline__ void exact_clusters_body(const ReduceParams& p, int first, int stride) {
   extern __shared__ __align__(16) unsigned char ex_smem[];
   __shared__ double strips[kExMaxStrips][6];
   __shared__ double qv[6];
@@ -822,10 +827,10 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
   const long long cap = (long long)p.frames * K;  // worklist capacity
   // (1) independent loads: the count and this block's first item (in bounds)
   const int n = *p.worklist_n;
-  int gk_next = (long long)blockIdx.x < cap ? p.worklist[blockIdx.x] : 0;
-  for (int item = blockIdx.x; item < n; item += gridDim.x) {
+  int gk_next = (long long)first < cap ? p.worklist[first] : 0;
+  for (int item = first; item < n; item += stride) {
     const int gk = gk_next;
-    if (item + (long long)gridDim.x < n) gk_next = p.worklist[item + gridDim.x];
+    if (item + (long long)stride < n) gk_next = p.worklist[item + stride];
     const int ff = gk / K, fk = gk - ff * K;
     // a frame that stopped early has no update this pass (k_cell enqueued its
     // clusters during its final association)
@@ -871,7 +876,7 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
     const int dq = 32 / ww, dr = 32 - dq * ww;
     const unsigned lt_mask = (1u << lane) - 1u;
 #pragma unroll 1
-    for (int j = warp; j < p.n_bl; j += kExWarps) {
+    for (int j = warp; warp < kExWarps && j < p.n_bl; j += kExWarps) {
       const int ya = max(ry0 + j * p.tile_len, 0);
       const int yz = min(ry0 + (j + 1) * p.tile_len, ry1);
       if (ya >= yz) continue;  // warp-uniform
@@ -976,6 +981,23 @@ __global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p
     if (warp == 0) finish_cluster(p, strips, qv, gk, r, c, lane);
     __syncthreads();  // the window and strips are reused by the next item
   }
+}
+
+__global__ void __launch_bounds__(kExWarps * 32) k_exact_clusters(ReduceParams p) {
+  exact_clusters_body(p, blockIdx.x, gridDim.x);
+}
+
+// The update of one pass as ONE launch (single-stream engine path): blocks
+// [0, red_blocks * frames) reduce (k_reduce_cells), the rest run the exact
+// fallback over the worklist k_cell filled (k_exact_clusters) -- the two
+// parts are independent, and one launch replaces a fork / join across two
+// streams (the chain a single frame waits on).
+__global__ void __launch_bounds__(kRedT) k_update(ReduceParams p, int red_blocks) {
+  const int nred = red_blocks * p.frames;
+  if ((int)blockIdx.x < nred)
+    reduce_cells_body(p, blockIdx.x % red_blocks, blockIdx.x / red_blocks);
+  else
+    exact_clusters_body(p, blockIdx.x - nred, gridDim.x - nred);
 }
 
 // Exact recomputation for large cells (S > 32), where most clusters are
@@ -1791,6 +1813,27 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   if (frames > 65535) {
     set_error("k_reduce_cells: at most 65535 frames per launch");
     return SPX_ERR_VALUE;
+  }
+  if (mode == kReduceExactMerged && s <= 32) {
+    const long long rb = ceil_div(nk, kRedN);
+    const long long ex_blocks = std::max<long long>(
+        num_sms(), std::min<long long>((long long)num_sms() * SPX_EXG, nk * frames / 64));
+    if (rb * frames + ex_blocks > 0x7FFFFFFFll) {
+      set_error("k_update: grid too large");
+      return SPX_ERR_VALUE;
+    }
+    static std::atomic<uint64_t> configured{0};  // per device
+    int dev = 0;
+    SPX_CUDA(cudaGetDevice(&dev));
+    if (!(configured.load() & (1ull << (dev & 63)))) {
+      SPX_CUDA(cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(kExWarps * 3 * kExCap * sizeof(float) +
+                                          kExWinSmemMax)));
+      configured.fetch_or(1ull << (dev & 63));
+    }
+    k_update<<<(unsigned)(rb * frames + ex_blocks), kRedT, exact_smem_bytes(s), st>>>(p, (int)rb);
+    SPX_LAUNCH_CHECK("k_update");
+    return SPX_OK;
   }
   if (mode != kExactOnly) {
     k_reduce_cells<<<dim3((unsigned)ceil_div(nk, kRedN), (unsigned)frames), kRedT, 0, st>>>(p);

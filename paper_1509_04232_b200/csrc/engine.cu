@@ -81,6 +81,9 @@ struct Engine {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool use_cell = false;
   bool wide = false;               // S > 32: per-(cluster, strip) sums (cell.cu)
+  // reduce and exact fallback as one launch (SPX_SPLIT_UPDATE=1: two
+  // launches on two streams, fork / join)
+  bool merged_update = !getenv("SPX_SPLIT_UPDATE");
   StripAcc* sacc = nullptr;
   long long* wwl = nullptr;
   int32_t* wwl_n = nullptr;
@@ -559,6 +562,15 @@ struct Engine {
                                      st.width, st.s, st.ns_r, st.ns_c, st.tile_len, B, s)))
           return rc;
         launches += 3;
+      } else if (use_cell && merged_update) {
+        // reduce + exact fallback of pass `it`'s worklist as one launch
+        // (k_update; the reduce also zeroes the next pass's count)
+        if ((rc = launch_reduce_cells(acc, lab, labels, cxy[cur], clab[cur], cxy[nxt], clab[nxt],
+                                      out_counts, rec, dn, worklist, wl_n + (it & 1), st.height,
+                                      st.width, st.s, st.ns_r, st.ns_c, st.tile_len, B, s, 0, -1,
+                                      0, kReduceExactMerged, wl_n + ((it + 1) & 1))))
+          return rc;
+        launches += 1;
       } else if (use_cell) {
         // fork: the exact fallback (pass `it`'s worklist) on the side stream,
         // the reduce (which also zeroes the next pass's count) here; join
