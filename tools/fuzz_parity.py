@@ -43,8 +43,12 @@ def frame(rng, kind, h, w):
                 np.arange(h)[:, None] // 3) % 7].astype(np.uint8)
 
 
+# share of cases with large cells (S > 32); SPX_FUZZ_BIG overrides
+BIG = float(os.environ.get("SPX_FUZZ_BIG", "0.15"))
+
+
 def case(rng):
-    big = rng.random() < 0.15  # large cells (S > 32: strip sums, 16/32 lanes per cell)
+    big = rng.random() < BIG  # large cells (S > 32: strip sums, 16/32 lanes per cell)
     h, w = int(rng.integers(6, 900 if big else 420)), int(rng.integers(6, 900 if big else 560))
     if rng.random() < 0.5:  # half the shapes 128-bit aligned (W % 4 == 0), half anything
         w += (-w) % 4
