@@ -89,6 +89,7 @@ struct CellParams {
   int runs_per_row;        // ceil(S / 4)
   int runs;                // S * runs_per_row
   int groups_per_warp;     // cell groups walked by one warp
+  int parts, part_runs;    // warps per cell group and runs per warp (small launches, LPC 32)
   unsigned row_magic;      // ceil(2^32 / runs_per_row)
   double xy_weight;
   float w32, k_mp, k_mc, k_xy, k_const, k_rel;
@@ -129,6 +130,10 @@ __device__ __noinline__ int exact_argmin(const double* __restrict__ cxy, const d
 constexpr int kWarps = 4;
 constexpr int kCellMaxS = 255;
 constexpr int kGroupsPerWarp = 4;  // max consecutive cell groups walked by one warp
+#ifndef SPX_CELL_WARPS_SMALL
+#define SPX_CELL_WARPS_SMALL 32
+#endif
+constexpr int kCellWarpsSmall = SPX_CELL_WARPS_SMALL;  // warps per SM a small LPC-32 launch aims for
 #ifndef SPX_MINB
 #define SPX_MINB 4  // resident blocks per SM the register budget is sized for
 #endif
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(128, ACC ? SPX_MINB : SPX_MINB_FIN) k_cell(Cel
   if (p.done && p.done[f] == 1) return;  // whole block: one frame
   const int n_cells = (p.cr1 - p.cr0) * p.ns_c;
   const int g_begin = (blockIdx.x * kWarps + warp) * p.groups_per_warp;
-  const int g_end = min(g_begin + p.groups_per_warp, (n_cells + CPW - 1) / CPW);
+  const int g_end = min(g_begin + p.groups_per_warp, (n_cells + CPW - 1) / CPW * p.parts);
   if (g_begin >= g_end) return;  // whole warp
 
   unsigned char* wbase = smem + (size_t)warp * warp_smem(LPC, ACC);
@@ -246,19 +251,25 @@ __global__ void __launch_bounds__(128, ACC ? SPX_MINB : SPX_MINB_FIN) k_cell(Cel
       Bx = make_float4(b[0], b[1], b[2], b[3]);
     }
   };
-  int row0, c40;
-  run_pos(ll, row0, c40);
-
+  // first run of the lane in its cell (LPC 32: per part, below)
+  int row0 = 0, c40 = 0;
+  if (LPC < 32) run_pos(ll, row0, c40);
   for (int grp = g_begin; grp < g_end; ++grp) {
     // ---- geometry (local grid) -----------------------------------------------
-    const int cell = p.cr0 * p.ns_c + grp * CPW + ci;
-    const bool active = grp * CPW + ci < n_cells;
+    // LPC 32 (one cell per warp): group = (cell, part), the part's runs
+    // [j0, j1) of the cell; narrower cells take whole cells (parts == 1)
+    const int cg = LPC == 32 ? grp / p.parts : grp;
+    const int j0 = LPC == 32 ? (grp - cg * p.parts) * p.part_runs : 0;
+    const int j1 = LPC == 32 ? min(p.runs, j0 + p.part_runs) : p.runs;
+    if (LPC == 32) run_pos(j0 + ll, row0, c40);
+    const int cell = p.cr0 * p.ns_c + cg * CPW + ci;
+    const bool active = cg * CPW + ci < n_cells;
     const int cr = active ? cell / p.ns_c : 0;
     const int cc = active ? cell - cr * p.ns_c : 0;
     const int x_cell = cc * S, y_cell = cr * S;  // local pixel origin
     const int y_glob0 = (cr + p.row_off) * S;    // global y of the cell's row 0
     // first run of this lane (its latency overlaps the staging below)
-    bool ok_n = active && ll < p.runs && y_cell + row0 < p.h && x_cell + c40 < p.w;
+    bool ok_n = active && j0 + ll < j1 && y_cell + row0 < p.h && x_cell + c40 < p.w;
     int row_n = row0, c4_n = c40;
     float4 Ln = make_float4(0.f, 0.f, 0.f, 0.f), An = Ln, Bn = Ln;
     int buf = 0;
@@ -315,12 +326,12 @@ __global__ void __launch_bounds__(128, ACC ? SPX_MINB : SPX_MINB_FIN) k_cell(Cel
         __fmaf_rn(mc, p.k_mc, __fmaf_rn(__fmaf_rn(3.f, mxy, 2.f * S), p.k_xy, p.k_const));
     if (okf == 0.f) two_a_cell = INFINITY;
 
-    for (int j = ll; j < p.runs; j += LPC) {
+    for (int j = j0 + ll; j < j1; j += LPC) {
       const int row = row_n, c4 = c4_n;
       const bool ok = ok_n;
       float4 Lv = Ln, Av = An, Bv = Bn;
       // prefetch the lane's next run of this cell (software pipelining)
-      if (j + LPC < p.runs) {
+      if (j + LPC < j1) {
         run_pos(j + LPC, row_n, c4_n);
         ok_n = active && y_cell + row_n < p.h && x_cell + c4_n < p.w;
         if (CPA)
@@ -1626,9 +1637,23 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   // Walk up to kGroupsPerWarp groups per warp, but keep >= 16 warps per SM
   // in flight for small launches (one 640x480 frame has only 300 groups).
   const long long groups = ceil_div((cr1 - cr0) * ns_c, 32 / lpc) * (long long)frames;
+  // large cells in a small launch (one cell per warp): several warps per
+  // cell, each walking a contiguous share of its runs (>= 2 per lane), so
+  // about 32 warps per SM are in flight (one 3631x3859 image at S = 118:
+  // 1,023 cells)
+  p.parts = 1;
+  p.part_runs = p.runs;
+  if (lpc == 32) {
+    const long long want = ceil_div((long long)num_sms() * kCellWarpsSmall, groups);
+    const long long maxp = std::max<long long>(1, p.runs / (2 * lpc));
+    p.parts = (int)std::max<long long>(1, std::min(want, maxp));
+    p.part_runs = (int)(ceil_div(ceil_div(p.runs, p.parts), lpc) * lpc);
+    p.parts = (int)ceil_div(p.runs, p.part_runs);
+  }
   p.groups_per_warp = (int)std::max<long long>(
-      1, std::min<long long>(kGroupsPerWarp, groups / ((long long)num_sms() * 16)));
-  const long long warps = ceil_div(ceil_div((cr1 - cr0) * ns_c, 32 / lpc), p.groups_per_warp);
+      1, std::min<long long>(kGroupsPerWarp, groups * p.parts / ((long long)num_sms() * 16)));
+  const long long warps =
+      ceil_div(ceil_div((cr1 - cr0) * ns_c, 32 / lpc) * p.parts, p.groups_per_warp);
   const dim3 blocks((unsigned)ceil_div(warps, kWarps), (unsigned)frames);
   if (frames > 65535) {
     set_error("k_cell: at most 65535 frames per launch");
@@ -1710,10 +1735,10 @@ int launch_wide_update(const float* img, const int32_t* labels, StripAcc* sacc, 
   // ceil(2^64 / ns_c); ns_c = 1 divides by itself (magic 0 marks it)
   wp.ns_c_magic = ns_c == 1 ? 0ull : ~0ull / (unsigned long long)ns_c + 1ull;
   // small launches split each cell into row bands (one warp each) so that
-  // about 16 warps per SM are in flight
+  // about 32 warps per SM are in flight
   {
     const long long cells = K * (long long)frames;
-    const long long want = (long long)num_sms() * 16;
+    const long long want = (long long)num_sms() * kCellWarpsSmall;
     int bands = (int)std::min<long long>(std::max<long long>(1, ceil_div(want, cells)), ceil_div(s, 8));
     wp.band_rows = (int)ceil_div(s, bands);
     wp.bands = (int)ceil_div(s, wp.band_rows);
