@@ -1643,7 +1643,7 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   // 1,023 cells)
   p.parts = 1;
   p.part_runs = p.runs;
-  if (lpc == 32) {
+  if (lpc == 32 && !acc) {  // (accumulating passes: more warps = more epilogues, slower)
     const long long want = ceil_div((long long)num_sms() * kCellWarpsSmall, groups);
     const long long maxp = std::max<long long>(1, p.runs / (2 * lpc));
     p.parts = (int)std::max<long long>(1, std::min(want, maxp));
