@@ -287,10 +287,10 @@ class SegEngine:
         if max_updates is not None:
             nu = min(nu, max_updates)
             na = min(na, max_updates + 1)
-        return StageTiming(convert=t.convert * ms, init=t.init * ms, perturb=t.perturb * ms,
-                           associate=tuple(v * ms for v in t.associate[:na]),
-                           update=tuple(v * ms for v in t.update[:nu]),
-                           connectivity=t.connectivity * ms, total=t.total * ms)
+        return StageTiming(t.convert * ms, t.init * ms, t.perturb * ms,
+                           tuple([v * ms for v in t.associate[:na]]),
+                           tuple([v * ms for v in t.update[:nu]]),
+                           t.connectivity * ms, t.total * ms)
 
     def last_launches(self):
         return int(self._lib.spx_engine_last_launches(self._h))
@@ -370,7 +370,7 @@ class SegEngine:
         labels, cxy, clab, counts, passes = outs
         tm = self.last_timing(max_updates=int(passes[0]))
         return SegResult(labels=LabelMap._trusted(labels[0]),
-                         spixel_map=SuperpixelMap(self.grid, cxy[0], clab[0], counts[0]),
+                         spixel_map=SuperpixelMap._trusted(self.grid, cxy[0], clab[0], counts[0]),
                          timing=tm)
 
     def perform_segmentation_batch(self, imgs):
