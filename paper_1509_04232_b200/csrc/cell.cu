@@ -1236,15 +1236,10 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
   const float* fimg = p.img + (long long)f * 3 * p.plane;
   const int32_t* flab = p.labels + (long long)f * hw;
   StripAcc* fsa = p.sacc + (long long)f * K * p.n_bl;
-  const unsigned tau = p.tau_bits;
   const bool small_grid = SG;
   const long long pl = p.plane;
   const int ns_c = p.ns_c;
   const int kbase = (cr - 1) * p.ns_c + (cc - 1);  // id of slot (0, 0)
-  auto bad_bit = [&](float v, unsigned bit) {  // not 0 and outside [tau_strip, 128)
-    const unsigned a = __float_as_uint(v) & 0x7FFFFFFFu;
-    return (a - 1u < tau - 1u || a >= 0x43000000u) ? bit : 0u;
-  };
   // a lane's pixels of a cell row: columns lane, lane + 32, ... (coalesced
   // 4-byte loads)
   int lb[kPx];
@@ -1318,8 +1313,12 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
         t = dr * 3 + (dk - dr * ns_c);
       }
       SPX_DCHECK(t >= 0 && t < 9);
-      const float l = fabsf(cL[u]);  // channel 0 carries the cluster-level flag: |L|
-      const unsigned bb = bad_bit(l, 1u) | bad_bit(cA[u], 2u) | bad_bit(cB[u], 4u);
+      // channel 0's sign bit: the engine's convert flags pixels with a
+      // channel outside the strip's certified range (wide mode); such a
+      // strip has all three channels refolded
+      const unsigned bits = __float_as_uint(cL[u]);
+      const float l = __uint_as_float(bits & 0x7FFFFFFFu);
+      const unsigned bb = (bits >> 31) * 7u;
       const unsigned long long pk = pk_row + ((unsigned long long)xr << 22);
       if (t != tc) {
         if (tc >= 0) put();
@@ -1690,10 +1689,7 @@ bool wide_mode(int64_t s, int64_t ns_r, int64_t ns_c) {
 }
 
 static unsigned strip_tau_bits(int64_t s, int64_t tile_len) {
-  // a strip holds <= tile_len * 3S members: tau = 2^k with tile_len * 3S <= 2^(23+k)
-  int k = -23;
-  while ((double)tile_len * 3.0 * (double)s > std::ldexp(1.0, 23 + k)) ++k;
-  const float tau = (float)std::ldexp(1.0, k);
+  const float tau = strip_tau(s, tile_len);
   unsigned bits;
   std::memcpy(&bits, &tau, sizeof bits);
   return bits;

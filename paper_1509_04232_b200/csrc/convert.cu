@@ -353,10 +353,11 @@ __global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* _
 }
 
 // planar_hw > 0: the engine's planar layout with the certified-sum flag of
-// grid interval `s` in channel 0's sign bit.
+// grid interval `s` in channel 0's sign bit (tau_flag > 0: that range
+// instead -- wide mode flags by the strip-level range).
 int launch_convert(const uint8_t* rgb, float* out, int64_t p0, int64_t p1, int space,
-                   cudaStream_t st, int64_t planar_hw, int64_t s) {
-  const float tau = planar_hw > 0 ? certified_tau(s) : 0.f;
+                   cudaStream_t st, int64_t planar_hw, int64_t s, float tau_flag) {
+  const float tau = planar_hw > 0 ? (tau_flag > 0.f ? tau_flag : certified_tau(s)) : 0.f;
   if (p1 <= p0) return SPX_OK;
   int rc = upload_tables();
   if (rc) return rc;
@@ -398,5 +399,5 @@ extern "C" int32_t spx_convert_band(const uint8_t* rgb, float* out, int64_t h, i
                    (long long)y0, (long long)y1, (long long)h);
     return SPX_ERR_DIMENSION;
   }
-  return spx::launch_convert(rgb, out, y0 * w, y1 * w, space, spx::as_stream(stream), 0, 1);
+  return spx::launch_convert(rgb, out, y0 * w, y1 * w, space, spx::as_stream(stream), 0, 1, -1.f);
 }

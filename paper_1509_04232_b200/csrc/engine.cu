@@ -12,7 +12,8 @@
 #include "spx_internal.cuh"
 
 namespace spx {
-int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
+int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t,
+                   float);
 int launch_assoc(const float*, const double*, const double*, int32_t*, const int32_t*, int64_t,
                  int64_t, int64_t, int64_t, int64_t, double, int64_t, int64_t, int, int64_t,
                  cudaStream_t);
@@ -524,7 +525,9 @@ struct Engine {
     launches = 0;
     const int32_t* dn = early ? done : nullptr;
     stage_mark(ev[EV_START], s);
-    if ((rc = launch_convert(rgb, lab, 0, (int64_t)B * hw, st.color_space, s, use_cell ? hw : 0, st.s)))
+    // (wide mode: the flag marks pixels outside the strip-level range)
+    if ((rc = launch_convert(rgb, lab, 0, (int64_t)B * hw, st.color_space, s, use_cell ? hw : 0,
+                             st.s, wide ? strip_tau(st.s, st.tile_len) : -1.f)))
       return rc;
     ++launches;
     stage_mark(ev[EV_CONVERT], s);

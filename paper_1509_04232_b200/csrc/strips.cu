@@ -26,7 +26,8 @@
 #include "spx_internal.cuh"
 
 namespace spx {
-int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
+int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t,
+                   float);
 int launch_records(const double*, const double*, CRec*, int64_t, int64_t, int64_t, int,
                    cudaStream_t, int64_t, int64_t, int64_t);
 int launch_weak2(const int32_t*, int32_t*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
@@ -129,7 +130,7 @@ struct Strip {
   int begin(const uint8_t* rgb_local, cudaStream_t s) {
     SPX_CUDA(cudaSetDevice(device));
     const int64_t hw = hl * g.width;
-    int rc = launch_convert(rgb_local, lab, 0, hw, g.color_space, s, hw, g.s);
+    int rc = launch_convert(rgb_local, lab, 0, hw, g.color_space, s, hw, g.s, -1.f);
     if (rc) return rc;
     cur = 0;
     const int64_t k0 = own0 * g.ns_c, k1 = own1 * g.ns_c;
