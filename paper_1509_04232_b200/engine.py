@@ -342,6 +342,13 @@ class SegEngine:
         blk = self._torch.empty((total,), dtype=self._torch.uint8, pin_memory=True).numpy()
         return tuple(blk[o:o + n].view(dt).reshape(sh) for o, n, sh, dt in parts)
 
+    def _pinned_outputs_ptrs(self, b):
+        """_pinned_outputs plus the five host addresses (plain ints: no
+        per-array ctypes objects on the per-frame path)."""
+        outs = self._pinned_outputs(b)
+        base = outs[0].__array_interface__["data"][0]
+        return outs, [base + o for o, _, _, _ in self._layouts[b][1]]
+
     def _pinned_input(self, b):
         """Engine-owned pinned staging for `b` input frames (grown on demand)."""
         st = self.settings
@@ -351,6 +358,7 @@ class SegEngine:
             buf = t.empty((b, st.img_height, st.img_width, 3), dtype=t.uint8,
                           pin_memory=True).numpy()
             self._pin_in = buf
+            self._pin_in_ptr = buf.__array_interface__["data"][0]
         return buf[:b]
 
     def perform_segmentation(self, img):
@@ -362,9 +370,8 @@ class SegEngine:
         self._check_frame(img)
         pin = self._pinned_input(1)
         np.copyto(pin[0], img.data)
-        outs = self._pinned_outputs(1)
-        rc = self._lib.spx_engine_segment_host(self._h, pin.ctypes.data, 1,
-                                               *(a.ctypes.data for a in outs))
+        outs, ptrs = self._pinned_outputs_ptrs(1)
+        rc = self._lib.spx_engine_segment_host(self._h, self._pin_in_ptr, 1, *ptrs)
         if rc:
             _lib.check(rc, "segment")
         labels, cxy, clab, counts, passes = outs
