@@ -103,6 +103,24 @@ __device__ __forceinline__ int4 weak_rule4(int4 v, int4 up, int4 dn, int lft, in
   return make_int4(o[0], o[1], o[2], o[3]);
 }
 
+// The rule for pixels whose left and upper neighbours are in the image
+// (interior tiles): an isolated pixel always adopts its left neighbour.
+__device__ __forceinline__ int4 weak_rule4_inner(int4 v, int4 up, int4 dn, int lft, int rgt) {
+  const int vv[4] = {v.x, v.y, v.z, v.w};
+  const int uu[4] = {up.x, up.y, up.z, up.w};
+  const int dd[4] = {dn.x, dn.y, dn.z, dn.w};
+  int o[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int L = k == 0 ? lft : vv[k - 1];
+    const int R = k == 3 ? rgt : vv[k + 1];
+    const int c = vv[k];
+    const bool keep = (L == c) | (R == c) | (uu[k] == c) | (dd[k] == c);
+    o[k] = keep ? c : L;
+  }
+  return make_int4(o[0], o[1], o[2], o[3]);
+}
+
 __global__ void __launch_bounds__(256) k_weak2(const int32_t* __restrict__ src,
                                                int32_t* __restrict__ dst, int h, int w, int y0,
                                                int y1) {
@@ -124,17 +142,19 @@ __global__ void __launch_bounds__(256) k_weak2(const int32_t* __restrict__ src,
       t0[r][g] = __ldg(reinterpret_cast<const int4*>(s + (long long)(ty0 - 2 + r) * w + tx0 - 8) + g);
     }
     __syncthreads();
+    // (every pass-1 and pass-2 pixel of an inner tile has its left and upper
+    // neighbours in the image: columns >= tx0 - 4 >= 4, rows >= ty0 - 1 >= 1)
     for (int i = tid; i < R1G * NG1; i += 256) {
       const int r = i / NG1, g = i - r * NG1;
-      t1[r][g] = weak_rule4(t0[r + 1][g + 1], t0[r][g + 1], t0[r + 2][g + 1], t0[r + 1][g].w,
-                            t0[r + 1][g + 2].x);
+      t1[r][g] = weak_rule4_inner(t0[r + 1][g + 1], t0[r][g + 1], t0[r + 2][g + 1],
+                                  t0[r + 1][g].w, t0[r + 1][g + 2].x);
     }
     __syncthreads();
     for (int i = tid; i < HG * (WG / 4); i += 256) {
       const int r = i / (WG / 4), g = i - r * (WG / 4);
       *reinterpret_cast<int4*>(d + (long long)(ty0 + r) * w + tx0 + 4 * g) =
-          weak_rule4(t1[r + 1][g + 1], t1[r][g + 1], t1[r + 2][g + 1], t1[r + 1][g].w,
-                     t1[r + 1][g + 2].x);
+          weak_rule4_inner(t1[r + 1][g + 1], t1[r][g + 1], t1[r + 2][g + 1], t1[r + 1][g].w,
+                           t1[r + 1][g + 2].x);
     }
     return;
   }
