@@ -1244,20 +1244,27 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
   // 4-byte loads)
   int lb[kPx];
   float L[kPx], A[kPx], B[kPx];
-  const int32_t* const lcell = flab + (long long)y_cell * p.w + x_cell + lane;
-  const float* const icell = fimg + (long long)y_cell * p.w + x_cell + lane;
-  auto load_row = [&](int yl) {
-    const long long o = (long long)yl * p.w;
-    const int32_t* lr = lcell + o;
-    const float* ir = icell + o;
+  // per-lane row pointers, advanced one image row per load (the band's
+  // first row first)
+  const long long o0 = (long long)(y_cell + yl0) * p.w + x_cell + lane;
+  const int32_t* lr = flab + o0;
+  const float* ir0 = fimg + o0;
+  const float* ir1 = ir0 + pl;
+  const float* ir2 = ir0 + 2 * pl;
+  const int w = p.w;
+  auto load_row = [&]() {
 #pragma unroll
     for (int u = 0; u < kPx; ++u) {
       const bool in = lane + 32 * u < cols;
       lb[u] = in ? lr[32 * u] : 0;
-      L[u] = in ? __ldg(ir + 32 * u) : 0.f;
-      A[u] = in ? __ldg(ir + pl + 32 * u) : 0.f;
-      B[u] = in ? __ldg(ir + 2 * pl + 32 * u) : 0.f;
+      L[u] = in ? __ldg(ir0 + 32 * u) : 0.f;
+      A[u] = in ? __ldg(ir1 + 32 * u) : 0.f;
+      B[u] = in ? __ldg(ir2 + 32 * u) : 0.f;
     }
+    lr += w;
+    ir0 += w;
+    ir1 += w;
+    ir2 += w;
   };
   // next strip boundary (last row of a strip) of each slot row dr: rows yl
   // with yl + 1 + (2 - dr) S a multiple of tile_len
@@ -1268,7 +1275,7 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
     const int b0 = m ? p.tile_len - m : 0;  // first boundary row of the cell
     nb[dr] = yl0 <= b0 ? b0 : b0 + (yl0 - b0 + p.tile_len - 1) / p.tile_len * p.tile_len;
   }
-  load_row(yl0);
+  load_row();
   __syncwarp();
 #pragma unroll 1
   for (int yl = yl0; yl < rows; ++yl) {
@@ -1281,7 +1288,7 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
       cA[u] = A[u];
       cB[u] = B[u];
     }
-    if (yl + 1 < rows) load_row(yl + 1);  // the next row's loads in flight
+    if (yl + 1 < rows) load_row();  // the next row's loads in flight
     const unsigned long long pk_row = 1ull | ((unsigned long long)yl << 43);
     // a lane's pixels of one slot are summed in registers first
     int tc = -1;
@@ -1320,21 +1327,16 @@ __global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
       const float l = __uint_as_float(bits & 0x7FFFFFFFu);
       const unsigned bb = (bits >> 31) * 7u;
       const unsigned long long pk = pk_row + ((unsigned long long)xr << 22);
-      if (t != tc) {
-        if (tc >= 0) put();
-        tc = t;
-        c0 = (double)l;
-        c1 = (double)cA[u];
-        c2 = (double)cB[u];
-        ci = pk;
-        cb = bb;
-      } else {
-        c0 = dadd(c0, (double)l);
-        c1 = dadd(c1, (double)cA[u]);
-        c2 = dadd(c2, (double)cB[u]);
-        ci += pk;
-        cb |= bb;
-      }
+      // branch-free run merge: a new slot spills the old run (rare) and
+      // restarts the sums from zero (0.0 + v == v exactly)
+      const bool same = t == tc;
+      if (!same && tc >= 0) put();
+      c0 = dadd(same ? c0 : 0.0, (double)l);
+      c1 = dadd(same ? c1 : 0.0, (double)cA[u]);
+      c2 = dadd(same ? c2 : 0.0, (double)cB[u]);
+      ci = (same ? ci : 0ull) + pk;
+      cb = (same ? cb : 0u) | bb;
+      tc = t;
     }
     if (tc >= 0) put();
     // Slot row dr holds clusters of cluster row cr - 1 + dr, whose windows
