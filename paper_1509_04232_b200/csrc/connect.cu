@@ -22,6 +22,9 @@
 //     only be set by such a keeper);
 //   * absorbed components take the final value of their seed-left
 //     component, resolved by pointer jumping.
+// Components are labelled tile by tile in shared memory first (k_cc_local),
+// joined across tile borders (k_cc_border) and resolved per pixel
+// (k_cc_resolve, which also lists the components for the later passes).
 #include <algorithm>
 #include <climits>
 
@@ -267,46 +270,129 @@ __device__ __forceinline__ PixIdx pix_idx(int h, int w) {
   return q;
 }
 
-__global__ void k_cc_init(int32_t* parent, int32_t* size, int h, int w) {
-  const PixIdx q = pix_idx(h, w);
-  if (!q.in) return;
-  parent[q.i] = q.i;
-  size[q.i] = 0;
+// ---- component labelling ------------------------------------------------------
+// (A) k_cc_local: one block per 64 x 16 tile labels the tile's components in
+//     shared memory (union-find with min-index roots, then a flatten and the
+//     component sizes) and writes every pixel's tile-local root as a global
+//     index, the local root's count into `size`.  Row-major order inside a
+//     tile is the frame's scan order restricted to it, so a local root is the
+//     minimum global index of its piece.
+// (B) k_cc_border: the tiles' bottom rows and right columns unite with the
+//     neighbouring tiles (global min-index union-find over the local roots).
+// (C) k_cc_resolve: every pixel's root, and each tile-local root adds its
+//     count to its component's root (B's path halving may already have
+//     re-pointed a local root, so (A) marks them by a non-zero count).
+constexpr int CTW = 64, CTH = 16, CTN = CTW * CTH;
+
+__device__ __forceinline__ int s_find(int* par, int x) {
+  int p = par[x];
+  while (p != x) {
+    const int g = par[p];
+    if (g != p) par[x] = g;
+    x = p;
+    p = g;
+  }
+  return x;
+}
+__device__ __forceinline__ void s_unite(int* par, int a, int b) {
+  while (true) {
+    a = s_find(par, a);
+    b = s_find(par, b);
+    if (a == b) return;
+    if (a > b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    const int old = atomicMin(par + b, a);
+    if (old == b) return;
+    b = old;
+  }
 }
 
-__global__ void k_cc_union(const int32_t* __restrict__ lab, int32_t* parent, int h, int w) {
-  const PixIdx q = pix_idx(h, w);
-  if (!q.in) return;
-  const int32_t v = lab[q.i];
-  if (q.x < w - 1 && lab[q.i + 1] == v) uf_unite(parent, q.i, q.i + 1);
-  if (q.y < h - 1 && lab[q.i + w] == v) uf_unite(parent, q.i, q.i + w);
+__global__ void __launch_bounds__(256) k_cc_local(const int32_t* __restrict__ lab,
+                                                  int32_t* __restrict__ parent,
+                                                  int32_t* __restrict__ size, int h, int w) {
+  __shared__ int t_lab[CTN];
+  __shared__ int t_par[CTN];
+  __shared__ int t_cnt[CTN];
+  const int tx0 = blockIdx.x * CTW, ty0 = blockIdx.y * CTH;
+  const int base = blockIdx.z * h * w;
+  const int tw = min(CTW, w - tx0), th = min(CTH, h - ty0);
+  for (int i = threadIdx.x; i < CTN; i += 256) {
+    const int r = i / CTW, c = i - r * CTW;
+    t_lab[i] = (r < th && c < tw) ? __ldg(lab + base + (ty0 + r) * w + tx0 + c) : 0;
+    t_par[i] = i;
+    t_cnt[i] = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < CTN; i += 256) {
+    const int r = i / CTW, c = i - r * CTW;
+    if (r >= th || c >= tw) continue;
+    const int v = t_lab[i];
+    if (c + 1 < tw && t_lab[i + 1] == v) s_unite(t_par, i, i + 1);
+    if (r + 1 < th && t_lab[i + CTW] == v) s_unite(t_par, i, i + CTW);
+  }
+  __syncthreads();
+  int root[CTN / 256];
+#pragma unroll
+  for (int k = 0; k < CTN / 256; ++k) {
+    const int i = threadIdx.x + 256 * k;
+    int x = i, p = t_par[x];
+    while (p != x) {  // read-only chase (no writers in this phase)
+      x = p;
+      p = t_par[x];
+    }
+    root[k] = x;
+    const int r = i / CTW, c = i - r * CTW;
+    if (r < th && c < tw) atomicAdd(t_cnt + x, 1);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < CTN / 256; ++k) {
+    const int i = threadIdx.x + 256 * k;
+    const int r = i / CTW, c = i - r * CTW;
+    if (r >= th || c >= tw) continue;
+    const int x = root[k];
+    const int gi = base + (ty0 + r) * w + tx0 + c;
+    parent[gi] = base + (ty0 + x / CTW) * w + tx0 + x % CTW;
+    size[gi] = x == i ? t_cnt[i] : 0;  // > 0 marks the tile-local roots for (C)
+  }
 }
 
-// Flatten to roots and count component sizes; lanes of a warp with the same
-// root add their count with one atomic.
-__global__ void k_cc_flatten(int32_t* parent, int32_t* size, int h, int w) {
+__global__ void __launch_bounds__(128) k_cc_border(const int32_t* __restrict__ lab,
+                                                   int32_t* parent, int h, int w) {
+  const int tx0 = blockIdx.x * CTW, ty0 = blockIdx.y * CTH;
+  const int base = blockIdx.z * h * w;
+  const int t = threadIdx.x;
+  if (t < CTW) {  // bottom row: unite downwards
+    const int x = tx0 + t, y = ty0 + CTH - 1;
+    if (x < w && y + 1 < h) {
+      const int gi = base + y * w + x;
+      if (__ldg(lab + gi) == __ldg(lab + gi + w)) uf_unite(parent, gi, gi + w);
+    }
+  } else if (t < CTW + CTH) {  // right column: unite rightwards
+    const int x = tx0 + CTW - 1, y = ty0 + (t - CTW);
+    if (y < h && x + 1 < w) {
+      const int gi = base + y * w + x;
+      if (__ldg(lab + gi) == __ldg(lab + gi + 1)) uf_unite(parent, gi, gi + 1);
+    }
+  }
+}
+
+__global__ void k_cc_resolve(int32_t* parent, int32_t* size, int32_t* roots, int32_t* nroots,
+                             int h, int w) {
   const PixIdx q = pix_idx(h, w);
   const int32_t r = q.in ? uf_root(parent, q.i) : -1;
-  if (q.in) parent[q.i] = r;
-  const unsigned grp = __match_any_sync(0xFFFFFFFFu, r);
-  if (q.in && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(size + r, __popc(grp));
-}
-
-__global__ void k_cc_first(const int32_t* __restrict__ lab, const int32_t* __restrict__ parent,
-                           const int32_t* __restrict__ size, int32_t* first, int h, int w,
-                           int64_t nlab, int64_t min_size) {
-  const PixIdx q = pix_idx(h, w);
-  if (!q.in || parent[q.i] != q.i || size[q.i] < min_size) return;
-  atomicMin(first + q.f * nlab + lab[q.i], q.i);
-}
-
-__global__ void k_cc_next(const int32_t* __restrict__ lab, const int32_t* __restrict__ parent,
-                          const int32_t* __restrict__ size, const int32_t* __restrict__ first,
-                          int32_t* nxt, int32_t* roots, int32_t* nroots, int h, int w,
-                          int64_t nlab, int64_t min_size) {
-  const PixIdx q = pix_idx(h, w);
-  const bool root = q.in && parent[q.i] == q.i;
-  // compact list of components (any order): one global atomic per block
+  const bool root = q.in && r == q.i;
+  if (q.in) {
+    parent[q.i] = r;
+    // a tile-local root (count > 0) that is not its component's root adds
+    // its count there; only component roots receive adds, a root never adds
+    const int32_t c = size[q.i];
+    if (c > 0 && r != q.i) atomicAdd(size + r, c);
+  }
+  // compact list of the components (any order): one global atomic per block
   __shared__ int bcount, bbase;
   if (threadIdx.x == 0) bcount = 0;
   __syncthreads();
@@ -314,14 +400,36 @@ __global__ void k_cc_next(const int32_t* __restrict__ lab, const int32_t* __rest
   __syncthreads();
   if (threadIdx.x == 0) bbase = bcount ? atomicAdd(nroots, bcount) : 0;
   __syncthreads();
-  if (!root) return;
-  roots[bbase + slot] = q.i;
-  const int base = q.f * h * w;
-  const int32_t v = lab[q.i];
-  const bool keep = q.i == base ||
-                    (size[q.i] >= min_size && first[q.f * nlab + v] == q.i && lab[base] != v);
-  // absorbed: the root of the seed's left neighbour (up in column 0)
-  nxt[q.i] = keep ? q.i : parent[q.x > 0 ? q.i - 1 : q.i - w];
+  if (root) roots[bbase + slot] = q.i;
+}
+
+// (over the component list; sizes are final once (C) has run)
+__global__ void k_cc_first(const int32_t* __restrict__ lab, const int32_t* __restrict__ size,
+                           const int32_t* __restrict__ roots, const int32_t* __restrict__ nroots,
+                           int32_t* first, int hw, int64_t nlab, int64_t min_size) {
+  const int n = *nroots;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int32_t i = roots[j];
+    if (size[i] < min_size) continue;
+    atomicMin(first + (i / hw) * nlab + lab[i], i);
+  }
+}
+
+__global__ void k_cc_next(const int32_t* __restrict__ lab, const int32_t* __restrict__ parent,
+                          const int32_t* __restrict__ size, const int32_t* __restrict__ first,
+                          const int32_t* __restrict__ roots, const int32_t* __restrict__ nroots,
+                          int32_t* nxt, int w, int hw, int64_t nlab, int64_t min_size) {
+  const int n = *nroots;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int32_t i = roots[j];
+    const int f = i / hw, base = f * hw;
+    const int32_t v = lab[i];
+    const bool keep = i == base ||
+                      (size[i] >= min_size && first[f * nlab + v] == i && lab[base] != v);
+    // absorbed: the root of the seed's left neighbour (up in column 0)
+    const int x = (i - base) % w;
+    nxt[i] = keep ? i : parent[x > 0 ? i - 1 : i - w];
+  }
 }
 
 // Final value of each component: pointer jumping on nxt over the compact
@@ -447,18 +555,20 @@ static int launch_strict_chunk(const int32_t* src, int32_t* dst, int64_t h, int6
   }
   const dim3 grid((unsigned)ceil_div(w, 256), (unsigned)h, (unsigned)frames);
   const int H = (int)h, W = (int)w;
-  k_cc_init<<<grid, 256, 0, st>>>(parent, size, H, W);
   SPX_CUDA(cudaMemsetAsync(first, 0x7f, (size_t)(frames * nlab) * 4, st));
-  k_cc_union<<<grid, 256, 0, st>>>(src, parent, H, W);
-  k_cc_flatten<<<grid, 256, 0, st>>>(parent, size, H, W);
-  k_cc_first<<<grid, 256, 0, st>>>(src, parent, size, first, H, W, nlab, min_size);
   // The component list lives in dst until the final write; its length and
   // the per-round change flags in the kStrictExtra ints after `first`.
   int32_t* nroots = first + frames * nlab;
   int32_t* changed = nroots + 1;
   SPX_CUDA(cudaMemsetAsync(nroots, 0, kStrictExtra * sizeof(int32_t), st));
-  k_cc_next<<<grid, 256, 0, st>>>(src, parent, size, first, nxt, dst, nroots, H, W, nlab,
-                                  min_size);
+  const dim3 tiles((unsigned)ceil_div(w, CTW), (unsigned)ceil_div(h, CTH), (unsigned)frames);
+  k_cc_local<<<tiles, 256, 0, st>>>(src, parent, size, H, W);
+  k_cc_border<<<tiles, 128, 0, st>>>(src, parent, H, W);
+  k_cc_resolve<<<grid, 256, 0, st>>>(parent, size, dst, nroots, H, W);
+  const unsigned lb = (unsigned)std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 16);
+  k_cc_first<<<lb, 256, 0, st>>>(src, size, dst, nroots, first, (int)hw, nlab, min_size);
+  k_cc_next<<<lb, 256, 0, st>>>(src, parent, size, first, dst, nroots, nxt, W, (int)hw, nlab,
+                                min_size);
   int rounds = 1;
   while ((1ll << rounds) < hw) ++rounds;
   const unsigned jb = (unsigned)std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 8);

@@ -642,7 +642,7 @@ struct Engine {
       if ((rc = launch_strict(labels, out_labels, st.height, st.width, B, K, st.min_size,
                               cc_parent, cc_size, cc_nxt, cc_first, s)))
         return rc;
-      int rounds = 1;  // k_cc_init, union, flatten, first, next, jump x (rounds + 1), write
+      int rounds = 1;  // k_cc_local, border, resolve, first, next, jump x (rounds + 1), write
       while ((1ll << rounds) < hw) ++rounds;
       launches += 6 + rounds + 1;
     } else {
