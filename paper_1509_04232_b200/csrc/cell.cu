@@ -1548,12 +1548,14 @@ bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
          h * w * 3 < (int64_t)1 << 40 && h < (1 << 30) && w < (1 << 30);
 }
 
-// Lanes per cell, measured on one B200 (tools/cellbench, random frames):
-// 4 for S <= 12 (S = 8: 0.61 vs 0.95 ms per fused pass with 16 lanes), 8 for
-// 16 <= S <= 24 (S = 16: 0.60 vs 0.64 ms), 16 for S >= 28.  Fewer lanes per
-// cell give each lane more runs over which to amortise the per-cell staging
-// and epilogue; too few leave too many cells in flight per warp.
-// Lanes per cell: 4 for S <= 12, 8 for S <= 24, 16 above.  A launch with
+// Lanes per cell, measured on one B200 (tools/cellbench, random frames;
+// late round 2: 16 1080p frames, fused pass with 2 / 4 lanes): 2 for S <= 10
+// (S = 4: 0.57 vs 0.67 ms, S = 6: 0.45 vs 0.49, S = 8: 0.30 vs 0.32, S = 10:
+// 0.362 vs 0.372), 4 for S = 11, 12 (S = 12: 0.30 vs 0.28), 8 for
+// 13 <= S <= 24 (S = 16: 0.60 vs 0.64 ms per 256 VGA frames), 16 up to 64.
+// Fewer lanes per cell give each lane more runs over which to amortise the
+// per-cell staging and epilogue; too few leave too many cells in flight per
+// warp.  A launch with
 // fewer warps than one resident wave (16 per SM) -- small batches, e.g. one
 // VGA frame is 1,200 cells -- doubles it when every lane still gets >= 2
 // runs: shorter per-lane walks cut the pass latency (one 640x480 frame:
@@ -1561,9 +1563,9 @@ bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
 // cells (batch 16: LPC 16 is 5% slower).
 static int cell_lpc(int64_t s, long long cells) {
   static const int env = getenv("SPX_LPC") ? atoi(getenv("SPX_LPC")) : 0;  // development
-  if (s <= 64 && (env == 4 || env == 8 || env == 16 || env == 32)) return env;
+  if (s <= 64 && (env == 2 || env == 4 || env == 8 || env == 16 || env == 32)) return env;
   // S > 64: 32 lanes per cell (the per-lane pixel count must stay <= 2047)
-  int lpc = s <= 12 ? 4 : (s <= 24 ? 8 : (s <= 64 ? 16 : 32));
+  int lpc = s <= 10 ? 2 : (s <= 12 ? 4 : (s <= 24 ? 8 : (s <= 64 ? 16 : 32)));
   const long long runs = s * ceil_div(s, 4);
   // up to two doublings (a single 640x480 frame: 8 -> 32 lanes per cell)
   for (int d = 0; d < 2; ++d)
@@ -1661,7 +1663,8 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
     return SPX_ERR_VALUE;
   }
   const size_t smem = (size_t)kWarps * warp_smem(lpc, acc);
-  const int rc = lpc == 4    ? launch_cell_lpc<4>(p, blocks, smem, st, acc)
+  const int rc = lpc == 2    ? launch_cell_lpc<2>(p, blocks, smem, st, acc)
+                 : lpc == 4  ? launch_cell_lpc<4>(p, blocks, smem, st, acc)
                  : lpc == 8  ? launch_cell_lpc<8>(p, blocks, smem, st, acc)
                  : lpc == 16 ? launch_cell_lpc<16>(p, blocks, smem, st, acc)
                              : launch_cell_lpc<32>(p, blocks, smem, st, acc);
