@@ -1565,11 +1565,16 @@ static int cell_lpc(int64_t s, long long cells) {
   static const int env = getenv("SPX_LPC") ? atoi(getenv("SPX_LPC")) : 0;  // development
   if (s <= 64 && (env == 2 || env == 4 || env == 8 || env == 16 || env == 32)) return env;
   // S > 64: 32 lanes per cell (the per-lane pixel count must stay <= 2047)
-  int lpc = s <= 10 ? 2 : (s <= 12 ? 4 : (s <= 24 ? 8 : (s <= 64 ? 16 : 32)));
+  int lpc = s <= 10 ? 2 : (s <= 12 ? 4 : (s <= 23 ? 8 : (s <= 64 ? 16 : 32)));
   const long long runs = s * ceil_div(s, 4);
+  const long long wave = (long long)num_sms() * 16 * 32;  // lanes of one resident wave
+  // large launches at S = 24 and S = 29..32 (16 1080p frames: S = 24 with 16
+  // lanes 0.267 vs 0.281 ms per fused pass; S = 30..32 with 4 lanes 3-9%
+  // faster than 16 or 32)
+  if (s >= 24 && s <= 32 && cells * 16 >= wave) return s >= 29 ? 4 : 16;
   // up to two doublings (a single 640x480 frame: 8 -> 32 lanes per cell)
   for (int d = 0; d < 2; ++d)
-    if (lpc < 32 && cells * lpc < (long long)num_sms() * 16 * 32 && runs >= 2 * lpc) lpc *= 2;
+    if (lpc < 32 && cells * lpc < wave && runs >= 2 * lpc) lpc *= 2;
   return lpc;
 }
 

@@ -272,6 +272,26 @@ def test_wide_mode_batches_graphs_and_lanes(kw):
         assert cxy[i].tobytes() == ox.tobytes() and clab[i].tobytes() == oc.tobytes(), (kw, i)
 
 
+@pytest.mark.parametrize("s", [24, 30, 32])
+def test_large_launch_lane_choice(s):
+    # big single-lane launches at S = 24 / 29..32 take 16 / 4 lanes per cell
+    # (cell_lpc); frames at both ends of the batch equal the oracle
+    import torch
+    h, w, b = 544, 960, 24
+    st = spx.Settings(img_width=w, img_height=h, spixel_size=s, no_iters=3)
+    frames = np.stack([_images(h, w, 300 + i)["noise"] if i % 2 == 0 else _images(h, w, 300 + i)["gray"]
+                       for i in range(b)])
+    eng = spx.SegEngine(st, max_batch=b)
+    eng.set_lanes(1)
+    labels, cxy, clab, counts, _ = (x.cpu().numpy() for x in eng.segment_device(
+        torch.from_numpy(frames).cuda()))
+    for i in (0, 1, b - 1):
+        ol, ox, oc, on, _ = _oracle_pipeline(frames[i], st)
+        assert np.array_equal(labels[i], ol), (s, i)
+        assert cxy[i].tobytes() == ox.tobytes() and clab[i].tobytes() == oc.tobytes(), (s, i)
+        assert np.array_equal(counts[i], on), (s, i)
+
+
 def test_odd_frame_batches_and_strips():
     # a batch of frames with h*w odd (frame f's pixels start at an unaligned
     # RGB offset for odd f) and a row-strip split of such a frame
