@@ -129,7 +129,14 @@ __device__ __noinline__ int exact_argmin(const double* __restrict__ cxy, const d
 // shared-memory carve-out and leave 92 KB of L1 for the Lab stream.
 constexpr int kWarps = 4;
 constexpr int kCellMaxS = 255;
-constexpr int kGroupsPerWarp = 4;  // max consecutive cell groups walked by one warp
+// Cell groups walked by one warp (at most).  Measured with 4 lanes, 256 C1
+// frames (bench_configs, late round 2): 1 group per warp -- more, shorter
+// warps, smaller tails -- fused pass 0.598 -> 0.584 ms, step 4.327 -> 4.310
+// ms; C4 6.96 -> 6.89 ms; C3 equal (2 and 3 in between, 8 worse).
+#ifndef SPX_GPW
+#define SPX_GPW 1
+#endif
+constexpr int kGroupsPerWarp = SPX_GPW;
 #ifndef SPX_CELL_WARPS_SMALL
 #define SPX_CELL_WARPS_SMALL 32
 #endif
