@@ -127,7 +127,13 @@ __device__ __noinline__ int exact_argmin(const double* __restrict__ cxy, const d
 //                   count | flags<<11 | sum_x<<22 | sum_y<<43).
 // With LPC >= 8 the per-warp block is <= 10 KB, so 16 warps fit the 164 KB
 // shared-memory carve-out and leave 92 KB of L1 for the Lab stream.
-constexpr int kWarps = 4;
+// Warps per k_cell block (same 16 warps per SM either way: the register
+// budget is per SM).  Two: 256 C1 frames with 4 lanes 4.316 -> 4.291 ms,
+// fused pass 0.585 -> 0.578 ms (C4 within 0.4%); eight: 5% slower.
+#ifndef SPX_CELL_WARPS
+#define SPX_CELL_WARPS 2
+#endif
+constexpr int kWarps = SPX_CELL_WARPS;
 constexpr int kCellMaxS = 255;
 // Cell groups walked by one warp (at most).  Measured with 4 lanes, 256 C1
 // frames (bench_configs, late round 2): 1 group per warp -- more, shorter
@@ -190,7 +196,8 @@ __host__ __device__ constexpr size_t warp_smem(int lpc, bool acc) {
 // are loaded and stored one by one and the pixels past the cell (or image)
 // edge are masked out of the labels, the certificate and the sums.
 template <bool ACC, int LPC, bool AL>
-__global__ void __launch_bounds__(128, ACC ? SPX_MINB : SPX_MINB_FIN) k_cell(CellParams p) {
+__global__ void __launch_bounds__(kWarps * 32, (ACC ? SPX_MINB : SPX_MINB_FIN) * 4 / kWarps)
+    k_cell(CellParams p) {
   constexpr int CPW = 32 / LPC;
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1596,7 +1603,7 @@ static int launch_cell_t(const CellParams& p, dim3 blocks, size_t smem, cudaStre
                                   (int)(kWarps * warp_smem(LPC, true))));
     configured.fetch_or(1ull << (dev & 63));
   }
-  k_cell<ACC, LPC, AL><<<blocks, 128, smem, st>>>(p);
+  k_cell<ACC, LPC, AL><<<blocks, kWarps * 32, smem, st>>>(p);
   return SPX_OK;
 }
 
