@@ -1565,33 +1565,32 @@ bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
          h * w * 3 < (int64_t)1 << 40 && h < (1 << 30) && w < (1 << 30);
 }
 
-// Lanes per cell, measured on one B200 (tools/cellbench, random frames;
-// late round 2: 16 1080p frames, fused pass with 2 / 4 lanes): 2 for S <= 10
-// (S = 4: 0.57 vs 0.67 ms, S = 6: 0.45 vs 0.49, S = 8: 0.30 vs 0.32, S = 10:
-// 0.362 vs 0.372), 4 for S = 11, 12 (S = 12: 0.30 vs 0.28), 8 for
-// 13 <= S <= 24 (S = 16: 0.60 vs 0.64 ms per 256 VGA frames), 16 up to 64.
-// Fewer lanes per cell give each lane more runs over which to amortise the
-// per-cell staging and epilogue; too few leave too many cells in flight per
-// warp.  A launch with
+// Lanes per cell (LPC), re-measured after the late round-2 launch shape (one
+// cell group per warp, two-warp blocks) on 16 1080p frames in one launch,
+// fused pass / association-only pass in ms: 2 lanes for S <= 10 (S = 8:
+// 0.284 vs 0.307 with 4), 4 for 11 <= S <= 22 (S = 16: 0.245 vs 0.254 with
+// 8 -- 256 C1 frames with lanes: 4.28 -> 4.14 ms per step), 8 for
+// 23 <= S <= 38 (S = 28: 0.248 vs 0.262 with 4), 32 above (wide-mode
+// association: S = 48: 0.192 vs 0.209 with 16).  Fewer lanes per cell give
+// each lane more runs over which to amortise the per-cell staging and
+// epilogue; too few leave too many cells in flight per warp.  A launch with
 // fewer warps than one resident wave (16 per SM) -- small batches, e.g. one
-// VGA frame is 1,200 cells -- doubles it when every lane still gets >= 2
-// runs: shorter per-lane walks cut the pass latency (one 640x480 frame:
-// 190 -> 170 us per segmentation) while large launches keep the narrower
-// cells (batch 16: LPC 16 is 5% slower).
+// VGA frame is 1,200 cells -- doubles the lanes while every lane still gets
+// >= 2 runs: shorter per-lane walks cut the pass latency.
+#ifndef SPX_LPC_DOUBLINGS
+#define SPX_LPC_DOUBLINGS 3
+#endif
+constexpr int kLpcDoublings = SPX_LPC_DOUBLINGS;
 static int cell_lpc(int64_t s, long long cells) {
   static const int env = getenv("SPX_LPC") ? atoi(getenv("SPX_LPC")) : 0;  // development
   if (s <= 64 && (env == 2 || env == 4 || env == 8 || env == 16 || env == 32)) return env;
-  // S > 64: 32 lanes per cell (the per-lane pixel count must stay <= 2047)
-  int lpc = s <= 10 ? 2 : (s <= 12 ? 4 : (s <= 23 ? 8 : (s <= 64 ? 16 : 32)));
+  // (S > 64: 32 lanes per cell -- the per-lane pixel count must stay <= 2047)
+  int lpc = s <= 10 ? 2 : (s <= 22 ? 4 : (s <= 38 ? 8 : 32));
   const long long runs = s * ceil_div(s, 4);
-  const long long wave = (long long)num_sms() * 16 * 32;  // lanes of one resident wave
-  // large launches at S = 24 and S = 29..32 (16 1080p frames: S = 24 with 16
-  // lanes 0.267 vs 0.281 ms per fused pass; S = 30..32 with 4 lanes 3-9%
-  // faster than 16 or 32)
-  if (s >= 24 && s <= 32 && cells * 16 >= wave) return s >= 29 ? 4 : 16;
-  // up to two doublings (a single 640x480 frame: 8 -> 32 lanes per cell)
-  for (int d = 0; d < 2; ++d)
-    if (lpc < 32 && cells * lpc < wave && runs >= 2 * lpc) lpc *= 2;
+  // small launches: up to SPX_LPC_DOUBLINGS doublings (a single 640x480
+  // frame: 4 -> 32 lanes per cell)
+  for (int d = 0; d < kLpcDoublings; ++d)
+    if (lpc < 32 && cells * lpc < (long long)num_sms() * 16 * 32 && runs >= 2 * lpc) lpc *= 2;
   return lpc;
 }
 
