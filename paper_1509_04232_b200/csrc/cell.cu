@@ -151,10 +151,10 @@ constexpr int kCellWarpsSmall = SPX_CELL_WARPS_SMALL;  // warps per SM a small L
 #define SPX_MINB 4  // resident blocks per SM the register budget is sized for
 #endif
 #ifndef SPX_MINB_FIN
-// the final (no-accumulation) pass: 20 warps per SM (96 registers, a 16-byte
-// spill) -- with cp.async staging it needs fewer live registers; measured
-// 0.449 -> 0.443 ms per 256 C1 frames (24 warps: 0.463)
-#define SPX_MINB_FIN 5
+// the final (no-accumulation) pass: 16 warps per SM like the accumulating
+// one (with 4 lanes per cell at S = 16: 0.434 vs 0.438 ms at 20 warps; with
+// 8 lanes 20 warps had been 1% faster)
+#define SPX_MINB_FIN SPX_MINB
 #endif
 #ifndef SPX_PAIRMIN
 #define SPX_PAIRMIN 1  // top-2 keys merged two candidates at a time (cellbench: -0.8% / -1.6%)
