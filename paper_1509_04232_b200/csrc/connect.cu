@@ -81,7 +81,13 @@ __global__ void __launch_bounds__(WTW* WTH) k_weak1(const int32_t* __restrict__ 
 // second int4 tile, pass 2 group-wise on the output tile.  A group reads its
 // own, the upper and the lower int4 and one word on each side: 5 shared
 // loads per 4 pixels per pass.
-constexpr int WG = 128, HG = 16;  // 128x16 tiles: 21 KB smem, 0.20 ms per 256 C1 frames (32 rows: 0.22)
+#ifndef SPX_WEAK_WG
+#define SPX_WEAK_WG 128
+#endif
+#ifndef SPX_WEAK_HG
+#define SPX_WEAK_HG 16
+#endif
+constexpr int WG = SPX_WEAK_WG, HG = SPX_WEAK_HG;  // 128x16 tiles: 21 KB smem, 0.19 ms per 256 C1 frames (32 rows: 0.22)
 constexpr int NG0 = WG / 4 + 4, R0G = HG + 4;  // source groups: cols [x0-8, x0+WG+8)
 constexpr int NG1 = WG / 4 + 2, R1G = HG + 2;  // pass-1 groups: cols [x0-4, x0+WG+4)
 
