@@ -11,7 +11,8 @@
 #include "../../paper_1509_04232_b200/csrc/spx_internal.cuh"
 
 namespace spx {
-int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t);
+int launch_convert(const uint8_t*, float*, int64_t, int64_t, int, cudaStream_t, int64_t, int64_t,
+                   float);
 int launch_records(const double*, const double*, CRec*, int64_t, int64_t, int64_t, int,
                    cudaStream_t, int64_t, int64_t, int64_t);
 }  // namespace spx
@@ -53,7 +54,7 @@ int main(int argc, char** argv) {
   CC(cudaMalloc(&wl, (B * K + 1) * 4));
   cudaStream_t s = 0;
   k_rand_rgb<<<1184, 256>>>(rgb, B * hw * 3, 12345u);
-  CK(launch_convert(rgb, lab, 0, B * hw, 2, s, hw, S));
+  CK(launch_convert(rgb, lab, 0, B * hw, 2, s, hw, S, -1.f));
   CK(launch_init(lab, H, W, S, ns_c, cxy[0], clab[0], 0, K, K, B, 0, 1, s, 1, -1, 0));
   CK(launch_records(cxy[0], clab[0], rec, ns_r, ns_c, S, B, s, 0, -1, 0));
   CC(cudaMemsetAsync(acc, 0, B * K * sizeof(ClusterAcc), s));
@@ -75,11 +76,11 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   {
-    for (int w = 0; w < 10; ++w) CK(launch_convert(rgb, lab, 0, B * hw, 2, s, hw, S));
+    for (int w = 0; w < 10; ++w) CK(launch_convert(rgb, lab, 0, B * hw, 2, s, hw, S, -1.f));
     std::vector<float> t(reps);
     for (int r = 0; r < reps; ++r) {
       cudaEventRecord(e0, s);
-      CK(launch_convert(rgb, lab, 0, B * hw, 2, s, hw, S));
+      CK(launch_convert(rgb, lab, 0, B * hw, 2, s, hw, S, -1.f));
       cudaEventRecord(e1, s);
       cudaEventSynchronize(e1);
       cudaEventElapsedTime(&t[r], e0, e1);
