@@ -1570,8 +1570,9 @@ bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
 // fused pass / association-only pass in ms: 2 lanes for S <= 10 (S = 8:
 // 0.284 vs 0.307 with 4), 4 for 11 <= S <= 22 (S = 16: 0.245 vs 0.254 with
 // 8 -- 256 C1 frames with lanes: 4.28 -> 4.14 ms per step), 8 for
-// 23 <= S <= 38 (S = 28: 0.248 vs 0.262 with 4), 32 above (wide-mode
-// association: S = 48: 0.192 vs 0.209 with 16).  Fewer lanes per cell give
+// 23 <= S <= 38 (S = 28: 0.248 vs 0.262 with 4), 16 for the accumulating
+// passes of 39 <= S <= 42 (S = 40: 2.79 vs 2.87 ms per call with 32), 32
+// above (wide-mode association: S = 48: 0.192 vs 0.209 with 16).  Fewer lanes per cell give
 // each lane more runs over which to amortise the per-cell staging and
 // epilogue; too few leave too many cells in flight per warp.  A launch with
 // fewer warps than one resident wave (16 per SM) -- small batches, e.g. one
@@ -1585,7 +1586,7 @@ static int cell_lpc(int64_t s, long long cells) {
   static const int env = getenv("SPX_LPC") ? atoi(getenv("SPX_LPC")) : 0;  // development
   if (s <= 64 && (env == 2 || env == 4 || env == 8 || env == 16 || env == 32)) return env;
   // (S > 64: 32 lanes per cell -- the per-lane pixel count must stay <= 2047)
-  int lpc = s <= 10 ? 2 : (s <= 22 ? 4 : (s <= 38 ? 8 : 32));
+  int lpc = s <= 10 ? 2 : (s <= 22 ? 4 : (s <= 38 ? 8 : (s <= 42 ? 16 : 32)));
   const long long runs = s * ceil_div(s, 4);
   // small launches: up to SPX_LPC_DOUBLINGS doublings (a single 640x480
   // frame: 4 -> 32 lanes per cell)
@@ -1627,7 +1628,7 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
                 int32_t* labels, ClusterAcc* sums, const int32_t* done, int64_t h, int64_t w,
                 int64_t s, int64_t ns_r, int64_t ns_c, double xy_weight, int frames, bool acc,
                 cudaStream_t st, int64_t cr0, int64_t cr1, int64_t row_off, int32_t* wl,
-                int32_t* wl_n) {
+                int32_t* wl_n, int conc) {
   CellParams p;
   p.wl = wl;
   p.wl_n = wl_n;
@@ -1657,7 +1658,9 @@ int launch_cell(const float* img, const double* cxy, const double* clab, const C
   p.xy_weight = xy_weight;
   assoc_bound_coefficients(xy_weight, p.w32, p.k_mp, p.k_mc, p.k_xy, p.k_const, p.k_rel);
   if (cr1 <= cr0) return SPX_OK;
-  const int lpc = cell_lpc(s, (cr1 - cr0) * ns_c * (long long)frames);
+  // (conc: launches of this shape running concurrently -- the engine's
+  // lanes -- so the small-launch doubling sees the GPU's real occupancy)
+  const int lpc = cell_lpc(s, (cr1 - cr0) * ns_c * (long long)frames * std::max(1, conc));
   // Walk up to kGroupsPerWarp groups per warp, but keep >= 16 warps per SM
   // in flight for small launches (one 640x480 frame has only 300 groups).
   const long long groups = ceil_div((cr1 - cr0) * ns_c, 32 / lpc) * (long long)frames;
@@ -1707,11 +1710,14 @@ int launch_records(const double* cxy, const double* clab, CRec* rec, int64_t ns_
   return SPX_OK;
 }
 
-// Wide mode for S > 32 (SPX_WIDE=0 keeps the per-cluster certificate and
-// k_exact_wide, for comparison).
+// Wide mode for S > 42 (SPX_WIDE=0 keeps the per-cluster certificate and
+// k_exact_wide, for comparison).  16 1080p frames per call, ms per call,
+// wide vs cluster-level + k_exact_wide: S = 33: 4.01 vs 3.01, 40: 3.24 vs
+// 2.87, 42: 3.34 vs 3.06, 44: 3.48 vs 3.83, 48: 3.10 vs 4.32, 64: 2.70 vs
+// 5.16, 118: 2.73 vs 7.30.
 bool wide_mode(int64_t s, int64_t ns_r, int64_t ns_c) {
   static const bool on = !getenv("SPX_WIDE") || atoi(getenv("SPX_WIDE")) != 0;
-  return on && s > 32 && ns_r * ns_c < ((int64_t)1 << 31);
+  return on && s > 42 && ns_r * ns_c < ((int64_t)1 << 31);
 }
 
 static unsigned strip_tau_bits(int64_t s, int64_t tile_len) {

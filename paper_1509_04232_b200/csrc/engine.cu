@@ -81,7 +81,11 @@ struct Engine {
   cudaStream_t s_side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool use_cell = false;
-  bool wide = false;               // S > 32: per-(cluster, strip) sums (cell.cu)
+  bool wide = false;               // S > 42: per-(cluster, strip) sums (cell.cu)
+  // lanes running beside this engine, for the lanes-per-cell choice (kept
+  // at 1: counting the sibling lanes measured 2-3% faster at S = 34 / 40 but
+  // 12% slower for 16 VGA frames, where the doubled lanes cut latency)
+  int conc = 1;
   // reduce and exact fallback as one launch (SPX_SPLIT_UPDATE=1: two
   // launches on two streams, fork / join)
   bool merged_update = !getenv("SPX_SPLIT_UPDATE");
@@ -325,7 +329,7 @@ struct Engine {
     int rc = use_cell ? launch_cell(lab, cxy[cur], clab[cur], rec, labels, acc, dn, st.height,
                                     st.width, st.s, st.ns_r, st.ns_c, xy_weight, frames,
                                     with_update && !wide, s, 0, -1, 0, worklist,
-                                    wl_n + (pass & 1))
+                                    wl_n + (pass & 1), conc)
                       : launch_assoc(lab, cxy[cur], clab[cur], labels, dn, st.height, st.width,
                                      st.s, st.ns_r, st.ns_c, xy_weight, 0, st.height, frames, K, s);
     stage_mark(pass_event(ev_assoc, 2 * n_assoc + 1), s);
