@@ -1186,7 +1186,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_exact_wide(ReduceParams p) 
   }
 }
 
-// ---- wide cells (S > 32): per-(cluster, strip) sums ------------------------
+// ---- wide cells (S > 42): per-(cluster, strip) sums ------------------------
 //
 // With large cells nearly every cluster has a member outside the certified
 // range 2^k <= |v| < 128 (9 S^2 <= 2^(23+k): S = 118 needs |v| >= 2^-6), so

@@ -236,14 +236,14 @@ def test_cell_path_large_cells_and_odd_frames(s, h, w):
 
 
 @pytest.mark.parametrize("kw", [
-    dict(spixel_size=40),
+    dict(spixel_size=46),
     dict(spixel_size=48, early_stop_threshold=40.0, no_iters=9),
-    dict(spixel_size=36, enable_perturbation=True, tile_len=7),
+    dict(spixel_size=44, enable_perturbation=True, tile_len=7),
     dict(spixel_size=70, connectivity_mode=spx.ConnectivityMode.STRICT, tile_len=30),
-    dict(spixel_size=33, color_space=spx.ColorSpace.XYZ, compactness=3.0),
+    dict(spixel_size=52, color_space=spx.ColorSpace.XYZ, compactness=3.0),
 ])
 def test_wide_mode_batches_graphs_and_lanes(kw):
-    # S > 32 (per-(cluster, strip) sums): a mixed batch through the graph
+    # S > 42 (wide mode, per-(cluster, strip) sums): a mixed batch through the graph
     # replay (calls 3 and 4) and through concurrent lanes, every frame equal
     # to the oracle; early stop, perturbation, strict connectivity, odd tile
     # lengths and XYZ included
