@@ -233,7 +233,13 @@ __device__ __forceinline__ float with_flag(float o0, float o1, float o2, float t
 #define SPX_CONV_MINB 3  // 80 registers, 24 warps per SM (measured ~1% faster than 4 and 6)
 #endif
 template <int SPACE, bool PLANAR>
-__global__ void __launch_bounds__(256, SPX_CONV_MINB) k_convert(const uint8_t* __restrict__ rgb,
+// Threads per convert block.  Late round 2 (256 C1 frames, 4 lanes): 512 x 1
+// block per SM made the convert itself 4% faster (0.70 -> 0.68 ms unsplit)
+// but the laned step 0.3% slower; 128 x 6 within noise.  256 kept.
+#ifndef SPX_CONV_T
+#define SPX_CONV_T 256
+#endif
+__global__ void __launch_bounds__(SPX_CONV_T, SPX_CONV_MINB) k_convert(const uint8_t* __restrict__ rgb,
                                                  float* __restrict__ out, int64_t p0,
                                                  int64_t p1, int vec, int64_t hw, float tau) {
   __shared__ double lut[SPACE == 0 ? 1 : 9 * 256];  // g_mlut (SPACE 1, 2)
@@ -370,13 +376,13 @@ int launch_convert(const uint8_t* rgb, float* out, int64_t p0, int64_t p1, int s
   if (planar) vec = (uintptr_t)rgb % 4 == 0;
   int64_t groups = planar ? (p1 / planar_hw) * ((planar_hw + 3) >> 2)
                           : ((p1 + 3) >> 2) - (p0 >> 2);
-  int64_t blocks = ceil_div(groups, 256);
+  int64_t blocks = ceil_div(groups, SPX_CONV_T);
   int64_t cap = (int64_t)num_sms() * SPX_CONV_BPS;
   if (blocks > cap) blocks = cap;
 #define SPX_CONVERT(SP)                                                                  \
-  (planar ? k_convert<SP, true><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec,  \
+  (planar ? k_convert<SP, true><<<(unsigned)blocks, SPX_CONV_T, 0, st>>>(rgb, out, p0, p1, vec, \
                                                                   planar_hw, tau)         \
-          : k_convert<SP, false><<<(unsigned)blocks, 256, 0, st>>>(rgb, out, p0, p1, vec, 1, \
+          : k_convert<SP, false><<<(unsigned)blocks, SPX_CONV_T, 0, st>>>(rgb, out, p0, p1, vec, 1, \
                                                                    0.f))
   switch (space) {
     case 0: SPX_CONVERT(0); break;
