@@ -1225,14 +1225,21 @@ constexpr int kWideWarpSmem = (kWideAccBytes + 15) & ~15;
 
 // kPx: pixels per lane and cell row, ceil(S / 32); SG: fewer than 3 cluster
 // columns (slots from a division instead of the id offset)
+// Warps per k_strip_acc block (4: 16 3631x3859 frames, S = 118 / 84: 16.8 /
+// 17.6 ms per call; 2: 17.3 / 17.4 -- mixed, 4 kept; more than 4 need the
+// dynamic shared-memory opt-in)
+#ifndef SPX_SACC_WARPS
+#define SPX_SACC_WARPS 4
+#endif
+constexpr int kSaccWarps = SPX_SACC_WARPS;
 template <int kPx, bool SG>
-__global__ void __launch_bounds__(128) k_strip_acc(WideParams p) {
+__global__ void __launch_bounds__(kSaccWarps * 32) k_strip_acc(WideParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int f = blockIdx.y;
   if (p.done && p.done[f] == 1) return;  // whole block: one frame
   const int K = p.ns_r * p.ns_c;
-  const int wid = blockIdx.x * 4 + warp;
+  const int wid = blockIdx.x * kSaccWarps + warp;
   const int cell = wid / p.bands, band = wid - cell * p.bands;
   if (cell >= K) return;  // whole warp
   unsigned char* wb = smem + warp * kWideWarpSmem;
@@ -1771,12 +1778,12 @@ int launch_wide_update(const float* img, const int32_t* labels, StripAcc* sacc, 
     wp.band_rows = (int)ceil_div(s, bands);
     wp.bands = (int)ceil_div(s, wp.band_rows);
   }
-  const dim3 grid((unsigned)ceil_div(K * (long long)wp.bands, 4), (unsigned)frames);
-  const size_t smem = 4 * kWideWarpSmem;
+  const dim3 grid((unsigned)ceil_div(K * (long long)wp.bands, kSaccWarps), (unsigned)frames);
+  const size_t smem = kSaccWarps * kWideWarpSmem;
   const bool sg = ns_c < 3;
 #define SPX_STRIP_ACC(PX)                                        \
-  (sg ? k_strip_acc<PX, true><<<grid, 128, smem, st>>>(wp)       \
-      : k_strip_acc<PX, false><<<grid, 128, smem, st>>>(wp))
+  (sg ? k_strip_acc<PX, true><<<grid, kSaccWarps * 32, smem, st>>>(wp) \
+      : k_strip_acc<PX, false><<<grid, kSaccWarps * 32, smem, st>>>(wp))
   switch ((int)ceil_div(s, 32)) {  // S in (32, 255]
     case 2: SPX_STRIP_ACC(2); break;
     case 3: SPX_STRIP_ACC(3); break;
