@@ -1215,7 +1215,6 @@ struct WideParams {
   int32_t* wl_n;
   int h, w, s, ns_r, ns_c, frames, n_bl, tile_len;
   long long plane;
-  unsigned tau_bits;               // tau_strip
   unsigned long long ns_c_magic;   // ceil(2^64 / ns_c): k / ns_c = umul64hi(k, magic)
   int bands, band_rows;            // k_strip_acc: warps per cell, rows per warp
 };
@@ -1727,13 +1726,6 @@ bool wide_mode(int64_t s, int64_t ns_r, int64_t ns_c) {
   return on && s > 42 && ns_r * ns_c < ((int64_t)1 << 31);
 }
 
-static unsigned strip_tau_bits(int64_t s, int64_t tile_len) {
-  const float tau = strip_tau(s, tile_len);
-  unsigned bits;
-  std::memcpy(&bits, &tau, sizeof bits);
-  return bits;
-}
-
 int launch_wide_update(const float* img, const int32_t* labels, StripAcc* sacc, long long* wl,
                        int32_t* wl_n, const double* prev_xy, const double* prev_lab,
                        double* out_xy, double* out_lab, int64_t* counts, CRec* rec,
@@ -1766,7 +1758,6 @@ int launch_wide_update(const float* img, const int32_t* labels, StripAcc* sacc, 
   wp.n_bl = (int)n_bl;
   wp.tile_len = (int)tile_len;
   wp.plane = plane_of(h * w);
-  wp.tau_bits = strip_tau_bits(s, tile_len);
   // ceil(2^64 / ns_c); ns_c = 1 divides by itself (magic 0 marks it)
   wp.ns_c_magic = ns_c == 1 ? 0ull : ~0ull / (unsigned long long)ns_c + 1ull;
   // small launches split each cell into row bands (one warp each) so that
@@ -1855,11 +1846,7 @@ int launch_reduce_cells(ClusterAcc* acc, const float* img, const int32_t* labels
   p.frames = frames;
   p.plane = plane_of(h * w);
   p.win_staged = exact_win_staged(s);
-  {  // a strip holds <= tile_len * 3S members: tau = 2^k, tile_len*3S <= 2^(23+k)
-    int k = -23;
-    while ((double)tile_len * 3.0 * (double)s > std::ldexp(1.0, 23 + k)) ++k;
-    p.tau_strip = (float)std::ldexp(1.0, k);
-  }
+  p.tau_strip = strip_tau(s, tile_len);  // a strip's certified range (k_exact_wide)
   p.n_bl = (int)ceil_div(3 * s, tile_len);
   p.tile_len = (int)tile_len;
   if (kr1 < 0) kr1 = ns_r;
