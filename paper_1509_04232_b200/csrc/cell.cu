@@ -1,8 +1,9 @@
 // cell.cu -- the engine's fused association + centre-update path.
 //
 // Work unit: one grid cell (S x S pixels).  All pixels of a cell share the
-// same 9 candidate centres, so the cell's LPC lanes (4, 8, 16 or 32 by S)
-// stage the 9 fp32 candidate records in shared memory and stream the cell's
+// same 9 candidate centres, so the cell's LPC lanes (2 to 32 by S and launch
+// size, cell_lpc) stage the 9 fp32 candidate records in shared memory and
+// stream the cell's
 // pixels in runs of 4 (one 128-bit load per planar Lab channel; the final
 // pass stages its runs with cp.async).  Distances are evaluated two pixels
 // at a time with Blackwell's packed FFMA2/FADD2/FMUL2 (the candidate as a
@@ -27,7 +28,10 @@
 // Pixels outside that range carry a flag (sign bit of Lab channel 0, set by
 // the engine's convert); a cluster with a flagged member is queued and
 // recomputed by k_exact_clusters (S <= 32) / k_exact_wide (S > 32) with the
-// reference's strip folds and tree.  k_reduce_cells divides the exact sums.
+// reference's strip folds and tree.  k_reduce_cells divides the exact sums
+// (k_update runs the reduce and k_exact_clusters as one launch).  For
+// S > 42 the engine uses wide mode instead (per-(cluster, strip) sums, see
+// "wide cells" below).
 #include <algorithm>
 #include <atomic>
 #include <cmath>
