@@ -278,15 +278,19 @@ class SegEngine:
         """Per-stage device times (seconds) of the last call, batch-wide
         (`max_updates`: keep only that many update passes and one more
         association, the passes a given frame ran)."""
-        t = self.__dict__.get("_timing_buf")
-        if t is None:
-            t = self._timing_buf = _lib.SpxTiming()
-        _lib.check(self._lib.spx_engine_timing(self._h, ctypes.byref(t)), "timing")
-        ms = 1e-3
+        tb = self.__dict__.get("_timing_buf")
+        if tb is None:
+            t = _lib.SpxTiming()
+            tb = self._timing_buf = (t, ctypes.byref(t))
+        t, ref = tb
+        rc = self._lib.spx_engine_timing(self._h, ref)
+        if rc:
+            _lib.check(rc, "timing")
         na, nu = t.n_associate, t.n_update
         if max_updates is not None:
             nu = min(nu, max_updates)
             na = min(na, max_updates + 1)
+        ms = 1e-3
         return StageTiming(t.convert * ms, t.init * ms, t.perturb * ms,
                            tuple([v * ms for v in t.associate[:na]]),
                            tuple([v * ms for v in t.update[:nu]]),
@@ -368,17 +372,34 @@ class SegEngine:
         results land in a fresh pinned block (one D2H); the call is
         synchronous, as the reference's."""
         self._check_frame(img)
-        pin = self._pinned_input(1)
-        np.copyto(pin[0], img.data)
-        outs, ptrs = self._pinned_outputs_ptrs(1)
-        rc = self._lib.spx_engine_segment_host(self._h, self._pin_in_ptr, 1, *ptrs)
+        fast = self.__dict__.get("_ps_fast")
+        if fast is None:
+            fast = self._ps_fast = self._perform_prepare()
+        pin0, pin_ptr, total, parts = fast
+        np.copyto(pin0, img.data)
+        blk = self._torch.empty((total,), dtype=self._torch.uint8, pin_memory=True).numpy()
+        base = blk.__array_interface__["data"][0]
+        rc = self._lib.spx_engine_segment_host(self._h, pin_ptr, 1, *(base + o for o, _, _ in parts))
         if rc:
             _lib.check(rc, "segment")
-        labels, cxy, clab, counts, passes = outs
+        # one frame's arrays straight on the block (they keep it alive)
+        labels, cxy, clab, counts, passes = (np.ndarray(sh, dt, blk, o) for o, sh, dt in parts)
         tm = self.last_timing(max_updates=int(passes[0]))
-        return SegResult(labels=LabelMap._trusted(labels[0]),
-                         spixel_map=SuperpixelMap._trusted(self.grid, cxy[0], clab[0], counts[0]),
+        return SegResult(labels=LabelMap._trusted(labels),
+                         spixel_map=SuperpixelMap._trusted(self.grid, cxy, clab, counts),
                          timing=tm)
+
+    def _perform_prepare(self):
+        """Per-engine constants of perform_segmentation: the pinned staging
+        frame and its address, and the one-frame result block's layout."""
+        pin = self._pinned_input(1)
+        self._pinned_outputs(1)  # fills the layout cache
+        total, parts = self._layouts[1]
+        st = self.settings
+        k = self.grid.num_clusters
+        shapes = ((st.img_height, st.img_width), (k, 2), (k, 3), (k,), (1,))
+        return (pin[0], self._pin_in_ptr, total,
+                [(o, sh, dt) for (o, _, _, dt), sh in zip(parts, shapes)])
 
     def perform_segmentation_batch(self, imgs):
         """Segment a list of same-sized frames in batches of max_batch."""
