@@ -346,13 +346,6 @@ class SegEngine:
         blk = self._torch.empty((total,), dtype=self._torch.uint8, pin_memory=True).numpy()
         return tuple(blk[o:o + n].view(dt).reshape(sh) for o, n, sh, dt in parts)
 
-    def _pinned_outputs_ptrs(self, b):
-        """_pinned_outputs plus the five host addresses (plain ints: no
-        per-array ctypes objects on the per-frame path)."""
-        outs = self._pinned_outputs(b)
-        base = outs[0].__array_interface__["data"][0]
-        return outs, [base + o for o, _, _, _ in self._layouts[b][1]]
-
     def _pinned_input(self, b):
         """Engine-owned pinned staging for `b` input frames (grown on demand)."""
         st = self.settings
