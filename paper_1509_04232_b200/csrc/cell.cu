@@ -1588,6 +1588,9 @@ bool cell_path_ok(int64_t h, int64_t w, int64_t s, int64_t tile_len) {
 // fewer warps than one resident wave (16 per SM) -- small batches, e.g. one
 // VGA frame is 1,200 cells -- doubles the lanes while every lane still gets
 // >= 2 runs: shorter per-lane walks cut the pass latency.
+#ifndef SPX_LPC_WAVE
+#define SPX_LPC_WAVE 16  // warps per SM below which a launch doubles its lanes (8, 24, 32: slower)
+#endif
 #ifndef SPX_LPC_DOUBLINGS
 #define SPX_LPC_DOUBLINGS 3
 #endif
@@ -1601,7 +1604,8 @@ static int cell_lpc(int64_t s, long long cells) {
   // small launches: up to SPX_LPC_DOUBLINGS doublings (a single 640x480
   // frame: 4 -> 32 lanes per cell)
   for (int d = 0; d < kLpcDoublings; ++d)
-    if (lpc < 32 && cells * lpc < (long long)num_sms() * 16 * 32 && runs >= 2 * lpc) lpc *= 2;
+    if (lpc < 32 && cells * lpc < (long long)num_sms() * SPX_LPC_WAVE * 32 && runs >= 2 * lpc)
+      lpc *= 2;
   return lpc;
 }
 
